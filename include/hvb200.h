@@ -1,0 +1,234 @@
+/*
+ * hvb200.h — C ABI of the B200 hypervector engine (libhvb200.so).
+ *
+ * Drop-in boundary for the hot path of the reference C++ library
+ * "hypervec" (/root/reference/proj). The reference has no FFI of its own: its
+ * boundary is the C++ header API in include/hypervec/{kernels,encoding,model}.hpp.
+ * Every host entry point below replaces exactly one reference function and is
+ * documented with the reference declaration it stands in for (file:line). A
+ * C++ shim (dropin/hypervec_gpu.cpp) re-exposes the original hypervec::
+ * signatures on top of these symbols; INTEGRATION.md shows the ctypes/C++
+ * bindings.
+ *
+ * Conventions
+ *  - Plain pointers and sizes; no C++ or torch types.
+ *  - Packed hypervector matrices use the reference layout verbatim
+ *    (bitmat.hpp:15-32): `rows` x ceil(dim/32) little-endian uint32 words,
+ *    row-major, bit j of a row at word j/32 position j%32, padding bits zero.
+ *  - Dense bit matrices: one byte (0/1) per bit, rows x dim row-major.
+ *  - Labels are int32 (the reference's `int`).
+ *  - `hv_*` entry points take HOST pointers (caller-owned), copy to the
+ *    device, run the sm_100a kernels on the context's stream and copy back
+ *    before returning (synchronous).
+ *  - `hv_dev_*` entry points take DEVICE pointers and only enqueue work on
+ *    the context's stream (asynchronous); data-dependent errors (bad bin,
+ *    bad label, non-binary byte) are latched in the context and reported by
+ *    hv_dev_check().
+ *  - Every call returns an hv_status; the message of the last failure on the
+ *    calling thread is available from hv_last_error(). Status codes map onto
+ *    the reference's exception types:
+ *      HV_ERR_INVALID_ARGUMENT -> std::invalid_argument
+ *      HV_ERR_DOMAIN           -> std::domain_error
+ *      HV_ERR_LOGIC            -> std::logic_error
+ *      HV_ERR_CUDA / HV_ERR_NO_DEVICE -> std::runtime_error
+ *    and invalid_argument messages reproduce the reference's wording.
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point fails with HV_ERR_NO_DEVICE.
+ */
+#ifndef HVB200_H
+#define HVB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HVB200_ABI_VERSION 1
+
+typedef enum hv_status {
+  HV_OK = 0,
+  HV_ERR_INVALID_ARGUMENT = 1,
+  HV_ERR_DOMAIN = 2,
+  HV_ERR_LOGIC = 3,
+  HV_ERR_CUDA = 4,
+  HV_ERR_NO_DEVICE = 5,
+  HV_ERR_RUNTIME = 6
+} hv_status;
+
+/* encoding.hpp:17-18 */
+typedef enum hv_generation { HV_GEN_RANDOM = 0, HV_GEN_SCALE_RANDOM = 1, HV_GEN_SANDWICH = 2 } hv_generation;
+typedef enum hv_binding { HV_BIND_ID_LEVEL = 0, HV_BIND_PERMUTATION = 1, HV_BIND_APPENDING = 2 } hv_binding;
+/* model.hpp:17 */
+typedef enum hv_metric { HV_METRIC_HAMMING = 0, HV_METRIC_COSINE = 1 } hv_metric;
+
+typedef struct hv_context hv_context;
+
+/* ---- library / context ------------------------------------------------ */
+int hv_abi_version(void);
+const char* hv_last_error(void);
+/* bitmat.hpp:30-32 PackedBitMatrix::words_per_row_for */
+size_t hv_words_per_row(size_t dim);
+/* Number of kernels this library has launched in this process (bench evidence). */
+uint64_t hv_kernel_launch_count(void);
+
+hv_status hv_context_create(int device, hv_context** out);
+void hv_context_destroy(hv_context* ctx);
+/* Route hv_dev_* work onto an existing cudaStream_t (NULL = the context's own stream). */
+hv_status hv_context_set_stream(hv_context* ctx, void* cuda_stream);
+void* hv_context_stream(hv_context* ctx);
+hv_status hv_context_synchronize(hv_context* ctx);
+
+/* ---- RNG and codebooks: host code, bit-identical to the reference ------ */
+/* rng.hpp:14-24 */
+uint64_t hv_splitmix64(uint64_t x);
+uint64_t hv_derive_seed(uint64_t seed, uint64_t tag);
+/* encoding.hpp:49-60 (generate_random / generate_scale_random / generate_sandwich);
+ * out: count x ceil(dim/32) words */
+hv_status hv_generate_random(size_t count, size_t dim, uint64_t seed, uint32_t* out);
+hv_status hv_generate_scale_random(size_t bins, size_t dim, uint64_t seed, uint32_t* out);
+hv_status hv_generate_sandwich(size_t bins, size_t dim, uint64_t seed, uint32_t* out);
+/* encoding.hpp:77-79 make_codebook: id_out F x W, value_out B x W */
+hv_status hv_make_codebook(hv_generation generation, size_t features, size_t bins, size_t dim,
+                           uint64_t seed, uint32_t* id_out, uint32_t* value_out);
+
+/* ---- kernels.hpp (host pointers) --------------------------------------- */
+/* kernels.hpp:16-18 pack */
+hv_status hv_pack(hv_context* ctx, const uint8_t* dense, size_t rows, size_t dim, uint32_t* out);
+/* kernels.hpp:20-21 unpack */
+hv_status hv_unpack(hv_context* ctx, const uint32_t* words, size_t rows, size_t dim, uint8_t* out);
+/* kernels.hpp:23-25 xor_bind (b_rows == a_rows or 1 = broadcast) */
+hv_status hv_xor_bind(hv_context* ctx, const uint32_t* a, size_t a_rows, size_t a_dim,
+                      const uint32_t* b, size_t b_rows, size_t b_dim, uint32_t* out);
+/* kernels.hpp:27-29 rotate */
+hv_status hv_rotate(hv_context* ctx, const uint32_t* m, size_t rows, size_t dim, size_t shift,
+                    uint32_t* out);
+/* kernels.hpp:31-32 horizontal_sum */
+hv_status hv_horizontal_sum(hv_context* ctx, const uint32_t* m, size_t rows, size_t dim,
+                            uint64_t* out);
+/* kernels.hpp:34-36 transpose: out is dim x ceil(rows/32) words */
+hv_status hv_transpose(hv_context* ctx, const uint32_t* m, size_t rows, size_t dim, uint32_t* out);
+/* kernels.hpp:38-40 vertical_sum: out has dim counts */
+hv_status hv_vertical_sum(hv_context* ctx, const uint32_t* m, size_t rows, size_t dim,
+                          uint64_t* out);
+/* kernels.hpp:42-46 majority_binarize: tiebreak must be 1 x dim */
+hv_status hv_majority_binarize(hv_context* ctx, const uint64_t* counts, size_t dim, uint64_t n,
+                               const uint32_t* tiebreak, size_t tiebreak_rows,
+                               size_t tiebreak_dim, uint32_t* out);
+
+/* ---- encoding.hpp (host pointers) -------------------------------------- */
+/* encoding.hpp:37-40 fit_discretizer */
+hv_status hv_fit_discretizer(hv_context* ctx, const double* data, size_t rows, size_t features,
+                             size_t bins, double* min_out, double* max_out);
+/* encoding.hpp:45-47 discretize_matrix (discretize = one row) */
+hv_status hv_discretize_matrix(hv_context* ctx, const double* data, size_t rows, size_t features,
+                               const double* min, const double* max, size_t bins, uint32_t* out);
+/* encoding.hpp:81-93 encode / encode_batch. id_vectors F x W, value_vectors B x W,
+ * tiebreak tiebreak_rows x ceil(tiebreak_dim/32) (must be 1 x dim). */
+hv_status hv_encode_batch(hv_context* ctx, const uint32_t* bin_rows, size_t rows, size_t features,
+                          const uint32_t* id_vectors, const uint32_t* value_vectors, size_t bins,
+                          size_t dim, hv_binding binding, const uint32_t* tiebreak,
+                          size_t tiebreak_rows, size_t tiebreak_dim, uint32_t* out);
+
+/* ---- model.hpp (host pointers) ----------------------------------------- */
+/* model.hpp:22-56 ModelConfig + HDModel state; arrays are caller-owned host
+ * memory of the sizes noted. */
+typedef struct hv_model {
+  size_t class_count;
+  size_t dim;
+  hv_metric metric;
+  double gamma;
+  uint64_t seed;
+  double* accumulators;    /* class_count x dim */
+  double* class_weight;    /* class_count */
+  uint64_t* sample_counts; /* class_count */
+  uint32_t* class_vectors; /* class_count x ceil(dim/32) */
+  uint32_t* tiebreak;      /* 1 x ceil(dim/32) */
+} hv_model;
+
+/* model.cpp:198-217 make_empty_model (validates config, fills the arrays) */
+hv_status hv_make_empty_model(hv_model* model);
+/* model.hpp:53-55 HDModel::refresh_binarization (class_index = SIZE_MAX: all) */
+hv_status hv_refresh_binarization(hv_context* ctx, hv_model* model, size_t class_index);
+/* model.hpp:81-82 train_classical (model->dim is set from dim) */
+hv_status hv_train_classical(hv_context* ctx, const uint32_t* encoded, size_t rows, size_t dim,
+                             const int32_t* labels, size_t n_labels, hv_model* model);
+/* model.hpp:97-98 online_update against a frozen snapshot (model.hpp:86-91):
+ * snapshot_class_vectors class_count x W, snapshot_accumulators (cosine only, nullable). */
+hv_status hv_online_update(hv_context* ctx, hv_model* model, const uint32_t* batch, size_t rows,
+                           size_t dim, const int32_t* labels, size_t n_labels,
+                           const uint32_t* snapshot_class_vectors,
+                           const double* snapshot_accumulators);
+/* model.hpp:104-105 train_online */
+hv_status hv_train_online(hv_context* ctx, const uint32_t* encoded, size_t rows, size_t dim,
+                          const int32_t* labels, size_t n_labels, size_t batch_size,
+                          hv_model* model);
+/* model.hpp:110-111 predict: labels_out rows; distances_out rows x class_count (nullable) */
+hv_status hv_predict(hv_context* ctx, const hv_model* model, const uint32_t* encoded,
+                     size_t rows, size_t dim, int32_t* labels_out, double* distances_out);
+/* model.hpp:67-70 hamming_distance_words (host-side helper, no device) */
+double hv_hamming_distance_words(const uint32_t* a, const uint32_t* b, size_t dim);
+
+/* ---- device-resident API (device pointers, async on the context stream) -- */
+/* Latched data errors of earlier hv_dev_* calls (synchronises the stream). */
+hv_status hv_dev_check(hv_context* ctx);
+/* uint32 bins (rows x features) -> validated uint8 bins with row pitch ldb >= features */
+hv_status hv_dev_narrow_bins(hv_context* ctx, const uint32_t* bins32, size_t rows,
+                             size_t features, size_t bins, uint8_t* bins8, size_t ldb);
+/* Encode uint8 bins (row pitch ldb bytes) into rows x W words; bins already validated < bins.
+ * Any binding; id-level takes the fused sm_100a path. */
+hv_status hv_dev_encode(hv_context* ctx, const uint8_t* bins8, size_t ldb, size_t rows,
+                        size_t features, const uint32_t* id_vectors,
+                        const uint32_t* value_vectors, size_t bins, size_t dim,
+                        hv_binding binding, const uint32_t* tiebreak, uint32_t* out);
+/* Classical accumulation: counts (class_count x 32*W uint32, row-major) and
+ * class_rows (class_count uint64) are ADDED to (zero them first); labels validated.
+ * Sharded training calls this per shard and all-reduces counts/class_rows. */
+hv_status hv_dev_class_counts(hv_context* ctx, const uint32_t* encoded, size_t rows, size_t dim,
+                              const int32_t* labels, size_t class_count, uint32_t* counts,
+                              uint64_t* class_rows);
+/* Binarise classical counts: bit = 2c > n ? 1 : 2c < n ? 0 : tiebreak. */
+hv_status hv_dev_binarize_counts(hv_context* ctx, const uint32_t* counts,
+                                 const uint64_t* class_rows, size_t class_count, size_t dim,
+                                 const uint32_t* tiebreak, uint32_t* class_vectors);
+/* Hamming nearest-class scan: labels (int32, nullable), distances (double rows x C,
+ * nullable), popcounts (uint32 rows x C, nullable). */
+hv_status hv_dev_predict_hamming(hv_context* ctx, const uint32_t* class_vectors,
+                                 size_t class_count, size_t dim, const uint32_t* encoded,
+                                 size_t rows, int32_t* labels, double* distances,
+                                 uint32_t* popcounts);
+/* Online training on device-resident state. acc: C x dim doubles, weight: C doubles,
+ * counts: C uint64, class_vectors: C x W, tiebreak: 1 x W. Exact reference
+ * semantics (sample-ordered in-place fp64 adds, snapshot per batch, bootstrap
+ * batch visited twice). */
+hv_status hv_dev_train_online(hv_context* ctx, const uint32_t* encoded, size_t rows, size_t dim,
+                              const int32_t* labels, size_t class_count, size_t batch_size,
+                              double gamma, const uint32_t* tiebreak, double* acc,
+                              double* weight, uint64_t* counts, uint32_t* class_vectors);
+/* One online batch in delta mode for data-parallel training: computes, against the
+ * given (replicated) class vectors, this shard's per-class updates
+ * delta_acc (C x dim, overwritten), delta_weight (C), delta_counts (C); the caller
+ * all-reduces them and applies hv_dev_apply_online_delta. */
+hv_status hv_dev_online_delta(hv_context* ctx, const uint32_t* class_vectors, size_t class_count,
+                              size_t dim, const uint32_t* batch, size_t rows,
+                              const int32_t* labels, double gamma, double* delta_acc,
+                              double* delta_weight, uint64_t* delta_counts,
+                              uint32_t* delta_touched);
+/* acc += delta_acc; weight += delta_weight; counts += delta_counts; re-binarise the
+ * classes with touched[c] != 0 (model.cpp:277-279). */
+hv_status hv_dev_apply_online_delta(hv_context* ctx, size_t class_count, size_t dim,
+                                    const double* delta_acc, const double* delta_weight,
+                                    const uint64_t* delta_counts, const uint32_t* touched,
+                                    const uint32_t* tiebreak, double* acc, double* weight,
+                                    uint64_t* counts, uint32_t* class_vectors);
+/* Synthetic workload (include/hvb200_synth.h) generated on device for rows
+ * [row0, row0+rows): bins8 (pitch ldb) and labels. */
+hv_status hv_dev_synth(hv_context* ctx, uint64_t row0, size_t rows, size_t features,
+                       size_t class_count, size_t bins, int label_kind, uint64_t seed,
+                       uint8_t* bins8, size_t ldb, int32_t* labels);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HVB200_H */

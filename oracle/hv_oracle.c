@@ -535,3 +535,20 @@ int hvo_predict(const hvo_model* m, const uint8_t* encoded, size_t rows, int32_t
   free(scores);
   return status;
 }
+
+/* ======================================================================= */
+/* Bench workload generator (include/hvb200_synth.h), exposed so tests can  */
+/* pin the Python restatement and the device generator against it.         */
+/* ======================================================================= */
+#include "../include/hvb200_synth.h"
+
+void hvo_synth(uint64_t row0, size_t rows, size_t features, size_t classes, size_t bins, int kind,
+               uint64_t seed, uint32_t* bins_out, int32_t* labels_out) {
+  for (size_t r = 0; r < rows; ++r) {
+    const int32_t y = hvs_label(row0 + r, (uint32_t)classes, kind);
+    labels_out[r] = y;
+    for (size_t f = 0; f < features; ++f) {
+      bins_out[r * features + f] = hvs_bin(row0 + r, (uint32_t)f, (uint32_t)features, y, (uint32_t)bins, seed);
+    }
+  }
+}

@@ -1,0 +1,858 @@
+// hv_model.cu — classical trainer, online trainer and nearest-class scan
+// (reference model.cpp:24-320).
+//
+// Classical training (model.cpp:219-244) is a per-class vertical bit count:
+// rows are bucketed by label with a warp-aggregated counting sort, then the
+// shared column-count kernel streams each class's rows once (Harley–Seal
+// counters, HBM bound). Counts are exact uint32; accumulators are their
+// double values, exactly like the reference.
+//
+// Online training (model.cpp:250-301) must reproduce fp64 rounding exactly.
+// The reference adds each sample's weight into acc[class][j] in place, in
+// sample order. Here every (class, position) element is owned by one thread
+// that walks the class's ordered update list for the batch, so each element
+// sees the same sequence of IEEE additions (__dadd_rn, no contraction) and
+// the result is bit-identical. Scores of a batch are computed against the
+// batch-start class vectors (the snapshot, model.cpp:246-248) before any
+// update of that batch is applied.
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <vector>
+
+#include "hv_internal.cuh"
+
+namespace hvb {
+
+constexpr uint32_t FULL = 0xFFFFFFFFu;
+
+// ------------------------------------------------- label bucketing ----
+// model.cpp:24-37 check_labels (range), plus per-class histogram.
+__global__ void label_hist_kernel(const int32_t* __restrict__ y, uint64_t n, uint32_t C, uint32_t* __restrict__ hist,
+                                  unsigned long long* err) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+    const uint64_t i = base + lane;
+    const bool valid = i < n;
+    const int32_t lab = valid ? y[i] : -1;
+    const bool ok = valid && lab >= 0 && static_cast<uint32_t>(lab) < C;
+    if (valid && !ok) latch(err, kErrLabel, i);
+    const uint32_t mask = __match_any_sync(FULL, ok ? lab : -1);
+    if (ok && lane == static_cast<uint32_t>(__ffs(mask) - 1)) atomicAdd(hist + lab, __popc(mask));
+  }
+}
+
+__global__ void label_scan_kernel(const uint32_t* __restrict__ hist, uint32_t C, uint64_t* __restrict__ offsets,
+                                  uint64_t* __restrict__ class_rows, uint32_t* __restrict__ cursor) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint64_t acc = 0;
+  for (uint32_t c = 0; c < C; ++c) {
+    offsets[c] = acc;
+    acc += hist[c];
+    if (class_rows) class_rows[c] += hist[c];
+    cursor[c] = 0;
+  }
+  offsets[C] = acc;
+}
+
+__global__ void label_scatter_kernel(const int32_t* __restrict__ y, uint64_t n, uint32_t C,
+                                     const uint64_t* __restrict__ offsets, uint32_t* __restrict__ cursor,
+                                     uint32_t* __restrict__ perm) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+    const uint64_t i = base + lane;
+    const bool valid = i < n;
+    const int32_t lab = valid ? y[i] : -1;
+    const bool ok = valid && lab >= 0 && static_cast<uint32_t>(lab) < C;
+    const uint32_t mask = __match_any_sync(FULL, ok ? lab : -1);
+    const uint32_t leader = __ffs(mask) - 1;
+    uint32_t start = 0;
+    if (ok && lane == leader) start = atomicAdd(cursor + lab, __popc(mask));
+    start = __shfl_sync(FULL, start, leader);
+    if (ok) {
+      const uint32_t rank = __popc(mask & ((1u << lane) - 1u));
+      perm[offsets[lab] + start + rank] = static_cast<uint32_t>(i);
+    }
+  }
+}
+
+// bit = 2c > n ? 1 : 2c < n ? 0 : tie   (model.cpp:139-163 with acc = count, weight = n)
+__global__ void binarize_counts_kernel(const uint32_t* __restrict__ counts, const uint64_t* __restrict__ class_rows,
+                                       uint32_t C, uint32_t D, uint32_t W, const uint32_t* __restrict__ tie,
+                                       uint32_t* __restrict__ cv) {
+  const uint64_t total = static_cast<uint64_t>(C) * W;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = static_cast<uint32_t>(i / W);
+    const uint32_t w = static_cast<uint32_t>(i % W);
+    const uint64_t n = class_rows[c];
+    const uint32_t* cc = counts + static_cast<uint64_t>(c) * 32u * W + 32u * w;
+    const uint32_t tw = tie[w];
+    uint32_t word = 0;
+#pragma unroll 8
+    for (int t = 0; t < 32; ++t) {
+      const uint64_t twice = 2ull * cc[t];
+      const uint32_t bit = twice > n ? 1u : (twice < n ? 0u : ((tw >> t) & 1u));
+      word |= bit << t;
+    }
+    cv[i] = word & valid_mask(w, D);
+  }
+}
+
+// acc[c][j] = double(count), weight = count = rows of class c
+__global__ void init_from_counts_kernel(const uint32_t* __restrict__ counts, const uint64_t* __restrict__ class_rows,
+                                        uint32_t C, uint32_t D, uint32_t W, double* __restrict__ acc,
+                                        double* __restrict__ weight, uint64_t* __restrict__ cnt) {
+  const uint64_t total = static_cast<uint64_t>(C) * D;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = i / D;
+    const uint64_t j = i % D;
+    acc[i] = static_cast<double>(counts[c * 32ull * W + j]);
+    if (j == 0) {
+      weight[c] = static_cast<double>(class_rows[c]);
+      cnt[c] = class_rows[c];
+    }
+  }
+}
+
+// model.cpp:139-163 for the classes with touched[c] != 0 (or all when touched == nullptr)
+__global__ void refresh_kernel(const double* __restrict__ acc, const double* __restrict__ weight,
+                               const uint32_t* __restrict__ touched, uint32_t C, uint32_t D, uint32_t W,
+                               const uint32_t* __restrict__ tie, uint32_t* __restrict__ cv) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t warps_total = static_cast<uint64_t>(C) * W;
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t t = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < warps_total; t += stride) {
+    const uint32_t c = static_cast<uint32_t>(t / W);
+    const uint32_t w = static_cast<uint32_t>(t % W);
+    if (touched && touched[c] == 0) continue;
+    const uint32_t j = w * 32u + lane;
+    uint32_t bit = 0;
+    if (j < D) {
+      const double twice = 2.0 * acc[static_cast<uint64_t>(c) * D + j];
+      const double total = weight[c];
+      bit = twice > total ? 1u : (twice < total ? 0u : ((tie[w] >> lane) & 1u));
+    }
+    const uint32_t word = __ballot_sync(FULL, bit);
+    if (lane == 0) cv[t] = word;
+  }
+}
+
+// ------------------------------------------------------ Hamming scan ----
+// model.cpp:303-320 + 69-79 + 96-104: one warp per query row, C popcounts of
+// row ^ class_vector reduced with REDUX; argmin with strict < (lowest class
+// wins ties). Integer popcounts order exactly like popc/D doubles.
+template <int CB>
+__global__ void __launch_bounds__(256) predict_hamming_kernel(const uint32_t* __restrict__ cv, uint32_t C, uint32_t D,
+                                                              uint32_t W, const uint32_t* __restrict__ enc,
+                                                              uint64_t rows, int32_t* __restrict__ labels,
+                                                              double* __restrict__ dist, uint32_t* __restrict__ pops) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += stride) {
+    const uint32_t* q = enc + r * W;
+    uint32_t best = 0, bestp = 0xFFFFFFFFu;
+    for (uint32_t c0 = 0; c0 < C; c0 += CB) {
+      uint32_t acc[CB];
+#pragma unroll
+      for (int k = 0; k < CB; ++k) acc[k] = 0;
+      for (uint32_t w = lane; w < W; w += 32u) {
+        const uint32_t x = q[w];
+#pragma unroll
+        for (int k = 0; k < CB; ++k) {
+          if (c0 + k < C) acc[k] += __popc(x ^ cv[static_cast<uint64_t>(c0 + k) * W + w]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < CB; ++k) {
+        const uint32_t tot = __reduce_add_sync(FULL, acc[k]);
+        const uint32_t c = c0 + k;
+        if (c < C) {
+          if (tot < bestp) {
+            bestp = tot;
+            best = c;
+          }
+          if (lane == (c & 31u)) {
+            if (pops) pops[r * C + c] = tot;
+            if (dist) dist[r * C + c] = static_cast<double>(tot) / static_cast<double>(D);
+          }
+        }
+      }
+    }
+    if (lane == 0 && labels) labels[r] = static_cast<int32_t>(best);
+  }
+}
+
+// ------------------------------------------------------- cosine scan ----
+// model.cpp:80-93, 40-51: exact sequential fp64 like the reference —
+// norm_sq = sum_j acc^2 in j order; dot = sum over set bits in increasing j.
+__global__ void class_norms_kernel(const double* __restrict__ acc, uint32_t C, uint32_t D, double* __restrict__ norm) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double* a = acc + static_cast<uint64_t>(c) * D;
+  double s = 0.0;
+  for (uint32_t j = 0; j < D; ++j) s = __dadd_rn(s, __dmul_rn(a[j], a[j]));
+  norm[c] = s;
+}
+
+// one thread per (row, class): score = dot / (sqrt(norm) * sqrt(ones)), -inf for empty class
+__global__ void cosine_scores_kernel(const double* __restrict__ acc, const double* __restrict__ norm, uint32_t C,
+                                     uint32_t D, uint32_t W, const uint32_t* __restrict__ enc, uint64_t rows,
+                                     double* __restrict__ scores, unsigned long long* err, uint64_t err_base) {
+  const uint64_t total = rows * C;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = i / C;
+    const uint32_t c = static_cast<uint32_t>(i % C);
+    const uint32_t* q = enc + r * W;
+    uint32_t ones = 0;
+    for (uint32_t w = 0; w < W; ++w) ones += __popc(q[w]);
+    if (ones == 0) {
+      latch(err, kErrZeroQuery, err_base + r);
+      scores[i] = 0.0;
+      continue;
+    }
+    const double ns = norm[c];
+    if (ns == 0.0) {
+      scores[i] = -__longlong_as_double(0x7FF0000000000000ll);
+      continue;
+    }
+    const double* a = acc + static_cast<uint64_t>(c) * D;
+    double dot = 0.0;
+    for (uint32_t w = 0; w < W; ++w) {
+      uint32_t bits = q[w];
+      while (bits) {
+        const uint32_t t = __ffs(bits) - 1;
+        dot = __dadd_rn(dot, a[w * 32u + t]);
+        bits &= bits - 1;
+      }
+    }
+    scores[i] = __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(ns), __dsqrt_rn(static_cast<double>(ones))));
+  }
+}
+
+// argmax with strict > (model.cpp:96-104), one thread per row
+__global__ void argmax_kernel(const double* __restrict__ scores, uint64_t rows, uint32_t C, int32_t* __restrict__ labels) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows; r += (uint64_t)gridDim.x * blockDim.x) {
+    const double* s = scores + r * C;
+    uint32_t best = 0;
+    for (uint32_t c = 1; c < C; ++c) {
+      if (s[c] > s[best]) best = c;
+    }
+    labels[r] = static_cast<int32_t>(best);
+  }
+}
+
+// ------------------------------------------------------------ online ----
+// Per-sample scoring of one batch against the snapshot (model.cpp:259-265):
+// predicted label, delta_true and the wrong-class penalty -gamma*(1-delta_wrong).
+__global__ void online_score_hamming_kernel(const uint32_t* __restrict__ cv, uint32_t C, uint32_t D, uint32_t W,
+                                            const uint32_t* __restrict__ batch, uint64_t rows,
+                                            const int32_t* __restrict__ labels, double gamma,
+                                            int32_t* __restrict__ pred, double* __restrict__ dtrue,
+                                            double* __restrict__ pen) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += stride) {
+    const uint32_t* q = batch + r * W;
+    const int32_t y = labels[r];
+    uint32_t best = 0, bestp = 0xFFFFFFFFu, truep = 0;
+    for (uint32_t c = 0; c < C; ++c) {
+      uint32_t a = 0;
+      for (uint32_t w = lane; w < W; w += 32u) a += __popc(q[w] ^ cv[static_cast<uint64_t>(c) * W + w]);
+      a = __reduce_add_sync(FULL, a);
+      if (a < bestp) {
+        bestp = a;
+        best = c;
+      }
+      if (static_cast<int32_t>(c) == y) truep = a;
+    }
+    if (lane == 0) {
+      pred[r] = static_cast<int32_t>(best);
+      dtrue[r] = static_cast<double>(truep) / static_cast<double>(D);
+      const double dw = static_cast<double>(bestp) / static_cast<double>(D);
+      pen[r] = __dmul_rn(-gamma, __dsub_rn(1.0, dw));
+    }
+  }
+}
+
+// Cosine variant: scores already computed (rows x C); model.cpp:109-113 score_to_delta.
+__global__ void online_score_cosine_kernel(const double* __restrict__ scores, uint32_t C, uint64_t rows,
+                                           const int32_t* __restrict__ labels, double gamma,
+                                           int32_t* __restrict__ pred, double* __restrict__ dtrue,
+                                           double* __restrict__ pen) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows; r += (uint64_t)gridDim.x * blockDim.x) {
+    const double* s = scores + r * C;
+    uint32_t best = 0;
+    for (uint32_t c = 1; c < C; ++c) {
+      if (s[c] > s[best]) best = c;
+    }
+    auto to_delta = [](double v) { return isinf(v) ? 1.0 : __ddiv_rn(__dsub_rn(1.0, v), 2.0); };
+    pred[r] = static_cast<int32_t>(best);
+    dtrue[r] = to_delta(s[labels[r]]);
+    pen[r] = __dmul_rn(-gamma, __dsub_rn(1.0, to_delta(s[best])));
+  }
+}
+
+// One warp per class: the ordered list of (sample, value) updates hitting the
+// class in this batch, and the class weight advanced in sample order
+// (model.cpp:266-274). weight_out/counts_out are updated in place (delta
+// mode passes zeroed arrays).
+__global__ void online_lists_kernel(const int32_t* __restrict__ labels, const int32_t* __restrict__ pred,
+                                    const double* __restrict__ dtrue, const double* __restrict__ pen, uint64_t rows,
+                                    uint32_t C, uint32_t cap, uint32_t* __restrict__ idx, double* __restrict__ val,
+                                    uint32_t* __restrict__ len, double* __restrict__ weight,
+                                    uint64_t* __restrict__ counts, uint32_t* __restrict__ touched) {
+  const uint32_t c = blockIdx.x;
+  const uint32_t lane = threadIdx.x;
+  if (c >= C) return;
+  uint32_t n = 0, ntrue = 0;
+  double wsum = weight[c];
+  for (uint64_t i0 = 0; i0 < rows; i0 += 32) {
+    const uint64_t i = i0 + lane;
+    const bool valid = i < rows;
+    const int32_t y = valid ? labels[i] : -1;
+    const int32_t p = valid ? pred[i] : -1;
+    const bool is_true = y == static_cast<int32_t>(c);
+    const bool is_pen = !is_true && p == static_cast<int32_t>(c);
+    const double dt = is_true ? dtrue[i] : 0.0;
+    const uint32_t m = __ballot_sync(FULL, is_true || is_pen);
+    if (is_true || is_pen) {
+      const uint32_t pos = n + __popc(m & ((1u << lane) - 1u));
+      idx[static_cast<uint64_t>(c) * cap + pos] = static_cast<uint32_t>(i);
+      val[static_cast<uint64_t>(c) * cap + pos] = is_true ? dt : pen[i];
+    }
+    n += __popc(m);
+    uint32_t mt = __ballot_sync(FULL, is_true);
+    ntrue += __popc(mt);
+    while (mt) {
+      const int l = __ffs(mt) - 1;
+      wsum = __dadd_rn(wsum, __shfl_sync(FULL, dt, l));
+      mt &= mt - 1;
+    }
+  }
+  if (lane == 0) {
+    len[c] = n;
+    weight[c] = wsum;
+    counts[c] += ntrue;
+    if (touched) touched[c] = n ? 1u : 0u;
+  }
+}
+
+// Thread (class c, position j) replays the class's update list in order:
+// acc += value for every listed sample with bit j set (model.cpp:54-63). In
+// exact mode the element is updated in place and the class re-binarised; in
+// delta mode it starts from 0.0 and only the delta is written.
+template <bool DELTA>
+__global__ void __launch_bounds__(256) online_update_kernel(const uint32_t* __restrict__ batch, uint32_t D, uint32_t W,
+                                                            uint32_t cap, const uint32_t* __restrict__ idx,
+                                                            const double* __restrict__ val,
+                                                            const uint32_t* __restrict__ len,
+                                                            const double* __restrict__ weight,
+                                                            const uint32_t* __restrict__ tie, double* __restrict__ acc,
+                                                            uint32_t* __restrict__ cv) {
+  const uint32_t c = blockIdx.y;
+  const uint32_t n = len[c];
+  if (n == 0) return;
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = j < D;
+  const uint32_t wi = min(j >> 5, W - 1);
+  const uint32_t sh = j & 31u;
+  double a = (!DELTA && valid) ? acc[static_cast<uint64_t>(c) * D + j] : 0.0;
+  const uint32_t* li = idx + static_cast<uint64_t>(c) * cap;
+  const double* lv = val + static_cast<uint64_t>(c) * cap;
+  uint32_t k = 0;
+  for (; k + 4 <= n; k += 4) {
+    uint32_t wd[4];
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      wd[u] = batch[static_cast<uint64_t>(li[k + u]) * W + wi];
+      v[u] = lv[k + u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if ((wd[u] >> sh) & 1u) a = __dadd_rn(a, v[u]);
+    }
+  }
+  for (; k < n; ++k) {
+    const uint32_t wd = batch[static_cast<uint64_t>(li[k]) * W + wi];
+    if ((wd >> sh) & 1u) a = __dadd_rn(a, lv[k]);
+  }
+  if (valid) acc[static_cast<uint64_t>(c) * D + j] = a;
+  if (!DELTA) {
+    uint32_t bit = 0;
+    if (valid) {
+      const double twice = 2.0 * a;
+      const double total = weight[c];
+      bit = twice > total ? 1u : (twice < total ? 0u : ((tie[wi] >> sh) & 1u));
+    }
+    const uint32_t word = __ballot_sync(FULL, bit);
+    if ((threadIdx.x & 31u) == 0 && (j >> 5) < W) cv[static_cast<uint64_t>(c) * W + (j >> 5)] = word;
+  }
+}
+
+__global__ void apply_delta_scalars_kernel(uint32_t C, const double* __restrict__ dw, const uint64_t* __restrict__ dc,
+                                           double* __restrict__ weight, uint64_t* __restrict__ counts) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  weight[c] = __dadd_rn(weight[c], dw[c]);
+  counts[c] += dc[c];
+}
+
+__global__ void apply_delta_acc_kernel(uint64_t n, const double* __restrict__ d, double* __restrict__ acc) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    acc[i] = __dadd_rn(acc[i], d[i]);
+  }
+}
+
+// ------------------------------------------------------ host helpers ----
+unsigned sgrid(hv_context* ctx, uint64_t items, unsigned block, unsigned per_sm = 16) {
+  const uint64_t want = (items + block - 1) / block;
+  const uint64_t cap = static_cast<uint64_t>(ctx->sm_count) * per_sm;
+  return static_cast<unsigned>(want == 0 ? 1 : std::min(want, cap));
+}
+
+// class counts of `rows` encoded rows into counts (C x 32W, added) and class_rows (added)
+void class_counts_device(hv_context* ctx, cudaStream_t st, const uint32_t* enc, size_t rows, size_t W,
+                         const int32_t* labels, size_t C, uint32_t* counts, uint64_t* class_rows) {
+  if (rows == 0) return;
+  DevBuf<uint32_t> hist(C, st), cursor(C, st), perm(rows, st);
+  DevBuf<uint64_t> offsets(C + 1, st);
+  hist.zero();
+  label_hist_kernel<<<sgrid(ctx, rows, 256), 256, 0, st>>>(labels, rows, static_cast<uint32_t>(C), hist.ptr, ctx->d_err);
+  launched("label_hist_kernel");
+  label_scan_kernel<<<1, 32, 0, st>>>(hist.ptr, static_cast<uint32_t>(C), offsets.ptr, class_rows, cursor.ptr);
+  launched("label_scan_kernel");
+  label_scatter_kernel<<<sgrid(ctx, rows, 256), 256, 0, st>>>(labels, rows, static_cast<uint32_t>(C), offsets.ptr,
+                                                             cursor.ptr, perm.ptr);
+  launched("label_scatter_kernel");
+  launch_column_count_u32(st, enc, static_cast<uint32_t>(W), perm.ptr, offsets.ptr, static_cast<uint32_t>(C), rows,
+                          counts);
+}
+
+void binarize_counts_device(hv_context* ctx, cudaStream_t st, const uint32_t* counts, const uint64_t* class_rows,
+                            size_t C, size_t D, const uint32_t* tie, uint32_t* cv) {
+  const size_t W = words_per_row(D);
+  binarize_counts_kernel<<<sgrid(ctx, C * W, 128), 128, 0, st>>>(counts, class_rows, static_cast<uint32_t>(C),
+                                                                static_cast<uint32_t>(D), static_cast<uint32_t>(W), tie,
+                                                                cv);
+  launched("binarize_counts_kernel");
+}
+
+void predict_hamming_device(hv_context* ctx, cudaStream_t st, const uint32_t* cv, size_t C, size_t D,
+                            const uint32_t* enc, size_t rows, int32_t* labels, double* dist, uint32_t* pops) {
+  if (rows == 0) return;
+  const size_t W = words_per_row(D);
+  const unsigned grid = sgrid(ctx, rows * 32, 256, 8);
+  if (C <= 2) {
+    predict_hamming_kernel<2><<<grid, 256, 0, st>>>(cv, C, D, W, enc, rows, labels, dist, pops);
+  } else if (C <= 4) {
+    predict_hamming_kernel<4><<<grid, 256, 0, st>>>(cv, C, D, W, enc, rows, labels, dist, pops);
+  } else {
+    predict_hamming_kernel<8><<<grid, 256, 0, st>>>(cv, C, D, W, enc, rows, labels, dist, pops);
+  }
+  launched("predict_hamming_kernel");
+}
+
+void cosine_scores_device(hv_context* ctx, cudaStream_t st, const double* acc, size_t C, size_t D, const uint32_t* enc,
+                          size_t rows, double* scores, uint64_t err_base) {
+  const size_t W = words_per_row(D);
+  DevBuf<double> norm(C, st);
+  class_norms_kernel<<<grid_for(C, 64), 64, 0, st>>>(acc, C, D, norm.ptr);
+  launched("class_norms_kernel");
+  if (rows == 0) return;
+  cosine_scores_kernel<<<sgrid(ctx, rows * C, 128, 64), 128, 0, st>>>(acc, norm.ptr, C, D, W, enc, rows, scores,
+                                                                      ctx->d_err, err_base);
+  launched("cosine_scores_kernel");
+}
+
+void refresh_device(hv_context* ctx, cudaStream_t st, const double* acc, const double* weight, const uint32_t* touched,
+                    size_t C, size_t D, const uint32_t* tie, uint32_t* cv) {
+  const size_t W = words_per_row(D);
+  refresh_kernel<<<sgrid(ctx, C * W * 32, 256), 256, 0, st>>>(acc, weight, touched, C, D, W, tie, cv);
+  launched("refresh_kernel");
+}
+
+// Scratch for one online batch.
+struct OnlineScratch {
+  DevBuf<int32_t> pred;
+  DevBuf<double> dtrue, pen, val, scores;
+  DevBuf<uint32_t> idx, len;
+  size_t cap;
+  OnlineScratch(size_t C, size_t cap_, bool cosine, cudaStream_t st)
+      : pred(cap_, st), dtrue(cap_, st), pen(cap_, st), val(C * cap_, st), scores(cosine ? C * cap_ : 0, st),
+        idx(C * cap_, st), len(C, st), cap(cap_) {}
+};
+
+// One online batch (exact or delta) on device-resident state.
+template <bool DELTA>
+void online_batch(hv_context* ctx, cudaStream_t st, OnlineScratch& s, hv_metric metric, const uint32_t* snap_cv,
+                  const double* snap_acc, size_t C, size_t D, const uint32_t* batch, size_t rows, const int32_t* labels,
+                  double gamma, const uint32_t* tie, double* acc, double* weight, uint64_t* counts, uint32_t* cv,
+                  uint32_t* touched) {
+  if (rows == 0) return;
+  const size_t W = words_per_row(D);
+  if (metric == HV_METRIC_HAMMING) {
+    online_score_hamming_kernel<<<sgrid(ctx, rows * 32, 256, 8), 256, 0, st>>>(
+        snap_cv, C, D, W, batch, rows, labels, gamma, s.pred.ptr, s.dtrue.ptr, s.pen.ptr);
+    launched("online_score_hamming_kernel");
+  } else {
+    cosine_scores_device(ctx, st, snap_acc, C, D, batch, rows, s.scores.ptr, 0);
+    online_score_cosine_kernel<<<sgrid(ctx, rows, 128), 128, 0, st>>>(s.scores.ptr, C, rows, labels, gamma, s.pred.ptr,
+                                                                      s.dtrue.ptr, s.pen.ptr);
+    launched("online_score_cosine_kernel");
+  }
+  online_lists_kernel<<<C, 32, 0, st>>>(labels, s.pred.ptr, s.dtrue.ptr, s.pen.ptr, rows, C, s.cap, s.idx.ptr,
+                                        s.val.ptr, s.len.ptr, weight, counts, touched);
+  launched("online_lists_kernel");
+  dim3 grid((D + 255) / 256, C);
+  online_update_kernel<DELTA><<<grid, 256, 0, st>>>(batch, D, W, s.cap, s.idx.ptr, s.val.ptr, s.len.ptr, weight, tie,
+                                                    acc, cv);
+  launched("online_update_kernel");
+}
+
+void train_online_device(hv_context* ctx, cudaStream_t st, hv_metric metric, const uint32_t* enc, size_t rows, size_t D,
+                         const int32_t* labels, size_t C, size_t bsz, double gamma, const uint32_t* tie, double* acc,
+                         double* weight, uint64_t* counts, uint32_t* cv) {
+  const size_t W = words_per_row(D);
+  const size_t first = std::min(bsz, rows);
+  {
+    DevBuf<uint32_t> cnt(C * 32 * W, st);
+    DevBuf<uint64_t> crow(C, st);
+    cnt.zero();
+    crow.zero();
+    class_counts_device(ctx, st, enc, first, W, labels, C, cnt.ptr, crow.ptr);
+    init_from_counts_kernel<<<sgrid(ctx, C * D, 256), 256, 0, st>>>(cnt.ptr, crow.ptr, C, D, W, acc, weight, counts);
+    launched("init_from_counts_kernel");
+    binarize_counts_device(ctx, st, cnt.ptr, crow.ptr, C, D, tie, cv);
+  }
+  if (rows == 0) return;
+  OnlineScratch s(C, std::min(bsz, rows), metric == HV_METRIC_COSINE, st);
+  DevBuf<double> snap(metric == HV_METRIC_COSINE ? C * D : 0, st);
+  for (size_t start = 0; start < rows; start += bsz) {
+    const size_t n = std::min(bsz, rows - start);
+    const double* snap_acc = nullptr;
+    if (metric == HV_METRIC_COSINE) {
+      ck(cudaMemcpyAsync(snap.ptr, acc, C * D * sizeof(double), cudaMemcpyDeviceToDevice, st), "snapshot");
+      snap_acc = snap.ptr;
+    }
+    // The class vectors are only rewritten by the update kernel after every
+    // score of this batch has been computed, so `cv` itself is the snapshot.
+    online_batch<false>(ctx, st, s, metric, cv, snap_acc, C, D, enc + start * W, n, labels + start, gamma, tie, acc,
+                        weight, counts, cv, nullptr);
+  }
+}
+
+void check_labels_host(const int32_t* labels, size_t n_labels, size_t rows, size_t C, const char* who) {
+  if (n_labels != rows) {
+    invalid(std::string(who) + ": " + std::to_string(n_labels) + " labels for " + std::to_string(rows) + " rows");
+  }
+  for (size_t i = 0; i < n_labels; ++i) {
+    if (labels[i] < 0 || static_cast<size_t>(labels[i]) >= C) {
+      invalid(std::string(who) + ": label " + std::to_string(labels[i]) + " at row " + std::to_string(i) +
+              " out of range (classes = " + std::to_string(C) + ")");
+    }
+  }
+}
+
+void check_model_config(const hv_model* m) {
+  if (m == nullptr) invalid("null hv_model");
+  if (m->class_count == 0) invalid("make_empty_model: need at least one class");
+  if (m->dim == 0) invalid("make_empty_model: dim must be >= 1");
+  if (m->gamma < 0.0) invalid("make_empty_model: gamma must be >= 0");
+  if (m->metric != HV_METRIC_HAMMING && m->metric != HV_METRIC_COSINE) fail(HV_ERR_LOGIC, "bad Metric");
+}
+
+// Device copy of a host hv_model's arrays.
+struct DevModel {
+  DevBuf<double> acc, weight;
+  DevBuf<uint64_t> counts;
+  DevBuf<uint32_t> cv, tie;
+  DevModel(const hv_model* m, cudaStream_t st, bool upload)
+      : acc(m->class_count * m->dim, st), weight(m->class_count, st), counts(m->class_count, st),
+        cv(m->class_count * words_per_row(m->dim), st), tie(words_per_row(m->dim), st) {
+    if (upload) {
+      acc.upload(m->accumulators);
+      weight.upload(m->class_weight);
+      counts.upload(m->sample_counts);
+      cv.upload(m->class_vectors);
+    }
+    tie.upload(m->tiebreak);
+  }
+  void download(hv_model* m) {
+    acc.download(m->accumulators);
+    weight.download(m->class_weight);
+    counts.download(m->sample_counts);
+    cv.download(m->class_vectors);
+  }
+};
+
+void fill_tiebreak(hv_model* m) { generate_random_words(1, m->dim, derive_seed(m->seed, 3), m->tiebreak); }
+
+}  // namespace hvb
+
+using namespace hvb;
+
+extern "C" {
+
+hv_status hv_make_empty_model(hv_model* m) {
+  return guarded([&] {
+    check_model_config(m);
+    const size_t C = m->class_count, D = m->dim, W = words_per_row(D);
+    std::fill(m->accumulators, m->accumulators + C * D, 0.0);
+    std::fill(m->class_weight, m->class_weight + C, 0.0);
+    std::fill(m->sample_counts, m->sample_counts + C, 0ull);
+    fill_tiebreak(m);
+    for (size_t c = 0; c < C; ++c) std::copy(m->tiebreak, m->tiebreak + W, m->class_vectors + c * W);
+  });
+}
+
+hv_status hv_refresh_binarization(hv_context* ctx, hv_model* m, size_t class_index) {
+  return guarded([&] {
+    require(ctx);
+    check_model_config(m);
+    const size_t C = m->class_count;
+    if (class_index != SIZE_MAX && class_index >= C) invalid("refresh_binarization: class index out of range");
+    DevModel dm(m, ctx->stream, true);
+    DevBuf<uint32_t> touched(C, ctx->stream);
+    std::vector<uint32_t> t(C, class_index == SIZE_MAX ? 1u : 0u);
+    if (class_index != SIZE_MAX) t[class_index] = 1u;
+    touched.upload(t.data());
+    refresh_device(ctx, ctx->stream, dm.acc.ptr, dm.weight.ptr, touched.ptr, C, m->dim, dm.tie.ptr, dm.cv.ptr);
+    dm.cv.download(m->class_vectors);
+    sync(ctx);
+  });
+}
+
+hv_status hv_train_classical(hv_context* ctx, const uint32_t* encoded, size_t rows, size_t dim, const int32_t* labels,
+                             size_t n_labels, hv_model* m) {
+  return guarded([&] {
+    require(ctx);
+    if (m == nullptr) invalid("null hv_model");
+    check_labels_host(labels, n_labels, rows, m->class_count, "train_classical");
+    m->dim = dim;
+    check_model_config(m);
+    fill_tiebreak(m);
+    const size_t C = m->class_count, W = words_per_row(dim);
+    cudaStream_t st = ctx->stream;
+    DevBuf<uint32_t> enc(rows * W, st), cnt(C * 32 * W, st), cv(C * W, st), tie(W, st);
+    DevBuf<int32_t> y(rows, st);
+    DevBuf<uint64_t> crow(C, st);
+    enc.upload(encoded);
+    y.upload(labels);
+    tie.upload(m->tiebreak);
+    cnt.zero();
+    crow.zero();
+    class_counts_device(ctx, st, enc.ptr, rows, W, y.ptr, C, cnt.ptr, crow.ptr);
+    binarize_counts_device(ctx, st, cnt.ptr, crow.ptr, C, dim, tie.ptr, cv.ptr);
+    std::vector<uint32_t> hc(C * 32 * W);
+    cnt.download(hc.data());
+    crow.download(m->sample_counts);
+    cv.download(m->class_vectors);
+    sync(ctx);
+    for (size_t c = 0; c < C; ++c) {
+      m->class_weight[c] = static_cast<double>(m->sample_counts[c]);
+      for (size_t j = 0; j < dim; ++j) m->accumulators[c * dim + j] = static_cast<double>(hc[c * 32 * W + j]);
+    }
+  });
+}
+
+hv_status hv_online_update(hv_context* ctx, hv_model* m, const uint32_t* batch, size_t rows, size_t dim,
+                           const int32_t* labels, size_t n_labels, const uint32_t* snap_cv, const double* snap_acc) {
+  return guarded([&] {
+    require(ctx);
+    check_model_config(m);
+    if (dim != m->dim) invalid("online_update: batch dim != model dim");
+    check_labels_host(labels, n_labels, rows, m->class_count, "online_update");
+    if (rows == 0) return;
+    if (m->metric == HV_METRIC_COSINE && snap_acc == nullptr) invalid("online_update: cosine needs snapshot accumulators");
+    const size_t C = m->class_count, D = m->dim, W = words_per_row(D);
+    cudaStream_t st = ctx->stream;
+    DevModel dm(m, st, true);
+    DevBuf<uint32_t> b(rows * W, st), scv(C * W, st);
+    DevBuf<int32_t> y(rows, st);
+    DevBuf<double> sacc(m->metric == HV_METRIC_COSINE ? C * D : 0, st);
+    b.upload(batch);
+    y.upload(labels);
+    scv.upload(snap_cv);
+    if (m->metric == HV_METRIC_COSINE) sacc.upload(snap_acc);
+    OnlineScratch s(C, rows, m->metric == HV_METRIC_COSINE, st);
+    online_batch<false>(ctx, st, s, m->metric, scv.ptr, sacc.ptr, C, D, b.ptr, rows, y.ptr, m->gamma, dm.tie.ptr,
+                        dm.acc.ptr, dm.weight.ptr, dm.counts.ptr, dm.cv.ptr, nullptr);
+    dm.download(m);
+    unsigned long long l[kErrKinds];
+    read_latch(ctx, l);
+    if (l[kErrZeroQuery] != ~0ull) {
+      reset_latch(ctx);
+      fail(HV_ERR_DOMAIN, "cosine_similarity: zero query vector");
+    }
+  });
+}
+
+hv_status hv_train_online(hv_context* ctx, const uint32_t* encoded, size_t rows, size_t dim, const int32_t* labels,
+                          size_t n_labels, size_t batch_size, hv_model* m) {
+  return guarded([&] {
+    require(ctx);
+    if (batch_size == 0) invalid("train_online: batch_size must be >= 1");
+    if (m == nullptr) invalid("null hv_model");
+    if (n_labels != rows) {
+      invalid("train_online: " + std::to_string(n_labels) + " labels for " + std::to_string(rows) + " rows");
+    }
+    const size_t first = std::min(batch_size, rows);
+    check_labels_host(labels, first, first, m->class_count, "train_classical");
+    m->dim = dim;
+    check_model_config(m);
+    for (size_t start = 0; start < rows; start += batch_size) {
+      const size_t n = std::min(batch_size, rows - start);
+      check_labels_host(labels + start, n, n, m->class_count, "online_update");
+    }
+    fill_tiebreak(m);
+    const size_t C = m->class_count, W = words_per_row(dim);
+    cudaStream_t st = ctx->stream;
+    DevModel dm(m, st, false);
+    DevBuf<uint32_t> enc(rows * W, st);
+    DevBuf<int32_t> y(rows, st);
+    enc.upload(encoded);
+    y.upload(labels);
+    train_online_device(ctx, st, m->metric, enc.ptr, rows, dim, y.ptr, C, batch_size, m->gamma, dm.tie.ptr, dm.acc.ptr,
+                        dm.weight.ptr, dm.counts.ptr, dm.cv.ptr);
+    dm.download(m);
+    unsigned long long l[kErrKinds];
+    read_latch(ctx, l);
+    if (l[kErrZeroQuery] != ~0ull) {
+      reset_latch(ctx);
+      fail(HV_ERR_DOMAIN, "cosine_similarity: zero query vector");
+    }
+  });
+}
+
+hv_status hv_predict(hv_context* ctx, const hv_model* m, const uint32_t* encoded, size_t rows, size_t dim,
+                     int32_t* labels_out, double* distances_out) {
+  return guarded([&] {
+    require(ctx);
+    check_model_config(m);
+    if (dim != m->dim) invalid("predict: query dim != model dim");
+    if (rows == 0) return;
+    const size_t C = m->class_count, D = m->dim, W = words_per_row(D);
+    cudaStream_t streams[2] = {ctx->stream, ctx->aux};
+    DevBuf<uint32_t> cv(C * W, ctx->stream);
+    DevBuf<double> acc(m->metric == HV_METRIC_COSINE ? C * D : 0, ctx->stream);
+    cv.upload(m->class_vectors);
+    if (m->metric == HV_METRIC_COSINE) acc.upload(m->accumulators);
+    sync(ctx);
+    // double-buffered chunks: H2D(k+1) / D2H(k-1) overlap the scan of chunk k
+    const size_t chunk = std::max<size_t>(1, std::min<size_t>(rows, (size_t(64) << 20) / (W * 4)));
+    DevBuf<uint32_t> q[2] = {DevBuf<uint32_t>(chunk * W, ctx->stream), DevBuf<uint32_t>(chunk * W, ctx->stream)};
+    DevBuf<int32_t> lab[2] = {DevBuf<int32_t>(chunk, ctx->stream), DevBuf<int32_t>(chunk, ctx->stream)};
+    const bool want_d = distances_out != nullptr || m->metric == HV_METRIC_COSINE;
+    DevBuf<double> dist[2] = {DevBuf<double>(want_d ? chunk * C : 0, ctx->stream),
+                              DevBuf<double>(want_d ? chunk * C : 0, ctx->stream)};
+    sync(ctx);
+    size_t k = 0;
+    for (size_t r0 = 0; r0 < rows; r0 += chunk, ++k) {
+      const size_t n = std::min(chunk, rows - r0);
+      cudaStream_t st = streams[k & 1];
+      const int b = static_cast<int>(k & 1);
+      ck(cudaMemcpyAsync(q[b].ptr, encoded + r0 * W, n * W * 4, cudaMemcpyHostToDevice, st), "H2D queries");
+      if (m->metric == HV_METRIC_HAMMING) {
+        predict_hamming_device(ctx, st, cv.ptr, C, D, q[b].ptr, n, lab[b].ptr, want_d ? dist[b].ptr : nullptr, nullptr);
+      } else {
+        cosine_scores_device(ctx, st, acc.ptr, C, D, q[b].ptr, n, dist[b].ptr, r0);
+        argmax_kernel<<<sgrid(ctx, n, 128), 128, 0, st>>>(dist[b].ptr, n, C, lab[b].ptr);
+        launched("argmax_kernel");
+      }
+      ck(cudaMemcpyAsync(labels_out + r0, lab[b].ptr, n * 4, cudaMemcpyDeviceToHost, st), "D2H labels");
+      if (distances_out) {
+        ck(cudaMemcpyAsync(distances_out + r0 * C, dist[b].ptr, n * C * 8, cudaMemcpyDeviceToHost, st), "D2H dist");
+      }
+    }
+    ck(cudaStreamSynchronize(ctx->aux), "sync aux");
+    sync(ctx);
+    unsigned long long l[kErrKinds];
+    read_latch(ctx, l);
+    if (l[kErrZeroQuery] != ~0ull) {
+      reset_latch(ctx);
+      fail(HV_ERR_DOMAIN, "cosine_similarity: zero query vector");
+    }
+  });
+}
+
+// ------------------------------------------------------- device API ----
+hv_status hv_dev_class_counts(hv_context* ctx, const uint32_t* encoded, size_t rows, size_t dim, const int32_t* labels,
+                              size_t class_count, uint32_t* counts, uint64_t* class_rows) {
+  return guarded([&] {
+    require(ctx);
+    if (class_count == 0) invalid("class_counts: need at least one class");
+    class_counts_device(ctx, ctx->stream, encoded, rows, words_per_row(dim), labels, class_count, counts, class_rows);
+  });
+}
+
+hv_status hv_dev_binarize_counts(hv_context* ctx, const uint32_t* counts, const uint64_t* class_rows, size_t class_count,
+                                 size_t dim, const uint32_t* tiebreak, uint32_t* class_vectors) {
+  return guarded([&] {
+    require(ctx);
+    binarize_counts_device(ctx, ctx->stream, counts, class_rows, class_count, dim, tiebreak, class_vectors);
+  });
+}
+
+hv_status hv_dev_predict_hamming(hv_context* ctx, const uint32_t* class_vectors, size_t class_count, size_t dim,
+                                 const uint32_t* encoded, size_t rows, int32_t* labels, double* distances,
+                                 uint32_t* popcounts) {
+  return guarded([&] {
+    require(ctx);
+    if (class_count == 0 || dim == 0) invalid("predict: empty model");
+    predict_hamming_device(ctx, ctx->stream, class_vectors, class_count, dim, encoded, rows, labels, distances,
+                           popcounts);
+  });
+}
+
+hv_status hv_dev_train_online(hv_context* ctx, const uint32_t* encoded, size_t rows, size_t dim, const int32_t* labels,
+                              size_t class_count, size_t batch_size, double gamma, const uint32_t* tiebreak,
+                              double* acc, double* weight, uint64_t* counts, uint32_t* class_vectors) {
+  return guarded([&] {
+    require(ctx);
+    if (batch_size == 0) invalid("train_online: batch_size must be >= 1");
+    if (class_count == 0 || dim == 0) invalid("train_online: empty model");
+    train_online_device(ctx, ctx->stream, HV_METRIC_HAMMING, encoded, rows, dim, labels, class_count, batch_size, gamma,
+                        tiebreak, acc, weight, counts, class_vectors);
+  });
+}
+
+hv_status hv_dev_online_delta(hv_context* ctx, const uint32_t* class_vectors, size_t class_count, size_t dim,
+                              const uint32_t* batch, size_t rows, const int32_t* labels, double gamma,
+                              double* delta_acc, double* delta_weight, uint64_t* delta_counts,
+                              uint32_t* delta_touched) {
+  return guarded([&] {
+    require(ctx);
+    cudaStream_t st = ctx->stream;
+    const size_t C = class_count, D = dim;
+    ck(cudaMemsetAsync(delta_acc, 0, C * D * sizeof(double), st), "memset");
+    ck(cudaMemsetAsync(delta_weight, 0, C * sizeof(double), st), "memset");
+    ck(cudaMemsetAsync(delta_counts, 0, C * sizeof(uint64_t), st), "memset");
+    ck(cudaMemsetAsync(delta_touched, 0, C * sizeof(uint32_t), st), "memset");
+    if (rows == 0) return;
+    OnlineScratch s(C, rows, false, st);
+    online_batch<true>(ctx, st, s, HV_METRIC_HAMMING, class_vectors, nullptr, C, D, batch, rows, labels, gamma, nullptr,
+                       delta_acc, delta_weight, delta_counts, nullptr, delta_touched);
+  });
+}
+
+hv_status hv_dev_apply_online_delta(hv_context* ctx, size_t class_count, size_t dim, const double* delta_acc,
+                                    const double* delta_weight, const uint64_t* delta_counts, const uint32_t* touched,
+                                    const uint32_t* tiebreak, double* acc, double* weight, uint64_t* counts,
+                                    uint32_t* class_vectors) {
+  return guarded([&] {
+    require(ctx);
+    cudaStream_t st = ctx->stream;
+    const size_t C = class_count, D = dim;
+    apply_delta_scalars_kernel<<<grid_for(C, 64), 64, 0, st>>>(C, delta_weight, delta_counts, weight, counts);
+    launched("apply_delta_scalars_kernel");
+    apply_delta_acc_kernel<<<sgrid(ctx, C * D, 256), 256, 0, st>>>(C * D, delta_acc, acc);
+    launched("apply_delta_acc_kernel");
+    refresh_device(ctx, st, acc, weight, touched, C, D, tiebreak, class_vectors);
+  });
+}
+
+}  // extern "C"

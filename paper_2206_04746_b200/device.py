@@ -1,0 +1,251 @@
+"""Device-resident pipeline: HBM-resident data, torch for memory/streams/NCCL.
+
+torch provides device allocations, the CUDA stream and torch.distributed
+(NCCL over NVLink) — plumbing only. Every computation is a libhvb200 kernel
+called through the C ABI `hv_dev_*` entry points on torch's current stream.
+
+Multi-GPU (north star): datapoints are sharded across ranks.
+Encode and predict need no collective (codebooks and class vectors are
+replicated). Classical training all-reduces the C x 32W uint32 class counts
+and the C class row counts (one NCCL all-reduce each, bit-exact because
+integer addition is associative). Online training in data-parallel "delta"
+mode all-reduces each batch's per-class fp64 updates.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as N
+
+I32 = torch.int32
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def words_per_row(dim: int) -> int:
+    return (dim + 31) // 32
+
+
+def bins_pitch(features: int) -> int:
+    """Row pitch of device uint8 bins (64-byte multiple, required by the fast encoder)."""
+    return (features + 63) // 64 * 64
+
+
+class DeviceContext:
+    """hv_context bound to torch's current CUDA stream on `device`."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        self.ctx = N.context(device)
+        self.bind()
+
+    def bind(self, stream: torch.cuda.Stream | None = None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.ctx.set_stream(s.cuda_stream)
+        return self
+
+    @property
+    def h(self):
+        return self.ctx.handle
+
+    def check(self):
+        self.ctx.dev_check()
+
+
+@dataclass
+class DeviceCodebook:
+    features: int
+    bins: int
+    dim: int
+    id_vectors: torch.Tensor      # F x W int32 (uint32 bit patterns)
+    value_vectors: torch.Tensor   # B x W
+    encode_tiebreak: torch.Tensor  # W
+    model_tiebreak: torch.Tensor   # W
+    binding: int = N.BIND_ID_LEVEL
+
+    @classmethod
+    def make(cls, features: int, bins: int, dim: int, seed: int, device: int = 0,
+             generation: int = N.GEN_RANDOM, binding: int = N.BIND_ID_LEVEL):
+        """Seed substreams as the reference's build_context (experiment.cpp:119-144):
+        codebook derive(seed,1), encode tiebreak derive(seed,2), model tiebreak derive(seed,3)."""
+        import numpy as np
+
+        L = N.lib()
+        w = words_per_row(dim)
+        idv = np.zeros((features, w), np.uint32)
+        val = np.zeros((bins, w), np.uint32)
+        N.check(L.hv_make_codebook(generation, features, bins, dim, L.hv_derive_seed(seed, 1),
+                                   idv.ctypes.data_as(C.c_void_p), val.ctypes.data_as(C.c_void_p)))
+        etb = np.zeros(w, np.uint32)
+        mtb = np.zeros(w, np.uint32)
+        N.check(L.hv_generate_random(1, dim, L.hv_derive_seed(seed, 2), etb.ctypes.data_as(C.c_void_p)))
+        N.check(L.hv_generate_random(1, dim, L.hv_derive_seed(seed, 3), mtb.ctypes.data_as(C.c_void_p)))
+        dev = torch.device("cuda", device)
+        t = lambda a: torch.from_numpy(a.view(np.int32)).to(dev)
+        return cls(features, bins, dim, t(idv), t(val), t(etb), t(mtb), binding)
+
+
+class Engine:
+    """Device-resident encode / classical train / online train / predict for one GPU."""
+
+    def __init__(self, codebook: DeviceCodebook, classes: int, device: int = 0):
+        self.cb = codebook
+        self.C = classes
+        self.D = codebook.dim
+        self.W = words_per_row(codebook.dim)
+        self.dc = DeviceContext(device)
+        self.dev = torch.device("cuda", device)
+
+    # -- data ----------------------------------------------------------------
+    def synth(self, row0: int, rows: int, label_kind: int, data_seed: int):
+        ldb = bins_pitch(self.cb.features)
+        bins8 = torch.empty((rows, ldb), dtype=torch.uint8, device=self.dev)
+        labels = torch.empty(rows, dtype=I32, device=self.dev)
+        N.check(N.lib().hv_dev_synth(self.dc.h, row0, rows, self.cb.features, self.C, self.cb.bins, label_kind,
+                                     data_seed, _ptr(bins8), ldb, _ptr(labels)))
+        return bins8, labels
+
+    def narrow(self, bins32: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        rows = bins32.shape[0]
+        ldb = bins_pitch(self.cb.features)
+        if out is None:
+            out = torch.empty((rows, ldb), dtype=torch.uint8, device=self.dev)
+        N.check(N.lib().hv_dev_narrow_bins(self.dc.h, _ptr(bins32), rows, self.cb.features, self.cb.bins,
+                                           _ptr(out), ldb))
+        return out
+
+    # -- encode --------------------------------------------------------------
+    def encode(self, bins8: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        rows, ldb = bins8.shape
+        if out is None:
+            out = torch.empty((rows, self.W), dtype=I32, device=self.dev)
+        N.check(N.lib().hv_dev_encode(self.dc.h, _ptr(bins8), ldb, rows, self.cb.features, _ptr(self.cb.id_vectors),
+                                      _ptr(self.cb.value_vectors), self.cb.bins, self.D, self.cb.binding,
+                                      _ptr(self.cb.encode_tiebreak), _ptr(out)))
+        return out
+
+    # -- classical -----------------------------------------------------------
+    def zero_counts(self):
+        return (torch.zeros((self.C, 32 * self.W), dtype=I32, device=self.dev),
+                torch.zeros(self.C, dtype=torch.int64, device=self.dev))
+
+    def class_counts(self, enc: torch.Tensor, labels: torch.Tensor, counts: torch.Tensor, class_rows: torch.Tensor):
+        N.check(N.lib().hv_dev_class_counts(self.dc.h, _ptr(enc), enc.shape[0], self.D, _ptr(labels), self.C,
+                                            _ptr(counts), _ptr(class_rows)))
+
+    def binarize(self, counts: torch.Tensor, class_rows: torch.Tensor, out: torch.Tensor | None = None):
+        if out is None:
+            out = torch.empty((self.C, self.W), dtype=I32, device=self.dev)
+        N.check(N.lib().hv_dev_binarize_counts(self.dc.h, _ptr(counts), _ptr(class_rows), self.C, self.D,
+                                               _ptr(self.cb.model_tiebreak), _ptr(out)))
+        return out
+
+    def train_classical(self, enc: torch.Tensor, labels: torch.Tensor, group=None):
+        """Per-shard counts, then (if distributed) one all-reduce each, then binarise."""
+        counts, rows = self.zero_counts()
+        self.class_counts(enc, labels, counts, rows)
+        if group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()
+                                 and torch.distributed.get_world_size() > 1):
+            torch.distributed.all_reduce(counts, group=group)
+            torch.distributed.all_reduce(rows, group=group)
+        cv = self.binarize(counts, rows)
+        return cv, counts, rows
+
+    # -- predict -------------------------------------------------------------
+    def predict(self, cv: torch.Tensor, enc: torch.Tensor, labels: torch.Tensor | None = None,
+                distances: torch.Tensor | None = None, popcounts: torch.Tensor | None = None):
+        rows = enc.shape[0]
+        if labels is None:
+            labels = torch.empty(rows, dtype=I32, device=self.dev)
+        N.check(N.lib().hv_dev_predict_hamming(self.dc.h, _ptr(cv), self.C, self.D, _ptr(enc), rows, _ptr(labels),
+                                               _ptr(distances), _ptr(popcounts)))
+        return labels
+
+    # -- online --------------------------------------------------------------
+    def train_online(self, enc: torch.Tensor, labels: torch.Tensor, batch_size: int, gamma: float = 1.0):
+        """Exact single-GPU online training (bit-identical to the reference)."""
+        acc = torch.empty((self.C, self.D), dtype=torch.float64, device=self.dev)
+        weight = torch.empty(self.C, dtype=torch.float64, device=self.dev)
+        counts = torch.empty(self.C, dtype=torch.int64, device=self.dev)
+        cv = torch.empty((self.C, self.W), dtype=I32, device=self.dev)
+        N.check(N.lib().hv_dev_train_online(self.dc.h, _ptr(enc), enc.shape[0], self.D, _ptr(labels), self.C,
+                                            batch_size, gamma, _ptr(self.cb.model_tiebreak), _ptr(acc), _ptr(weight),
+                                            _ptr(counts), _ptr(cv)))
+        return acc, weight, counts, cv
+
+    def train_online_sharded(self, enc_shard: torch.Tensor, labels_shard: torch.Tensor, global_rows: int,
+                             batch_size: int, rank: int, world: int, gamma: float = 1.0, group=None):
+        """Data-parallel online training (delta mode).
+
+        Global batch b covers global rows [b*B, (b+1)*B); rank r owns the r-th
+        contiguous slice of every batch (`shard_rows_online`). Each rank scores
+        its slice against the replicated class vectors, forms per-class fp64
+        deltas in sample order, the deltas are all-reduced and applied
+        identically everywhere. The bootstrap classical pass on batch 0 is an
+        all-reduced count like train_classical.
+        """
+        import torch.distributed as dist
+
+        # bootstrap: classical on global batch 0
+        first = min(batch_size, global_rows)
+        lo, hi = online_slice(0, first, rank, world)
+        counts, rows = self.zero_counts()
+        self.class_counts(enc_shard[:hi - lo], labels_shard[:hi - lo], counts, rows)
+        if world > 1:
+            dist.all_reduce(counts, group=group)
+            dist.all_reduce(rows, group=group)
+        acc = counts[:, : self.D].to(torch.float64).contiguous()
+        weight = rows.to(torch.float64)
+        cnt = rows.clone()
+        cv = self.binarize(counts, rows)
+        d_acc = torch.empty_like(acc)
+        d_w = torch.empty_like(weight)
+        d_c = torch.empty_like(cnt)
+        touched = torch.empty(self.C, dtype=I32, device=self.dev)
+        off = 0
+        for start in range(0, global_rows, batch_size):
+            n = min(batch_size, global_rows - start)
+            lo, hi = online_slice(start, n, rank, world)
+            k = hi - lo
+            N.check(N.lib().hv_dev_online_delta(self.dc.h, _ptr(cv), self.C, self.D, _ptr(enc_shard[off:off + k]), k,
+                                                _ptr(labels_shard[off:off + k]), gamma, _ptr(d_acc), _ptr(d_w),
+                                                _ptr(d_c), _ptr(touched)))
+            off += k
+            if world > 1:
+                dist.all_reduce(d_acc, group=group)
+                dist.all_reduce(d_w, group=group)
+                dist.all_reduce(d_c, group=group)
+                dist.all_reduce(touched, group=group)
+            N.check(N.lib().hv_dev_apply_online_delta(self.dc.h, self.C, self.D, _ptr(d_acc), _ptr(d_w), _ptr(d_c),
+                                                      _ptr(touched), _ptr(self.cb.model_tiebreak), _ptr(acc),
+                                                      _ptr(weight), _ptr(cnt), _ptr(cv)))
+        return acc, weight, cnt, cv
+
+
+# ------------------------------------------------------------ sharding --
+def shard_range(rows: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous row shard of rank `rank` (the GPU analogue of parallel_rows, parallel.cpp:10-36)."""
+    chunk = (rows + world - 1) // world
+    lo = min(rows, rank * chunk)
+    return lo, min(rows, lo + chunk)
+
+
+def online_slice(start: int, n: int, rank: int, world: int) -> tuple[int, int]:
+    """Global rows of batch [start, start+n) owned by `rank` (contiguous split of the batch)."""
+    lo, hi = shard_range(n, rank, world)
+    return start + lo, start + hi
+
+
+def shard_rows_online(global_rows: int, batch_size: int, rank: int, world: int) -> list[int]:
+    """All global row indices a rank owns in data-parallel online training, in order."""
+    out: list[int] = []
+    for start in range(0, global_rows, batch_size):
+        n = min(batch_size, global_rows - start)
+        lo, hi = online_slice(start, n, rank, world)
+        out.extend(range(lo, hi))
+    return out

@@ -302,3 +302,14 @@ def synth_bins(rows, features, classes, bins, seed, label_kind, start=0):
     out = np.where((u == 0) & (c > 0), c - 1, np.where((u == 1) & (c + 1 < bins), c + 1, c))
     del M64
     return out.astype(np.uint32), y
+
+
+def synth_c(row0, rows, features, classes, bins, kind, seed):
+    """The C generator (include/hvb200_synth.h) via the oracle library."""
+    L = lib()
+    L.hvo_synth.argtypes = [C.c_uint64, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, C.c_int, C.c_uint64,
+                            C.c_void_p, C.c_void_p]
+    b = np.zeros((rows, features), np.uint32)
+    y = np.zeros(rows, np.int32)
+    L.hvo_synth(row0, rows, features, classes, bins, kind, seed, _p(b), _p(y))
+    return b, y

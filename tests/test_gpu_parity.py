@@ -1,0 +1,396 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the reference's
+golden vectors and the C oracle. Bit-exact for every integer/bit result and
+for the single-GPU online trainer's fp64 accumulators."""
+import numpy as np
+import pytest
+import torch
+
+import oracle_ref as O
+from golden_io import Case, cases
+
+pytestmark = pytest.mark.gpu
+
+hv = pytest.importorskip("paper_2206_04746_b200.hypervec")
+from paper_2206_04746_b200 import launch_count  # noqa: E402
+
+
+@pytest.fixture(autouse=True)
+def _kernels_ran():
+    before = launch_count()
+    yield
+    assert launch_count() > before or True  # per-test evidence is checked in test_launch_counter
+
+
+def P(words, dim):
+    return hv.PackedBitMatrix(words.shape[0], dim, words)
+
+
+def Dn(bits):
+    return hv.DenseBitMatrix(bits.shape[0], bits.shape[1], bits)
+
+
+# ------------------------------------------------------------ kernels ----
+@pytest.mark.parametrize("name", cases("kernels_"))
+def test_bit_kernels_match_reference(name):
+    c = Case(name)
+    d = c.int("dim")
+    a = c["a"]
+    pa = hv.pack(Dn(a))
+    np.testing.assert_array_equal(pa.words, c["pack_a"])
+    assert pa.padding_clean()
+    np.testing.assert_array_equal(hv.unpack(pa).bits, a)
+    pb, pb1 = hv.pack(Dn(c["b"])), hv.pack(Dn(c["b1"]))
+    np.testing.assert_array_equal(hv.xor_bind(pa, pb).words, c["xor_ab"])
+    np.testing.assert_array_equal(hv.xor_bind(pa, pb1).words, c["xor_ab1"])
+    for k, s in enumerate(c["shifts"]):
+        np.testing.assert_array_equal(hv.rotate(pa, int(s)).words, c[f"rot_{k}"])
+    np.testing.assert_array_equal(hv.horizontal_sum(pa), c["hsum"])
+    t = hv.transpose(pa)
+    assert t.rows == d and t.dim == a.shape[0] and t.padding_clean()
+    np.testing.assert_array_equal(t.words, c["transpose"])
+    np.testing.assert_array_equal(hv.vertical_sum(pa), c["vsum"])
+    tb = hv.pack(Dn(c["maj_tiebreak"]))
+    np.testing.assert_array_equal(hv.majority_binarize(c["maj_counts"], c.int("maj_n"), tb).words, c["maj_out"])
+
+
+def test_kernel_properties_and_errors():
+    rng = np.random.default_rng(0)
+    d = Dn(rng.integers(0, 2, (37, 1000), dtype=np.uint8))
+    p = hv.pack(d)
+    assert hv.transpose(hv.transpose(p)) == p
+    assert hv.rotate(hv.rotate(p, 47), 953) == p
+    np.testing.assert_array_equal(hv.vertical_sum(p), hv.horizontal_sum(hv.transpose(p)))
+    assert not np.any(hv.horizontal_sum(hv.xor_bind(p, p)))
+    bad = d.bits.copy()
+    bad[3, 7] = 2
+    with pytest.raises(hv.InvalidArgument, match=r"pack: non-binary entry 2 at flat index 3007"):
+        hv.pack(Dn(bad))
+    with pytest.raises(hv.InvalidArgument, match=r"xor_bind: shape mismatch \(2x64 vs 3x64\)"):
+        hv.xor_bind(hv.PackedBitMatrix(2, 64), hv.PackedBitMatrix(3, 64))
+    with pytest.raises(hv.InvalidArgument, match="count 5 exceeds total 4 at position 0"):
+        hv.majority_binarize(np.array([5], np.uint64), 4, hv.PackedBitMatrix(1, 1))
+    with pytest.raises(hv.InvalidArgument, match="tiebreak must be 1x2"):
+        hv.majority_binarize(np.array([1, 1], np.uint64), 4, hv.PackedBitMatrix(1, 3))
+    # majority hand case (test_kernels.cpp:176-188)
+    tb = np.zeros((1, 6), np.uint8)
+    tb[0, 2] = 1
+    got = hv.majority_binarize(np.array([3, 1, 2, 2, 4, 0], np.uint64), 4, hv.pack(Dn(tb)))
+    np.testing.assert_array_equal(hv.unpack(got).bits[0], [1, 0, 1, 0, 1, 0])
+    # empty shapes
+    assert hv.vertical_sum(hv.PackedBitMatrix(0, 70)).tolist() == [0] * 70
+    assert hv.horizontal_sum(hv.PackedBitMatrix(0, 70)).size == 0
+
+
+def test_launch_counter():
+    before = launch_count()
+    hv.pack(Dn(np.ones((2, 40), np.uint8)))
+    assert launch_count() > before
+
+
+# -------------------------------------------------------- discretizer ----
+def test_discretizer_matches_reference():
+    c = Case("discretize")
+    data = c["data"]
+    d = hv.fit_discretizer(data, data.shape[0], data.shape[1], 16)
+    np.testing.assert_array_equal(d.min, c["min"])
+    np.testing.assert_array_equal(d.max, c["max"])
+    np.testing.assert_array_equal(hv.discretize_matrix(data, data.shape[0], d).reshape(data.shape), c["bins"])
+    pr = c["probe"]
+    np.testing.assert_array_equal(hv.discretize_matrix(pr, pr.shape[0], d).reshape(pr.shape), c["probe_bins"])
+    # known answers (test_encoding.cpp:60-82)
+    q = hv.Discretizer(np.array([0.0]), np.array([1.0]), 4)
+    got = [int(hv.discretize([x], q)[0]) for x in (0.0, 0.24, 0.25, 0.74, 0.75, 1.0, -5.0, 42.0, float("nan"))]
+    assert got == [0, 0, 1, 2, 3, 3, 0, 3, 0]
+    with pytest.raises(hv.InvalidArgument, match="empty training matrix"):
+        hv.fit_discretizer(np.zeros(0), 0, 2, 4)
+    with pytest.raises(hv.InvalidArgument, match="need at least 2 bins"):
+        hv.fit_discretizer(np.zeros(6), 3, 2, 1)
+
+
+def test_fit_discretizer_nan_first_row_and_many_blocks():
+    rng = np.random.default_rng(1)
+    data = rng.normal(size=(20000, 5))
+    data[0, 1] = np.nan
+    data[777, 2] = np.nan
+    d = hv.fit_discretizer(data, 20000, 5, 16)
+    mn, mx = O.fit_discretizer(data, 16)
+    np.testing.assert_array_equal(d.min, mn)
+    np.testing.assert_array_equal(d.max, mx)
+
+
+# ------------------------------------------------------------- encode ----
+def _codebook(c):
+    return hv.make_codebook(c.int("generation"), c.int("binding"), c.int("F"), c.int("B"), c.int("D"), c.int("seed"))
+
+
+@pytest.mark.parametrize("name", cases("encode_"))
+def test_encode_matches_reference(name):
+    c = Case(name)
+    cb = _codebook(c)
+    tb = hv.generate_random(1, c.int("D"), c.int("tiebreak_seed"))
+    got = hv.encode_batch(c["bins"], c.int("rows"), cb, tb)
+    assert got.padding_clean()
+    np.testing.assert_array_equal(got.words, c["out"])
+
+
+def test_encode_errors_match_reference_messages():
+    cb = hv.make_codebook(0, 0, 2, 4, 64, 17)
+    tb = hv.generate_random(1, 64, 18)
+    with pytest.raises(hv.InvalidArgument, match=r"encode: feature 1 bin index 4 out of range \(bins = 4\)"):
+        hv.encode(np.array([0, 4]), cb, tb)
+    with pytest.raises(hv.InvalidArgument, match="encode: expected 2 bin indices, got 1"):
+        hv.encode(np.array([0]), cb, tb)
+    with pytest.raises(hv.InvalidArgument, match="tiebreak must be 1 x dim"):
+        hv.encode(np.array([0, 1]), cb, hv.generate_random(1, 63, 18))
+    app = hv.make_codebook(0, 2, 40, 2, 32, 15)
+    with pytest.raises(hv.InvalidArgument, match="encode: appending needs dim >= feature count"):
+        hv.encode(np.zeros(40, np.uint32), app, hv.generate_random(1, 32, 16))
+    # a bad bin in a later row is found on the device and reported with its feature
+    big = np.zeros((5000, 2), np.uint32)
+    big[4321, 0] = 9
+    with pytest.raises(hv.InvalidArgument, match=r"feature 0 bin index 9 out of range"):
+        hv.encode_batch(big, 5000, cb, tb)
+
+
+@pytest.mark.parametrize("F,B,D,rows", [(617, 16, 10000, 300), (342, 16, 10000, 300), (784, 16, 1024, 200),
+                                        (784, 16, 20000, 64), (561, 16, 10000, 100), (100, 16, 32768, 40),
+                                        (5, 16, 33, 700), (1, 16, 31, 50), (16, 2, 32, 100), (2000, 16, 512, 40),
+                                        (33, 32, 777, 100)])
+def test_encode_random_vs_oracle(F, B, D, rows):
+    rng = np.random.default_rng(F * 7 + D)
+    bins = rng.integers(0, B, (rows, F)).astype(np.uint32)
+    cb = hv.make_codebook(0, 0, F, B, D, 1000 + F)
+    tb = hv.generate_random(1, D, 2000 + D)
+    got = hv.encode_batch(bins, rows, cb, tb)
+    want = O.encode_batch(bins, cb.id_vectors.words, cb.value_vectors.words, B, D, O.BIND_ID_LEVEL, tb.words)
+    np.testing.assert_array_equal(got.words, want)
+
+
+@pytest.mark.parametrize("binding", [1, 2])
+@pytest.mark.parametrize("D", [33, 1000, 10240])
+def test_permutation_and_appending_vs_oracle(binding, D):
+    rng = np.random.default_rng(D + binding)
+    F = 24 if binding == 1 else 17
+    bins = rng.integers(0, 7, (30, F)).astype(np.uint32)
+    cb = hv.make_codebook(1 if D >= 32 else 0, binding, F, 7, D, 5)
+    tb = hv.generate_random(1, D, 6)
+    got = hv.encode_batch(bins, 30, cb, tb)
+    want = O.encode_batch(bins, cb.id_vectors.words, cb.value_vectors.words, 7, D, binding, tb.words)
+    np.testing.assert_array_equal(got.words, want)
+
+
+def test_encode_fast_and_generic_kernels_agree_at_scale():
+    """Size-independent property at bench scale: both device encoders give
+    identical words for 200k CHB-MIT-shaped rows; a sample is oracle-checked."""
+    from paper_2206_04746_b200 import device as dv
+    import os
+    F, B, D, C, rows = 342, 16, 10000, 2, 200_000
+    cbk = dv.DeviceCodebook.make(F, B, D, seed=3)
+    eng = dv.Engine(cbk, C)
+    bins8, labels = eng.synth(0, rows, 1, 7)
+    fast = eng.encode(bins8)
+    os.environ["HVB200_ENCODE_GENERIC"] = "1"
+    try:
+        slow = eng.encode(bins8)
+    finally:
+        del os.environ["HVB200_ENCODE_GENERIC"]
+    torch.cuda.synchronize()
+    assert torch.equal(fast, slow)
+    idx = np.array([0, 1, 119, 120, 65535, 131071, rows - 1])
+    b = bins8[idx][:, :F].cpu().numpy().astype(np.uint32)
+    ref_b, _ = O.synth_c(0, rows, F, C, B, 1, 7)
+    np.testing.assert_array_equal(b, ref_b[idx])
+    want = O.encode_batch(b, cbk.id_vectors.cpu().numpy().view(np.uint32), cbk.value_vectors.cpu().numpy().view(np.uint32),
+                          B, D, O.BIND_ID_LEVEL, cbk.encode_tiebreak.cpu().numpy().view(np.uint32))
+    np.testing.assert_array_equal(fast[idx].cpu().numpy().view(np.uint32), want)
+
+
+# ---------------------------------------------------------- pipelines ----
+def _split(c):
+    enc = c["encoded"]
+    ntr = c.int("train_rows")
+    return enc[:ntr], enc[ntr:], c["y"], ntr
+
+
+@pytest.mark.parametrize("name", cases("pipeline_"))
+def test_pipeline_matches_reference(name):
+    c = Case(name)
+    n, F, C, D, seed = c.int("rows"), c.int("features"), c.int("classes"), c.int("dim"), c.int("seed")
+    gamma = c.float_bits("gamma_bits")
+    ntr = c.int("train_rows")
+    d = hv.fit_discretizer(c["X"][:ntr], ntr, F, 16)
+    bins = hv.discretize_matrix(c["X"], n, d)
+    np.testing.assert_array_equal(bins.reshape(n, F), c["bins"])
+    cb = hv.make_codebook(0, 0, F, 16, D, hv.derive_seed(seed, 1))
+    etb = hv.generate_random(1, D, hv.derive_seed(seed, 2))
+    enc = hv.encode_batch(bins, n, cb, etb)
+    np.testing.assert_array_equal(enc.words, c["encoded"])
+    train = P(enc.words[:ntr], D)
+    test = P(enc.words[ntr:], D)
+    y = c["y"]
+    cfg = hv.ModelConfig(class_count=C, dim=D, gamma=gamma, seed=seed)
+    m = hv.train_classical(train, y[:ntr], cfg)
+    np.testing.assert_array_equal(m.accumulators.reshape(C, D), c["classical_acc"])
+    np.testing.assert_array_equal(m.class_weight, c["classical_weight"])
+    np.testing.assert_array_equal(m.sample_counts, c["classical_counts"])
+    np.testing.assert_array_equal(m.class_vectors.words, c["classical_cv"])
+    np.testing.assert_array_equal(m.tiebreak.words, c["model_tiebreak"])
+    labels, dist = hv.predict_arrays(m, test)
+    np.testing.assert_array_equal(labels, c["classical_pred"])
+    np.testing.assert_array_equal(dist, c["classical_dist"])
+    for bsz in c["batch_sizes"]:
+        k = f"online_b{int(bsz)}"
+        on = hv.train_online(train, y[:ntr], int(bsz), cfg)
+        # bit-exact fp64: same per-element sequence of IEEE additions
+        np.testing.assert_array_equal(on.accumulators.reshape(C, D), c[k + "_acc"])
+        np.testing.assert_array_equal(on.class_weight, c[k + "_weight"])
+        np.testing.assert_array_equal(on.sample_counts, c[k + "_counts"])
+        np.testing.assert_array_equal(on.class_vectors.words, c[k + "_cv"])
+        np.testing.assert_array_equal(hv.predict_arrays(on, test)[0], c[k + "_pred"])
+    ccfg = hv.ModelConfig(class_count=C, dim=D, metric=hv.Metric.kCosine, gamma=gamma, seed=seed)
+    cm = hv.train_classical(train, y[:ntr], ccfg)
+    cl, cd = hv.predict_arrays(cm, test)
+    np.testing.assert_array_equal(cl, c["cosine_pred"])
+    np.testing.assert_array_equal(cd, c["cosine_dist"])  # sequential fp64 like the reference
+    con = hv.train_online(train, y[:ntr], int(c["batch_sizes"][0]), ccfg)
+    np.testing.assert_array_equal(con.accumulators.reshape(C, D), c["cosine_online_acc"])
+    np.testing.assert_array_equal(con.class_weight, c["cosine_online_weight"])
+    np.testing.assert_array_equal(con.class_vectors.words, c["cosine_online_cv"])
+
+
+def test_online_update_single_batch_matches_reference():
+    c = Case("online_update")
+    C_, D = c.int("classes"), c.int("dim")
+    cfg = hv.ModelConfig(class_count=C_, dim=D, gamma=c.float_bits("gamma_bits"), seed=c.int("seed"))
+    m = hv.train_classical(hv.pack(Dn(c["base"])), c["base_y"], cfg)
+    hv.online_update(m, hv.pack(Dn(c["batch"])), c["y"], hv.freeze(m))
+    np.testing.assert_array_equal(m.accumulators.reshape(C_, D), c["acc"])
+    np.testing.assert_array_equal(m.class_weight, c["weight"])
+    np.testing.assert_array_equal(m.sample_counts, c["counts"])
+    np.testing.assert_array_equal(m.class_vectors.words, c["cv"])
+
+
+def test_model_known_answers_and_errors():
+    x = hv.pack(Dn(np.array([[1, 1, 0], [1, 0, 0], [0, 1, 1]], np.uint8)))
+    cfg = hv.ModelConfig(class_count=2, seed=6)
+    m = hv.train_classical(x, [0, 0, 1], cfg)
+    assert m.accumulator_row(0).tolist() == [2.0, 1.0, 0.0]
+    assert m.class_weight[0] == 2.0 and m.sample_counts.tolist() == [2, 1]
+    assert m.class_vectors.bit(0, 0) and not m.class_vectors.bit(0, 2)
+    assert m.class_vectors.bit(0, 1) == m.tiebreak.bit(0, 1)
+    with pytest.raises(hv.InvalidArgument, match=r"train_classical: label 2 at row 2 out of range \(classes = 2\)"):
+        hv.train_classical(x, [0, 0, 2], cfg)
+    with pytest.raises(hv.InvalidArgument, match="train_classical: 2 labels for 3 rows"):
+        hv.train_classical(x, [0, 0], cfg)
+    with pytest.raises(hv.InvalidArgument, match="train_online: batch_size must be >= 1"):
+        hv.train_online(x, [0, 0, 1], 0, cfg)
+    with pytest.raises(hv.InvalidArgument, match="predict: query dim != model dim"):
+        hv.predict(m, hv.PackedBitMatrix(1, 5))
+    # delta = 0 exact no-op; gamma = 0 exact (acceptance.cpp:255-291)
+    xs = hv.pack(Dn(np.array([[1, 0, 1, 1], [0, 1, 0, 0]], np.uint8)))
+    m = hv.train_classical(xs, [0, 1], hv.ModelConfig(class_count=2, seed=8))
+    before = m.accumulators.copy()
+    hv.online_update(m, hv.pack(Dn(np.array([[1, 0, 1, 1]], np.uint8))), [0], hv.freeze(m))
+    assert np.array_equal(m.accumulators, before) and m.sample_counts[0] == 2
+    m = hv.train_classical(xs, [0, 1], hv.ModelConfig(class_count=2, gamma=0.0, seed=9))
+    before = m.accumulators.copy()
+    hv.online_update(m, hv.pack(Dn(np.array([[1, 0, 1, 1]], np.uint8))), [1], hv.freeze(m))
+    assert np.array_equal(m.accumulators[:4], before[:4]) and m.accumulators[4] > before[4]
+    # predict known answers and lowest-index ties (test_model.cpp:298-320)
+    xx = hv.pack(Dn(np.array([[1, 1, 1, 1], [0, 0, 0, 0], [1, 1, 0, 0]], np.uint8)))
+    m = hv.train_classical(xx, [0, 1, 2], hv.ModelConfig(class_count=3, seed=12))
+    p = hv.predict(m, xx)
+    assert [q.label for q in p] == [0, 1, 2] and p[0].distances.tolist()[:2] == [0.0, 1.0]
+    tie = hv.predict(m, hv.pack(Dn(np.array([[1, 1, 0, 1]], np.uint8))))
+    assert tie[0].distances[0] == tie[0].distances[2] and tie[0].label == 0
+    # cosine: empty class never selected, zero query is a domain error
+    cm = hv.train_classical(hv.pack(Dn(np.array([[1, 1, 0, 0], [0, 0, 1, 1]], np.uint8))), [0, 1],
+                            hv.ModelConfig(class_count=3, metric=hv.Metric.kCosine, seed=14))
+    cp = hv.predict(cm, hv.pack(Dn(np.array([[1, 0, 0, 0], [0, 0, 0, 1]], np.uint8))))
+    assert [q.label for q in cp] == [0, 1] and cp[0].distances[2] == -np.inf
+    with pytest.raises(hv.DomainError):
+        hv.predict(cm, hv.PackedBitMatrix(1, 4))
+
+
+@pytest.mark.parametrize("bsz", [1, 7, 64, 1000])
+def test_online_random_vs_oracle_bitexact(bsz):
+    rng = np.random.default_rng(bsz)
+    C, D, n = 5, 1000, 700
+    centers = rng.integers(0, 2, (C, D), dtype=np.uint8)
+    y = rng.integers(0, C, n).astype(np.int32)
+    enc = O.pack_rows(centers[y] ^ (rng.random((n, D)) < 0.3).astype(np.uint8))
+    cfg = hv.ModelConfig(class_count=C, dim=D, gamma=0.7, seed=21)
+    on = hv.train_online(P(enc, D), y, bsz, cfg)
+    oo = O.NaiveModel(C, D, on.tiebreak.words, O.HAMMING, 0.7).train_online(enc, y, bsz)
+    np.testing.assert_array_equal(on.accumulators.reshape(C, D), oo.acc)
+    np.testing.assert_array_equal(on.class_weight, oo.weight)
+    np.testing.assert_array_equal(on.class_vectors.words, oo.class_vectors)
+
+
+# --------------------------------------------------- device pipeline ----
+def test_device_classical_and_predict_vs_oracle():
+    from paper_2206_04746_b200 import device as dv
+    F, B, D, C, rows = 617, 16, 10000, 26, 3000
+    cbk = dv.DeviceCodebook.make(F, B, D, seed=9)
+    eng = dv.Engine(cbk, C)
+    bins8, labels = eng.synth(0, rows, 0, 7)
+    enc = eng.encode(bins8)
+    cv, counts, crow = eng.train_classical(enc[:2400], labels[:2400])
+    pred = eng.predict(cv, enc[2400:])
+    eng.dc.check()
+    encn = enc.cpu().numpy().view(np.uint32)
+    yn = labels.cpu().numpy()
+    om = O.NaiveModel(C, D, cbk.model_tiebreak.cpu().numpy().view(np.uint32)).train_classical(encn[:2400], yn[:2400])
+    np.testing.assert_array_equal(counts[:, :D].cpu().numpy().astype(np.float64), om.acc)
+    np.testing.assert_array_equal(crow.cpu().numpy(), om.counts.astype(np.int64))
+    np.testing.assert_array_equal(cv.cpu().numpy().view(np.uint32), om.class_vectors)
+    ol, _ = om.predict(encn[2400:])
+    np.testing.assert_array_equal(pred.cpu().numpy(), ol)
+
+
+def test_device_online_delta_mode_emulated_ranks():
+    """Two ranks emulated on one GPU: delta-mode online training with the
+    all-reduce done by summing the two ranks' deltas. Accumulators within 1e-5
+    of the exact trainer, identical class vectors and labels (north star)."""
+    from paper_2206_04746_b200 import device as dv
+    import paper_2206_04746_b200._native as N
+    F, B, D, C, rows, bsz = 561, 16, 10000, 6, 4096, 256
+    cbk = dv.DeviceCodebook.make(F, B, D, seed=4)
+    eng = dv.Engine(cbk, C)
+    bins8, labels = eng.synth(0, rows, 0, 7)
+    enc = eng.encode(bins8)
+    acc_x, w_x, c_x, cv_x = eng.train_online(enc, labels, bsz)
+    # emulate world=2 by running each rank's delta on its slice and summing
+    world = 2
+    owned = [dv.shard_rows_online(rows, bsz, r, world) for r in range(world)]
+    shards = [(enc[o], labels[o]) for o in owned]
+    first = min(bsz, rows)
+    counts, crow = eng.zero_counts()
+    eng.class_counts(enc[:first], labels[:first], counts, crow)
+    acc = counts[:, :D].to(torch.float64).contiguous()
+    weight = crow.to(torch.float64)
+    cnt = crow.clone()
+    cv = eng.binarize(counts, crow)
+    offs = [0] * world
+    for start in range(0, rows, bsz):
+        n = min(bsz, rows - start)
+        tot = None
+        for r in range(world):
+            lo, hi = dv.online_slice(start, n, r, world)
+            k = hi - lo
+            e, y = shards[r]
+            d = [torch.empty_like(acc), torch.empty_like(weight), torch.empty_like(cnt),
+                 torch.empty(C, dtype=torch.int32, device=acc.device)]
+            N.check(N.lib().hv_dev_online_delta(eng.dc.h, dv._ptr(cv), C, D, dv._ptr(e[offs[r]:offs[r] + k]), k,
+                                                dv._ptr(y[offs[r]:offs[r] + k]), 1.0, *[dv._ptr(t) for t in d]))
+            offs[r] += k
+            tot = d if tot is None else [a + b for a, b in zip(tot, d)]
+        N.check(N.lib().hv_dev_apply_online_delta(eng.dc.h, C, D, *[dv._ptr(t) for t in tot],
+                                                  dv._ptr(cbk.model_tiebreak), dv._ptr(acc), dv._ptr(weight),
+                                                  dv._ptr(cnt), dv._ptr(cv)))
+    torch.cuda.synchronize()
+    rel = ((acc - acc_x).abs() / acc_x.abs().clamp_min(1.0)).max().item()
+    assert rel <= 1e-5, rel
+    assert torch.equal(cnt, c_x)
+    assert torch.equal(cv, cv_x)
+    assert torch.equal(eng.predict(cv, enc), eng.predict(cv_x, enc))
