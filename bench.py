@@ -1,0 +1,449 @@
+"""bench.py — encode+train+infer datapoints/s on the CHB-MIT-shaped workload.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W [--impl reference]`,
+N>1 under torchrun (one rank per GPU, NCCL). Prints ONE JSON line on rank 0.
+
+Workload (BASELINE.json metric "encode+train+infer datapoints/sec at D=10k,
+1/2/4/8 B200"; configs[3] CHB-MIT-shaped: ~7.06 M datapoints, 2 classes,
+unbalanced; F = 342 features = 19 x 18 channels, B = 16 bins, D = 10000),
+synthetic data from the shared counter-based generator
+(include/hvb200_synth.h). A step is one run_fold_packed pass
+(experiment.cpp:159-177) minus discretize, on one fold = a chronological
+80/20 split (data.cpp:245-257):
+    encode all rows -> classical train on the train rows -> predict the test rows.
+Datapoints are sharded across ranks (strong scaling: the dataset is fixed);
+training all-reduces the C x 32W uint32 class counts over NCCL; prediction
+needs no collective.
+
+value      : device-resident (bins already in HBM) whole-job datapoints/s.
+e2e        : the same step through the C-ABI fold entry points with HOST
+             buffers (uint32 bins in, predicted labels out), PCIe inside.
+roofline   : dominant kernel (the encoder) against the measured HBM peak,
+             plus its integer-pipe fraction (the binding ceiling).
+cpu_baseline: the reference library (oracle/_ref, built from the reference
+             sources) on a bounded sample, all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "encode+train+infer datapoints/sec at D=10k, 1/2/4/8 B200; HBM GB/s vs roofline"
+WORKLOAD = dict(workload="chbmit", features=342, classes=2, dim=10000, rows=7_060_000, bins=16,
+                label_kind=1, data_seed=7, seed=1)
+REF_BENCH = ROOT / "oracle" / "_ref" / "ref_bench"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--rows", type=int, default=WORKLOAD["rows"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--online", action="store_true", help="also time the exact online trainer (extra field)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def split(rows):
+    train = min(rows - 1, max(1, rows * 4 // 5))
+    return train, rows - train
+
+
+# ------------------------------------------------------------ clocks ----
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during timing."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self, gpus):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or not f[0].isdigit() or int(f[0]) not in gpus:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------- reference ----
+def run_ref_bench(rows, threads, reps=1, timeout=600):
+    w = WORKLOAD
+    cmd = [str(REF_BENCH), "--features", str(w["features"]), "--classes", str(w["classes"]), "--dim", str(w["dim"]),
+           "--rows", str(rows), "--bins", str(w["bins"]), "--threads", str(threads), "--labels", "chbmit",
+           "--trainer", "classical", "--seed", str(w["seed"]), "--data-seed", str(w["data_seed"]), "--reps", str(reps)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline(target_s=10.0):
+    """Reference CPU implementation on a bounded prefix sample, all host cores."""
+    if not REF_BENCH.exists():
+        return None
+    threads = os.cpu_count() or 1
+    cal = run_ref_bench(2048, threads)
+    rows = int(min(400_000, max(4096, 2048 * target_s / max(cal["total_s"], 1e-3))))
+    res = run_ref_bench(rows, threads)
+    return {"value": round(res["dp_per_s"], 3), "unit": "datapoints/s", "cores": threads, "kind": "reference",
+            "sample": f"first {rows} rows of the workload (80/20 split), reference encode_batch/train_classical/"
+                      f"predict with threads={threads}; {res['total_s']:.2f} s",
+            "stages_s": {k: res[k] for k in ("encode_s", "train_s", "predict_s")}}
+
+
+def impl_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    if not REF_BENCH.exists():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_bench not built (needs /root/reference)"}))
+        return
+    cal = run_ref_bench(2048, threads)
+    # each step is a bounded sample sized so warmup+steps stay within a few minutes
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    rows = int(min(400_000, max(2048, 2048 * budget / max(cal["total_s"], 1e-3))))
+    for _ in range(args.warmup):
+        run_ref_bench(rows, threads)
+    times = []
+    for _ in range(args.steps):
+        r = run_ref_bench(rows, threads)
+        times.append(r["total_s"])
+    t = sum(times) / len(times)
+    v = rows / t
+    w = WORKLOAD
+    line = {"metric": METRIC, "value": round(v, 3), "unit": "datapoints/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic (include/hvb200_synth.h, CHB-MIT-shaped)",
+            "impl": "reference",
+            "config": {"workload": w["workload"], "features": w["features"], "classes": w["classes"], "dim": w["dim"],
+                       "rows": rows, "full_rows": args.rows, "trainer": "classical"},
+            "cpu_baseline": {"value": round(v, 3), "unit": "datapoints/s", "cores": threads, "kind": "reference",
+                             "sample": f"first {rows} rows per step (of {args.rows}), threads={threads}"},
+            "e2e": {"value": round(v, 3), "unit": "datapoints/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ engine ----
+def impl_engine(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2206_04746_b200 import _native as N
+    from paper_2206_04746_b200 import device as dv
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = WORKLOAD
+    F, Cc, D, B = w["features"], w["classes"], w["dim"], w["bins"]
+    W = (D + 31) // 32
+    rows = args.rows
+    ntrain, ntest = split(rows)
+    tr_lo, tr_hi = dv.shard_range(ntrain, rank, world)
+    te_lo, te_hi = dv.shard_range(ntest, rank, world)
+    te_lo += ntrain
+    te_hi += ntrain
+    n_tr, n_te = tr_hi - tr_lo, te_hi - te_lo
+
+    cbk = dv.DeviceCodebook.make(F, B, D, seed=w["seed"], device=local)
+    eng = dv.Engine(cbk, Cc, device=local)
+    # HBM-resident inputs of this rank: its train shard then its test shard (uint8 bins, 64 B pitch)
+    bt, yt = eng.synth(tr_lo, n_tr, w["label_kind"], w["data_seed"])
+    bs, _ = eng.synth(te_lo, n_te, w["label_kind"], w["data_seed"])
+    bins8 = torch.cat([bt, bs])
+    del bt, bs
+    enc = torch.empty((n_tr + n_te, W), dtype=torch.int32, device=eng.dev)
+    counts, crow = eng.zero_counts()
+    cv = torch.empty((Cc, W), dtype=torch.int32, device=eng.dev)
+    pred = torch.empty(n_te, dtype=torch.int32, device=eng.dev)
+    stream = torch.cuda.current_stream()
+    eng.dc.bind(stream)
+
+    enc_ev = []
+
+    def step(record=False):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.encode(bins8, out=enc)
+        e1.record(stream)
+        if record:
+            enc_ev.append((e0, e1))
+        counts.zero_()
+        crow.zero_()
+        eng.class_counts(enc[:n_tr], yt, counts, crow)
+        if world > 1:
+            dist.all_reduce(counts)
+            dist.all_reduce(crow)
+        eng.binarize(counts, crow, out=cv)
+        eng.predict(cv, enc[n_tr:], labels=pred)
+
+    for _ in range(args.warmup):
+        step()
+    eng.dc.check()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler()
+    if rank == 0:
+        sampler.start()
+        time.sleep(0.3)
+    launches0 = N.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(record=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    launches = N.launch_count() - launches0
+    enc_ms = [a.elapsed_time(b) for a, b in enc_ev]
+    if world > 1:
+        t = torch.tensor([ms, float(launches)], dtype=torch.float64, device=eng.dev)
+        tm = t.clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        ms, launches = tm[0].item(), int(t[1].item())
+    clocks = sampler.stop(set(range(torch.cuda.device_count()))) if rank == 0 else None
+
+    ms_step = ms / args.steps
+    value = rows / (ms_step / 1e3)
+
+    # parity spot check of the timed result against the oracle (outside timing)
+    check = None
+    if rank == 0:
+        try:
+            sys.path.insert(0, str(ROOT / "tests"))
+            import oracle_ref as O
+            idx = np.array([0, 1, 17, n_tr - 1, n_tr, n_tr + n_te - 1])
+            idx = idx[(idx >= 0) & (idx < n_tr + n_te)]
+            gl = np.where(idx < n_tr, tr_lo + idx, te_lo + (idx - n_tr))
+            b = np.stack([O.synth_c(int(g), 1, F, Cc, B, w["label_kind"], w["data_seed"])[0][0] for g in gl])
+            want = O.encode_batch(b, cbk.id_vectors.cpu().numpy().view(np.uint32),
+                                  cbk.value_vectors.cpu().numpy().view(np.uint32), B, D, O.BIND_ID_LEVEL,
+                                  cbk.encode_tiebreak.cpu().numpy().view(np.uint32))
+            check = bool(np.array_equal(enc[idx].cpu().numpy().view(np.uint32), want))
+        except Exception as e:  # pragma: no cover - reporting only
+            check = f"skipped: {e}"
+
+    # ---- roofline of the dominant kernel (encoder) ----
+    enc_avg_ms = sum(enc_ms) / max(1, len(enc_ms))
+    local_rows = n_tr + n_te
+    alg_bytes = local_rows * (F + 4 * W)           # bins in (F B) + HVs out (4W B)
+    achieved_gbs = alg_bytes / (enc_avg_ms / 1e3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    sm_mhz = (clocks or {}).get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    # integer-pipe ceiling: every bound word needs >= 2 LOP3 (full adder) on the
+    # 64-lane/clk/SM ALU pipe -> peak bound words/s = SMs * 64 * f / 2
+    bound_words = local_rows * F * W
+    int_achieved = bound_words / (enc_avg_ms / 1e3) / 1e9
+    int_peak = sms * 64 * sm_mhz * 1e6 / 2 / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "encode_dram_bytes.json"
+    if prof.exists():
+        try:
+            p = json.loads(prof.read_text())
+            traffic = p.get("dram_bytes_per_row", 0) * local_rows or None
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the C ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, rank, world, local, rows, ntrain, ntest, (tr_lo, tr_hi), (te_lo, te_hi), eng, cbk)
+
+    online = None
+    if args.online and world == 1:
+        torch.cuda.synchronize()
+        s0 = time.perf_counter()
+        eng.train_online(enc[:n_tr], yt, 1024)
+        torch.cuda.synchronize()
+        online = {"rows": n_tr, "batch_size": 1024, "seconds": round(time.perf_counter() - s0, 4),
+                  "dp_per_s": round(n_tr / (time.perf_counter() - s0), 1)}
+
+    if rank == 0:
+        base = None if args.no_cpu else cpu_baseline()
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "datapoints/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32 (packed binary hypervectors), int32 counts",
+            "data": "synthetic: counter-based CHB-MIT-shaped generator (include/hvb200_synth.h)",
+            "config": {"workload": w["workload"], "features": F, "classes": Cc, "dim": D, "bins": B, "rows": rows,
+                       "train_rows": ntrain, "test_rows": ntest, "trainer": "classical", "binding": "id_level",
+                       "parallelism": f"dp{world} (datapoint shards, NCCL all-reduce of class counts)",
+                       "l2": "inputs larger than L2 (uint8 bins %.2f GB + HVs %.2f GB per step vs 126 MB L2)" % (
+                           (n_tr + n_te) * dv.bins_pitch(F) / 1e9, (n_tr + n_te) * 4 * W / 1e9)},
+            "roofline": {"bound": "hbm", "kernel": "encode_tt_kernel", "achieved": round(achieved_gbs, 2),
+                         "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved_gbs / hbm_peak, 5),
+                         "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_row": F + 4 * W, "avg_launch_ms": round(enc_avg_ms, 4),
+                         "int_pipe": {"achieved_gwords_s": round(int_achieved, 1), "peak_gwords_s": round(int_peak, 1),
+                                      "frac": round(int_achieved / int_peak, 4),
+                                      "model": "bound words (F*W per row) vs SMs*64 lanes*f_sm/2 (2 LOP3 per word)"}},
+            "cpu_baseline": base,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "stage_encode_ms": round(enc_avg_ms, 3),
+            "parity_check": check,
+        }
+        if online:
+            line["online_extra"] = online
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, rank, world, local, rows, ntrain, ntest, tr, te, eng, cbk):
+    """Same step through hv_fold_* with pinned host uint32 bins and host labels out."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2206_04746_b200 import _native as N
+
+    w = WORKLOAD
+    F, Cc, D = w["features"], w["classes"], w["dim"]
+    W = (D + 31) // 32
+    n_tr, n_te = tr[1] - tr[0], te[1] - te[0]
+    # host inputs (uint32 bins, the reference API type) in pinned memory
+    b32 = torch.empty((n_tr + n_te, F), dtype=torch.int32, pin_memory=True)
+    lab = torch.empty(n_tr, dtype=torch.int32, pin_memory=True)
+    bt, yt = eng.synth(tr[0], n_tr, w["label_kind"], w["data_seed"])
+    bs, _ = eng.synth(te[0], n_te, w["label_kind"], w["data_seed"])
+    b32.copy_(torch.cat([bt[:, :F], bs[:, :F]]).to(torch.int32).cpu())
+    lab.copy_(yt.cpu())
+    del bt, bs
+    idv = cbk.id_vectors.cpu().numpy()
+    val = cbk.value_vectors.cpu().numpy()
+    etb = cbk.encode_tiebreak.cpu().numpy()
+    mtb = cbk.model_tiebreak.cpu().numpy()
+    out = np.zeros(n_te, np.int32)
+    L = N.lib()
+    ctx = eng.dc.ctx
+    ctx.set_stream(None)  # the fold API runs on the context's own streams
+    p = lambda a: C.c_void_p(a.ctypes.data) if isinstance(a, np.ndarray) else C.c_void_p(a.data_ptr())
+    def one():
+        f = C.c_void_p()
+        N.check(L.hv_fold_encode_train(ctx.handle, p(b32), n_tr, p(lab), C.c_void_p(b32.data_ptr() + n_tr * F * 4),
+                                       n_te, F, p(idv), p(val), w["bins"], D, p(etb), Cc, C.byref(f)))
+        if world > 1:
+            cp, rp = C.c_void_p(), C.c_void_p()
+            N.check(L.hv_fold_counts(f, C.byref(cp), C.byref(rp)))
+            ct = _wrap_device(cp.value, (Cc * 32 * W,), torch.int32, local)
+            rt = _wrap_device(rp.value, (Cc,), torch.int64, local)
+            torch.cuda.synchronize()
+            dist.all_reduce(ct)
+            dist.all_reduce(rt)
+            torch.cuda.synchronize()
+        N.check(L.hv_fold_predict(ctx.handle, f, p(mtb), p(out)))
+        L.hv_fold_destroy(f)
+
+    one()  # warm-up (allocator pool, first-touch)
+    if world > 1:
+        dist.barrier()
+    times = []
+    for _ in range(max(1, min(args.steps, 3))):
+        s = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - s)
+    t = sum(times) / len(times)
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = tt.item()
+    eng.dc.bind()
+    h2d = (n_tr + n_te) * F * 4 + n_tr * 4 + idv.nbytes + val.nbytes + etb.nbytes + mtb.nbytes
+    d2h = n_te * 4
+    if world > 1:
+        h2d_t = torch.tensor([h2d, d2h], dtype=torch.int64, device=f"cuda:{local}")
+        dist.all_reduce(h2d_t)
+        h2d, d2h = int(h2d_t[0].item()), int(h2d_t[1].item())
+    return {"value": round(rows / t, 1), "unit": "datapoints/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "api": "hv_fold_encode_train + hv_fold_predict (C ABI, host uint32 bins in, host labels out)",
+            "seconds_per_step": round(t, 4)}
+
+
+def _wrap_device(ptr, shape, dtype, device):
+    """Zero-copy torch view of a device pointer owned by libhvb200."""
+    import torch
+
+    class _CAI:
+        def __init__(self):
+            typestr = {torch.int32: "<i4", torch.int64: "<i8"}[dtype]
+            self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False), "version": 3,
+                                             "strides": None, "stream": None}
+
+    return torch.as_tensor(_CAI(), device=f"cuda:{device}")
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        impl_reference(args)
+    else:
+        impl_engine(args)
+
+
+if __name__ == "__main__":
+    main()

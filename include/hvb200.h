@@ -167,6 +167,23 @@ hv_status hv_train_online(hv_context* ctx, const uint32_t* encoded, size_t rows,
 /* model.hpp:110-111 predict: labels_out rows; distances_out rows x class_count (nullable) */
 hv_status hv_predict(hv_context* ctx, const hv_model* model, const uint32_t* encoded,
                      size_t rows, size_t dim, int32_t* labels_out, double* distances_out);
+/* ---- one fold of the reference pipeline (experiment.cpp:159-177) ------- */
+/* run_fold_packed minus discretize: encode_batch(train) + encode_batch(test)
+ * -> train_classical -> predict, with the encoded hypervectors kept in HBM
+ * (they never cross PCIe). Split in two calls so a data-parallel caller can
+ * all-reduce the class counts in between (hv_fold_counts). */
+typedef struct hv_fold hv_fold;
+hv_status hv_fold_encode_train(hv_context* ctx, const uint32_t* train_bins, size_t train_rows,
+                               const int32_t* train_labels, const uint32_t* test_bins,
+                               size_t test_rows, size_t features, const uint32_t* id_vectors,
+                               const uint32_t* value_vectors, size_t bins, size_t dim,
+                               const uint32_t* encode_tiebreak, size_t class_count, hv_fold** out);
+/* device pointers of the fold's class counts (class_count x 32*W uint32) and class rows (uint64) */
+hv_status hv_fold_counts(hv_fold* fold, void** counts_dev, void** class_rows_dev);
+/* binarise with the model tiebreak (1 x W host words) and predict the test rows into labels_out (host) */
+hv_status hv_fold_predict(hv_context* ctx, hv_fold* fold, const uint32_t* model_tiebreak, int32_t* labels_out);
+void hv_fold_destroy(hv_fold* fold);
+
 /* model.hpp:67-70 hamming_distance_words (host-side helper, no device) */
 double hv_hamming_distance_words(const uint32_t* a, const uint32_t* b, size_t dim);
 

@@ -398,7 +398,7 @@ bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
 // Encodes validated uint8 bins on stream `st`.
 void encode_device(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, size_t ldb, size_t rows, size_t F,
                    const uint32_t* id, const uint32_t* val, size_t B, size_t D, hv_binding binding,
-                   const uint32_t* tie, uint32_t* out, bool allow_fast = true) {
+                   const uint32_t* tie, uint32_t* out, bool allow_fast) {
   const size_t W = words_per_row(D);
   if (rows == 0 || W == 0) return;
   if (D > 0xFFFFFFFFull || F > 0xFFFFFFFFull) invalid("encode: shape too large");
@@ -441,8 +441,6 @@ void narrow_device(hv_context* ctx, cudaStream_t st, const uint32_t* bins32, siz
                                           static_cast<uint32_t>(ldb), flat_base, ctx->d_err);
   launched("narrow_bins_kernel");
 }
-
-inline size_t bins_pitch(size_t F) { return (F + 63) / 64 * 64; }
 
 }  // namespace hvb
 

@@ -100,6 +100,16 @@ struct DevBuf {
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), n(o.n), stream(o.stream) { o.ptr = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      if (ptr) cudaFreeAsync(ptr, stream);
+      ptr = o.ptr;
+      n = o.n;
+      stream = o.stream;
+      o.ptr = nullptr;
+    }
+    return *this;
+  }
   ~DevBuf() {
     if (ptr) cudaFreeAsync(ptr, stream);
   }
@@ -132,6 +142,14 @@ inline unsigned grid_for(size_t n, unsigned block, unsigned cap = 1u << 30) {
 // Column counts over a permuted, class-segmented row sequence (hv_bits.cu).
 void launch_column_count_u32(cudaStream_t st, const uint32_t* m, uint32_t W, const uint32_t* perm,
                              const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, uint32_t* counts);
+
+// Encoder entry points shared with the fold pipeline (hv_encode.cu).
+void encode_device(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, size_t ldb, size_t rows, size_t F,
+                   const uint32_t* id, const uint32_t* val, size_t B, size_t D, hv_binding binding,
+                   const uint32_t* tie, uint32_t* out, bool allow_fast = true);
+void narrow_device(hv_context* ctx, cudaStream_t st, const uint32_t* bins32, size_t rows, size_t F, size_t B,
+                   uint8_t* bins8, size_t ldb, uint64_t flat_base);
+inline size_t bins_pitch(size_t F) { return (F + 63) / 64 * 64; }
 
 // Host-side codebook helpers shared by several entry points (hv_host.cpp).
 void generate_random_words(size_t count, size_t dim, uint64_t seed, uint32_t* out);

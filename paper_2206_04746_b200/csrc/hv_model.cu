@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <limits>
+#include <memory>
 #include <vector>
 
 #include "hv_internal.cuh"
@@ -854,5 +855,130 @@ hv_status hv_dev_apply_online_delta(hv_context* ctx, size_t class_count, size_t 
     refresh_device(ctx, st, acc, weight, touched, C, D, tiebreak, class_vectors);
   });
 }
+
+}  // extern "C"
+
+// ------------------------------------------------------------- fold ----
+// experiment.cpp:159-177 with HBM-resident hypervectors.
+struct hv_fold {
+  size_t train_rows = 0, test_rows = 0, F = 0, D = 0, W = 0, C = 0;
+  hvb::DevBuf<uint32_t> enc, counts;
+  hvb::DevBuf<uint64_t> class_rows;
+};
+
+namespace hvb {
+namespace {
+
+// Chunked, double-buffered upload + narrow + encode of host uint32 bins into `out`.
+void encode_host_rows(hv_context* ctx, const uint32_t* bins, size_t rows, size_t F, size_t B, size_t D,
+                      const uint32_t* d_id, const uint32_t* d_val, const uint32_t* d_tie, uint32_t* out,
+                      uint64_t flat_base, DevBuf<uint32_t>* b32, DevBuf<uint8_t>* b8, size_t chunk, size_t& k) {
+  const size_t W = words_per_row(D), ldb = bins_pitch(F);
+  cudaStream_t streams[2] = {ctx->stream, ctx->aux};
+  for (size_t r0 = 0; r0 < rows; r0 += chunk, ++k) {
+    const size_t n = std::min(chunk, rows - r0);
+    cudaStream_t st = streams[k & 1];
+    ck(cudaMemcpyAsync(b32[k & 1].ptr, bins + r0 * F, n * F * 4, cudaMemcpyHostToDevice, st), "H2D bins");
+    narrow_device(ctx, st, b32[k & 1].ptr, n, F, B, b8[k & 1].ptr, ldb, flat_base + r0 * F);
+    encode_device(ctx, st, b8[k & 1].ptr, ldb, n, F, d_id, d_val, B, D, HV_BIND_ID_LEVEL, d_tie, out + r0 * W);
+  }
+}
+
+}  // namespace
+}  // namespace hvb
+
+extern "C" {
+
+hv_status hv_fold_encode_train(hv_context* ctx, const uint32_t* train_bins, size_t train_rows,
+                               const int32_t* train_labels, const uint32_t* test_bins, size_t test_rows,
+                               size_t features, const uint32_t* id_vectors, const uint32_t* value_vectors,
+                               size_t bins, size_t dim, const uint32_t* encode_tiebreak, size_t class_count,
+                               hv_fold** out) {
+  return guarded([&] {
+    require(ctx);
+    if (!out) invalid("fold: null output");
+    *out = nullptr;
+    if (features == 0 || dim == 0 || class_count == 0) invalid("fold: features, dim and classes must be >= 1");
+    auto fold = std::make_unique<hv_fold>();
+    const size_t W = words_per_row(dim), ldb = bins_pitch(features), rows = train_rows + test_rows;
+    fold->train_rows = train_rows;
+    fold->test_rows = test_rows;
+    fold->F = features;
+    fold->D = dim;
+    fold->W = W;
+    fold->C = class_count;
+    cudaStream_t st = ctx->stream;
+    fold->enc = DevBuf<uint32_t>(rows * W, st);
+    fold->counts = DevBuf<uint32_t>(class_count * 32 * W, st);
+    fold->class_rows = DevBuf<uint64_t>(class_count, st);
+    fold->counts.zero();
+    fold->class_rows.zero();
+    DevBuf<uint32_t> d_id(features * W, st), d_val(bins * W, st), d_tie(W, st);
+    DevBuf<int32_t> d_y(train_rows, st);
+    d_id.upload(id_vectors);
+    d_val.upload(value_vectors);
+    d_tie.upload(encode_tiebreak);
+    d_y.upload(train_labels);
+    const size_t chunk = std::max<size_t>(1, std::min<size_t>(std::max<size_t>(rows, 1), (size_t(128) << 20) / (features * 4)));
+    DevBuf<uint32_t> b32[2] = {DevBuf<uint32_t>(chunk * features, st), DevBuf<uint32_t>(chunk * features, st)};
+    DevBuf<uint8_t> b8[2] = {DevBuf<uint8_t>(chunk * ldb, st), DevBuf<uint8_t>(chunk * ldb, st)};
+    sync(ctx);
+    size_t k = 0;
+    encode_host_rows(ctx, train_bins, train_rows, features, bins, dim, d_id.ptr, d_val.ptr, d_tie.ptr, fold->enc.ptr,
+                     0, b32, b8, chunk, k);
+    // classical counts of the train rows overlap the upload/encode of the test rows
+    cudaEvent_t ev;
+    ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    ck(cudaEventRecord(ev, ctx->aux), "event");
+    ck(cudaStreamWaitEvent(ctx->stream, ev, 0), "wait");
+    cudaEventDestroy(ev);
+    class_counts_device(ctx, ctx->stream, fold->enc.ptr, train_rows, W, d_y.ptr, class_count, fold->counts.ptr,
+                        fold->class_rows.ptr);
+    encode_host_rows(ctx, test_bins, test_rows, features, bins, dim, d_id.ptr, d_val.ptr, d_tie.ptr,
+                     fold->enc.ptr + train_rows * W, train_rows * features, b32, b8, chunk, k);
+    ck(cudaStreamSynchronize(ctx->aux), "sync aux");
+    sync(ctx);
+    unsigned long long l[kErrKinds];
+    read_latch(ctx, l);
+    if (l[kErrBin] != ~0ull || l[kErrLabel] != ~0ull) {
+      reset_latch(ctx);
+      if (l[kErrLabel] != ~0ull) {
+        invalid("train_classical: label " + std::to_string(train_labels[l[kErrLabel]]) + " at row " +
+                std::to_string(l[kErrLabel]) + " out of range (classes = " + std::to_string(class_count) + ")");
+      }
+      const uint64_t idx = l[kErrBin];
+      const uint32_t b = idx < train_rows * features ? train_bins[idx] : test_bins[idx - train_rows * features];
+      invalid("encode: feature " + std::to_string(idx % features) + " bin index " + std::to_string(b) +
+              " out of range (bins = " + std::to_string(bins) + ")");
+    }
+    *out = fold.release();
+  });
+}
+
+hv_status hv_fold_counts(hv_fold* fold, void** counts_dev, void** class_rows_dev) {
+  return guarded([&] {
+    if (!fold) invalid("fold: null");
+    if (counts_dev) *counts_dev = fold->counts.ptr;
+    if (class_rows_dev) *class_rows_dev = fold->class_rows.ptr;
+  });
+}
+
+hv_status hv_fold_predict(hv_context* ctx, hv_fold* fold, const uint32_t* model_tiebreak, int32_t* labels_out) {
+  return guarded([&] {
+    require(ctx);
+    if (!fold) invalid("fold: null");
+    cudaStream_t st = ctx->stream;
+    DevBuf<uint32_t> tie(fold->W, st), cv(fold->C * fold->W, st);
+    DevBuf<int32_t> lab(fold->test_rows, st);
+    tie.upload(model_tiebreak);
+    binarize_counts_device(ctx, st, fold->counts.ptr, fold->class_rows.ptr, fold->C, fold->D, tie.ptr, cv.ptr);
+    predict_hamming_device(ctx, st, cv.ptr, fold->C, fold->D, fold->enc.ptr + fold->train_rows * fold->W,
+                           fold->test_rows, lab.ptr, nullptr, nullptr);
+    lab.download(labels_out);
+    sync(ctx);
+  });
+}
+
+void hv_fold_destroy(hv_fold* fold) { delete fold; }
 
 }  // extern "C"

