@@ -182,6 +182,8 @@ def impl_engine(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # one non-default stream for everything (library kernels, torch ops, NCCL)
+    torch.cuda.set_stream(torch.cuda.Stream(local))
     w = WORKLOAD
     F, Cc, D, B = w["features"], w["classes"], w["dim"], w["bins"]
     W = (D + 31) // 32

@@ -75,7 +75,8 @@ uint64_t hv_kernel_launch_count(void);
 
 hv_status hv_context_create(int device, hv_context** out);
 void hv_context_destroy(hv_context* ctx);
-/* Route hv_dev_* work onto an existing cudaStream_t (NULL = the context's own stream). */
+/* Route hv_dev_* work onto an existing cudaStream_t (NULL = the context's own stream;
+ * pass cudaStreamLegacy, (void*)0x1, for the legacy default stream). */
 hv_status hv_context_set_stream(hv_context* ctx, void* cuda_stream);
 void* hv_context_stream(hv_context* ctx);
 hv_status hv_context_synchronize(hv_context* ctx);

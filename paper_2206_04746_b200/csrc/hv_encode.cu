@@ -194,128 +194,6 @@ __global__ void encode_append_kernel(const uint8_t* __restrict__ bins8, uint32_t
   }
 }
 
-// ---------------------------------------------- fast ID-level encoder ----
-// Work item = (slice of NC output words, tile of 32*G datapoints). Warp
-// (c, g) of the CTA computes output word slice_base + c for the 32 datapoints
-// of group g, lane = datapoint. Shared memory holds
-//   T[c][f][b]  = ID_f[w_c] ^ V_b[w_c]                 (NC * F16 * 16 words)
-//   S[g][buf]   = bins of group g's 32 rows for a 64-feature chunk,
-//                 stored feature-major with a lane-permuting swizzle so that
-//                 the per-lane 4-byte reads are bank-conflict free.
-// A lane's T address is chunk_base + (f*16 + b)*4: one byte extract, one
-// address add and one conflict-free LDS per bound word.
-constexpr int kTTBins = 16;     // table rows per feature (B <= 16)
-constexpr int kTTChunk = 64;    // features per staged chunk
-
-struct TTParams {
-  const uint8_t* bins8;
-  uint32_t ldb;
-  uint64_t rows;
-  uint32_t F, F16, D, W;
-  const uint32_t* id;
-  const uint32_t* val;
-  uint32_t B;
-  const uint32_t* tie;
-  uint32_t* out;
-  uint32_t slices;      // ceil(W / NC)
-  uint64_t tiles;       // ceil(rows / (32*G))
-};
-
-template <int NC, int G, int NH>
-__global__ void __launch_bounds__(NC * G * 32, 1) encode_tt_kernel(TTParams p) {
-  extern __shared__ __align__(16) uint32_t smem[];
-  const uint32_t tsz = p.F16 * kTTBins;          // words per table
-  uint32_t* T = smem;                             // NC tables
-  uint32_t* S = smem + NC * tsz;                  // G groups x 2 buffers x 512 words
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int c = warp % NC;
-  const int g = warp / NC;
-  const uint64_t items = static_cast<uint64_t>(p.slices) * p.tiles;
-  const uint32_t nthreads = NC * G * 32;
-  const uint32_t nchunks = (p.F16 + kTTChunk - 1) / kTTChunk;
-
-  // contiguous range of items per CTA, slice-major so the tables are reused
-  const uint64_t per = (items + gridDim.x - 1) / gridDim.x;
-  const uint64_t it0 = blockIdx.x * per;
-  const uint64_t it1 = min(items, it0 + per);
-  uint32_t cur_slice = 0xFFFFFFFFu;
-
-  for (uint64_t it = it0; it < it1; ++it) {
-    const uint32_t slice = static_cast<uint32_t>(it / p.tiles);
-    const uint64_t tile = it % p.tiles;
-    if (slice != cur_slice) {
-      __syncthreads();
-      // build NC tables: T[cc][f][b] = ID[f][w] ^ V[b][w] (zero rows for f >= F, b >= B, w >= W)
-      for (uint32_t k = threadIdx.x; k < NC * tsz; k += nthreads) {
-        const uint32_t cc = k / tsz;
-        const uint32_t rem = k % tsz;
-        const uint32_t f = rem / kTTBins;
-        const uint32_t b = rem % kTTBins;
-        const uint32_t w = slice * NC + cc;
-        uint32_t v = 0;
-        if (w < p.W && f < p.F && b < p.B) {
-          v = p.id[static_cast<uint64_t>(f) * p.W + w] ^ p.val[static_cast<uint64_t>(b) * p.W + w];
-        }
-        T[k] = v;
-      }
-      cur_slice = slice;
-      __syncthreads();
-    }
-    const uint32_t w = slice * NC + c;
-    const uint64_t row0 = tile * (32ull * G) + 32ull * g;
-    const uint32_t* Tc = T + c * tsz;
-    HSCounter<NH> h;
-    for (uint32_t ch = 0; ch < nchunks; ++ch) {
-      // stage chunk ch of each group's 32 rows: 32 rows x 64 bytes, cooperatively by
-      // the NC warps of the group; word q (4 features) of row k lands at
-      // S[q*32 + (k ^ swz(q))] with swz chosen so both the staging stores and the
-      // per-lane reads below are conflict free.
-      __syncthreads();
-      for (uint32_t k = threadIdx.x; k < G * 32 * 16; k += nthreads) {
-        const uint32_t gg = k / (32 * 16);
-        const uint32_t rem = k % (32 * 16);
-        const uint32_t row = rem / 16;   // 0..31 (a warp reads 2 rows x 64 contiguous bytes)
-        const uint32_t q = rem % 16;     // word within the 64-byte chunk
-        const uint64_t grow = tile * (32ull * G) + 32ull * gg + row;
-        const uint32_t f0 = ch * kTTChunk + q * 4;
-        uint32_t v = 0;
-        if (grow < p.rows && f0 < p.ldb) {
-          v = *reinterpret_cast<const uint32_t*>(p.bins8 + grow * p.ldb + f0);
-        }
-        // feature-major with a (row + 2q) rotation: conflict-free for these
-        // stores (2 rows x 16 q per warp) and for the per-lane reads below.
-        S[gg * 512 + q * 32 + ((row + 2 * q) & 31u)] = v;
-      }
-      __syncthreads();
-      const uint32_t* Sg = S + g * 512;
-      const uint32_t fbase = ch * kTTChunk;
-      const uint32_t nf = min(static_cast<uint32_t>(kTTChunk), p.F16 - fbase);  // multiple of 16
-      const uint32_t* Tch = Tc + fbase * kTTBins;
-      for (uint32_t f16 = 0; f16 < nf; f16 += 16) {
-        uint32_t x[16];
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const uint32_t q = (f16 >> 2) + q4;
-          const uint32_t bq = Sg[q * 32 + ((lane + 2 * q) & 31u)];
-          const uint32_t* Tq = Tch + (q * 4) * kTTBins;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) x[q4 * 4 + t] = Tq[t * kTTBins + __byte_perm(bq, 0, 0x4440 | t)];
-        }
-        h.add16(x);
-      }
-    }
-    const uint64_t row = row0 + lane;
-    if (w < p.W && row < p.rows) {
-      p.out[row * p.W + w] = h.majority(p.F, p.tie[w]) & valid_mask(w, p.D);
-    }
-  }
-}
-
-struct TTConfig {
-  int nc = 0, g = 0;
-  size_t smem = 0;
-};
 
 }  // namespace hvb
 
@@ -341,58 +219,6 @@ void launch_generic(hv_context* ctx, cudaStream_t st, int nh, const uint8_t* bin
   }
 #undef HV_GEN_CASE
   launched("encode_generic_kernel");
-}
-
-template <int NC, int G, int NH>
-void launch_tt_inst(hv_context* ctx, cudaStream_t st, const TTParams& p, size_t smem) {
-  auto kern = encode_tt_kernel<NC, G, NH>;
-  static bool configured = false;
-  if (!configured) {
-    ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem > 48 * 1024 ? 227 * 1024 : 48 * 1024)), "cudaFuncSetAttribute");
-    configured = true;
-  }
-  int per_sm = 0;
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NC * G * 32, smem), "occupancy");
-  if (per_sm < 1) per_sm = 1;
-  const uint64_t items = static_cast<uint64_t>(p.slices) * p.tiles;
-  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(ctx->sm_count) * per_sm));
-  kern<<<grid, NC * G * 32, smem, st>>>(p);
-  launched("encode_tt_kernel");
-}
-
-// Returns false when the fast path does not apply.
-bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
-               const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
-               uint32_t* out) {
-  if (B > static_cast<uint32_t>(kTTBins) || F == 0 || rows == 0) return false;
-  if (ldb % 64 != 0 || (reinterpret_cast<uintptr_t>(bins8) & 15u)) return false;
-  const int nh = hs_high_planes(F);
-  if (nh > 8) return false;
-  const uint32_t F16 = (F + 15) / 16 * 16;
-  const size_t table = static_cast<size_t>(F16) * kTTBins * 4;
-  const size_t limit = std::min<size_t>(ctx->smem_optin, 220 * 1024);
-  // candidate shapes (NC output words x G datapoint groups), 16 warps per CTA
-  struct Shape { int nc, g; };
-  const Shape shapes[] = {{4, 4}, {2, 8}, {1, 16}};
-  for (const Shape& s : shapes) {
-    const size_t smem = s.nc * table + static_cast<size_t>(s.g) * 512 * 4;
-    if (smem > limit) continue;
-    TTParams p{bins8, ldb, rows, F, F16, D, W, id, val, B, tie, out,
-               static_cast<uint32_t>((W + s.nc - 1) / s.nc), (rows + 32ull * s.g - 1) / (32ull * s.g)};
-#define HV_TT_CASE(NC, G, N)                                                   \
-  if (s.nc == NC && nh == N) {                                                 \
-    launch_tt_inst<NC, G, N>(ctx, st, p, smem);                                \
-    return true;                                                               \
-  }
-#define HV_TT_NH(NC, G) HV_TT_CASE(NC, G, 1) HV_TT_CASE(NC, G, 2) HV_TT_CASE(NC, G, 3) HV_TT_CASE(NC, G, 4) \
-                        HV_TT_CASE(NC, G, 5) HV_TT_CASE(NC, G, 6) HV_TT_CASE(NC, G, 7) HV_TT_CASE(NC, G, 8)
-    HV_TT_NH(4, 4)
-    HV_TT_NH(2, 8)
-    HV_TT_NH(1, 16)
-#undef HV_TT_NH
-#undef HV_TT_CASE
-  }
-  return false;
 }
 
 // Encodes validated uint8 bins on stream `st`.

@@ -184,6 +184,7 @@ hv_status hv_context_create(int device, hv_context** out) {
     ck(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking), "cudaStreamCreate");
     ctx->stream = ctx->own;
     ck(cudaMalloc(&ctx->d_err, sizeof(unsigned long long) * kErrKinds), "cudaMalloc");
+    ck(cudaMalloc(&ctx->d_counters, sizeof(unsigned int) * hv_context::kCounters), "cudaMalloc");
     // Keep freed scratch in the pool instead of returning it to the driver.
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -201,6 +202,7 @@ void hv_context_destroy(hv_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->d_err);
+  cudaFree(ctx->d_counters);
   cudaStreamDestroy(ctx->aux);
   cudaStreamDestroy(ctx->own);
   delete ctx;

@@ -77,6 +77,9 @@ struct hv_context {
   unsigned long long* d_err = nullptr;  // hvb::kErrKinds slots
   int sm_count = 148;
   size_t smem_optin = 0;
+  static constexpr unsigned kCounters = 64;
+  unsigned int* d_counters = nullptr;   // dynamic-scheduling counters (ring)
+  unsigned next_counter = 0;
 };
 
 namespace hvb {
@@ -150,6 +153,9 @@ void encode_device(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, size_
 void narrow_device(hv_context* ctx, cudaStream_t st, const uint32_t* bins32, size_t rows, size_t F, size_t B,
                    uint8_t* bins8, size_t ldb, uint64_t flat_base);
 inline size_t bins_pitch(size_t F) { return (F + 63) / 64 * 64; }
+bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
+               const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
+               uint32_t* out);
 
 // Host-side codebook helpers shared by several entry points (hv_host.cpp).
 void generate_random_words(size_t count, size_t dim, uint64_t seed, uint32_t* out);

@@ -46,7 +46,9 @@ class DeviceContext:
 
     def bind(self, stream: torch.cuda.Stream | None = None):
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        self.ctx.set_stream(s.cuda_stream)
+        # torch's default stream is the legacy NULL stream; hand the library
+        # cudaStreamLegacy (0x1) explicitly so its kernels order with torch's.
+        self.ctx.set_stream(s.cuda_stream or 0x1)
         return self
 
     @property
