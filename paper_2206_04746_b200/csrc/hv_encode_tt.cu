@@ -2,34 +2,36 @@
 // the hot loop of the whole pipeline).
 //
 // Output bit j of datapoint i = majority over f < F of ID_f[j] ^ V_{bin(i,f)}[j].
-// Per CTA, shared memory holds, for NC output words w_c,
-//     T_c[f][b] = ID_f[w_c] ^ V_b[w_c]      (F16 x 16 words per table)
-// so the XOR bind disappears: a bound word is one table lookup. Lane = datapoint,
-// warp (c, g) = output word w_c for the 32 datapoints of group g. Per lane and
-// bound word the cost is one conflict-free LDS (16 bins of one feature occupy
-// 16 distinct banks; equal bins broadcast) plus a ~2.2-LOP3 share of a
-// bit-sliced Harley–Seal carry-save counter (HS-32 blocks + ripple).
+// Per CTA, shared memory holds, for NP pairs of output words (w0, w1),
+//     T_p[f][b] = { ID_f[w0] ^ V_b[w0], ID_f[w1] ^ V_b[w1] }   (8 bytes)
+// so the XOR bind disappears and one 64-bit LDS yields the bound words of two
+// output words. Lane = datapoint; warp (p, g) = word pair p for the 32
+// datapoints of group g. The 16 bins of one feature occupy 128 contiguous bytes,
+// so each half-warp's LDS.64 is bank-conflict free for any bin pattern (equal
+// bins broadcast). Per lane and bound word the cost is half an LDS.64, half a
+// byte extract (PRMT) and a ~2.2-LOP3 share of a bit-sliced Harley–Seal
+// carry-save counter (HS-32 blocks + ripple into the high planes).
 //
-// Bins are staged per 64-feature chunk as 16-bit table byte offsets
-// ((f*16 + b) * 4), two per 32-bit word, in a feature-major layout rotated by
-// row so both the staging stores and the per-lane loads are bank-conflict
-// free, and shared by the NC warps of a group.
+// Raw uint8 bins are staged per 64-feature chunk in a [word][row] layout (lane
+// = row on both the stores and the loads: conflict free, no address math),
+// double-buffered through registers so the global loads of chunk k+1 overlap
+// the counting of chunk k, with one CTA barrier per chunk.
 //
-// Work is scheduled dynamically in items = (block of rows, word slice), ordered
-// block-major, so CTAs working concurrently on the same row block share its
-// bins through L2 (each row's bins leave HBM ~once) while each CTA rebuilds
-// its tables only when its slice changes (<1 % of an item's work).
+// Work is scheduled dynamically in items = (block of rows, word-pair slice),
+// ordered block-major, so CTAs working concurrently on the same row block share
+// its bins through L2 (each row's bins leave HBM ~once) while each CTA rebuilds
+// its tables only when its slice changes.
 #include <algorithm>
 
 #include "hv_internal.cuh"
 
 namespace hvb {
 
-constexpr int kTBins = 16;    // table rows per feature (B <= 16)
-constexpr int kChunk = 64;    // features per staged chunk
+constexpr int kTBins = 16;     // table rows per feature (B <= 16)
+constexpr int kChunk = 64;     // features per staged chunk
 constexpr int kBlockRows = 8192;
 
-struct TT2Params {
+struct TT3Params {
   const uint8_t* bins8;
   uint32_t ldb;
   uint64_t rows;
@@ -38,48 +40,87 @@ struct TT2Params {
   const uint32_t* val;
   const uint32_t* tie;
   uint32_t* out;
-  uint32_t slices;       // ceil(W / NC)
-  uint64_t blocks;       // ceil(rows / kBlockRows)
+  uint32_t slices;        // ceil(W / (2 NP))
+  uint64_t blocks;        // ceil(rows / kBlockRows)
   unsigned int* counter;  // dynamic work counter (zeroed before launch)
 };
 
-// Harley–Seal over 32 inputs: acc[0..4] hold weights 1..16, the returned
-// carry has weight 32.
+struct HS2 {
+  uint32_t a[5], b[5];
+};
+
+// Harley–Seal over 2^K inputs for two independent counters (word pair).
+// Levels 0..K-1 accumulate; the returned carries have weight 2^K.
 template <int K, class Load>
-__device__ __forceinline__ uint32_t hs_tree(uint32_t (&acc)[5], Load& ld) {
+__device__ __forceinline__ uint2 hs_tree2(HS2& s, Load& ld) {
   if constexpr (K == 1) {
-    const uint32_t a = ld();
-    const uint32_t b = ld();
-    uint32_t h;
-    csa(h, acc[0], acc[0], a, b);
+    const uint2 x = ld();
+    const uint2 y = ld();
+    uint2 h;
+    csa(h.x, s.a[0], s.a[0], x.x, y.x);
+    csa(h.y, s.b[0], s.b[0], x.y, y.y);
     return h;
   } else {
-    const uint32_t c1 = hs_tree<K - 1>(acc, ld);
-    const uint32_t c2 = hs_tree<K - 1>(acc, ld);
-    uint32_t h;
-    csa(h, acc[K - 1], acc[K - 1], c1, c2);
+    const uint2 c1 = hs_tree2<K - 1>(s, ld);
+    const uint2 c2 = hs_tree2<K - 1>(s, ld);
+    uint2 h;
+    csa(h.x, s.a[K - 1], s.a[K - 1], c1.x, c2.x);
+    csa(h.y, s.b[K - 1], s.b[K - 1], c1.y, c2.y);
     return h;
   }
 }
 
-template <int NC, int G, int NH>
-__global__ void __launch_bounds__(NC * G * 32, 2) encode_tt2_kernel(TT2Params p) {
+template <int NH>
+__device__ __forceinline__ void ripple(uint32_t (&hi)[NH], uint32_t carry) {
+#pragma unroll
+  for (int k = 0; k < NH; ++k) {
+    const uint32_t t = hi[k] & carry;
+    hi[k] ^= carry;
+    carry = t;
+  }
+}
+
+// bit = 2c > F ? 1 : 2c < F ? 0 : tie   (planes acc[0..4] weights 1..16, hi[k] weight 32 << k)
+template <int NH>
+__device__ __forceinline__ uint32_t majority_bits(const uint32_t (&acc)[5], const uint32_t (&hi)[NH], uint32_t F,
+                                                  uint32_t tie) {
+  const uint32_t half_f = F >> 1;
+  uint32_t gt = 0u, eq = 0xFFFFFFFFu;
+#pragma unroll
+  for (int k = 4 + NH; k >= 0; --k) {
+    const uint32_t pl = k >= 5 ? hi[k - 5] : acc[k];
+    if ((half_f >> k) & 1u) {
+      eq &= pl;
+    } else {
+      gt |= eq & pl;
+      eq &= ~pl;
+    }
+  }
+  return gt | ((F & 1u) ? 0u : (eq & tie));
+}
+
+template <int NP, int G, int NH>
+__global__ void __launch_bounds__(NP * G * 32, 2) encode_tt3_kernel(TT3Params p) {
   extern __shared__ __align__(16) uint32_t smem[];
-  const uint32_t tsz = p.F16 * kTBins;  // words per table
-  uint32_t* T = smem;                    // NC tables
-  uint32_t* S = smem + NC * tsz;         // G x (32 pairs x 32 rows) offset words
+  const uint32_t tsz = p.F16 * kTBins * 2;  // words per pair table
+  uint32_t* T = smem;                        // NP tables of uint2 entries
+  uint32_t* S = smem + NP * tsz;             // 2 buffers x G groups x 16 words x 32 rows
+  constexpr uint32_t kStage = 16 * 32;       // words per group and buffer
   __shared__ unsigned int s_item;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int c = warp % NC;
-  const int g = warp / NC;
-  constexpr uint32_t nthreads = NC * G * 32;
+  const int cp = warp % NP;
+  const int g = warp / NP;
+  constexpr uint32_t nthreads = NP * G * 32;
   constexpr uint32_t tile_rows = 32u * G;
   const uint64_t items = static_cast<uint64_t>(p.slices) * p.blocks;
   const uint32_t nchunks = (p.F16 + kChunk - 1) / kChunk;
   uint32_t cur_slice = 0xFFFFFFFFu;
-  const char* Tc = reinterpret_cast<const char*>(T + c * tsz);
-  const uint32_t* Sg = S + g * (kChunk / 2) * 32;
+  const char* Tp = reinterpret_cast<const char*>(T + cp * tsz);
+
+  // staging role: per chunk, G*64 32-byte sectors (group, half, row); thread
+  // owns sectors threadIdx.x + i*nthreads, i < SPT.
+  constexpr int SPT = (G * 64 + nthreads - 1) / nthreads;
 
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(p.counter, 1u);
@@ -89,13 +130,13 @@ __global__ void __launch_bounds__(NC * G * 32, 2) encode_tt2_kernel(TT2Params p)
     const uint32_t slice = static_cast<uint32_t>(item % p.slices);
     const uint64_t block = item / p.slices;
     if (slice != cur_slice) {
-      // T_cc[f][b] = ID_f[w] ^ V_b[w]; zero for f >= F, b >= B, w >= W
-      for (uint32_t k = threadIdx.x; k < NC * tsz; k += nthreads) {
-        const uint32_t cc = k / tsz;
-        const uint32_t rem = k - cc * tsz;
-        const uint32_t f = rem / kTBins;
-        const uint32_t b = rem % kTBins;
-        const uint32_t w = slice * NC + cc;
+      // T_pp[f][b] = {ID_f[w0]^V_b[w0], ID_f[w1]^V_b[w1]}; zero for f >= F, b >= B, w >= W
+      for (uint32_t k = threadIdx.x; k < NP * tsz; k += nthreads) {
+        const uint32_t pp = k / tsz;
+        const uint32_t rem = k - pp * tsz;
+        const uint32_t f = rem / (kTBins * 2);
+        const uint32_t b = (rem / 2) % kTBins;
+        const uint32_t w = 2 * (slice * NP + pp) + (rem & 1u);
         uint32_t v = 0;
         if (w < p.W && f < p.F && b < p.B) {
           v = __ldg(p.id + static_cast<uint64_t>(f) * p.W + w) ^ __ldg(p.val + static_cast<uint64_t>(b) * p.W + w);
@@ -105,106 +146,106 @@ __global__ void __launch_bounds__(NC * G * 32, 2) encode_tt2_kernel(TT2Params p)
       cur_slice = slice;
       __syncthreads();
     }
-    const uint32_t w = slice * NC + c;
+    const uint32_t w0 = 2 * (slice * NP + cp);
     const uint64_t r_begin = block * kBlockRows;
     const uint64_t r_end = min(p.rows, r_begin + kBlockRows);
     for (uint64_t tile0 = r_begin; tile0 < r_end; tile0 += tile_rows) {
-      uint32_t acc[5] = {0, 0, 0, 0, 0};
-      uint32_t hi[NH];
+      HS2 s;
 #pragma unroll
-      for (int k = 0; k < NH; ++k) hi[k] = 0;
-      for (uint32_t ch = 0; ch < nchunks; ++ch) {
-        __syncthreads();
-        // stage chunk ch: for every group, 32 rows x 64 features -> 32 offset
-        // pairs per row, stored pair-major [pair][row] so that a warp's stores
-        // (lane = row) and the per-lane loads below are both conflict free and
-        // the loads need no address arithmetic (pair index is an immediate).
-        // Each thread moves one full 32-byte sector (32 features) of one row.
-        for (uint32_t k = threadIdx.x; k < G * 64; k += nthreads) {
-          const uint32_t gg = k >> 6;
-          const uint32_t hf = (k >> 5) & 1u;  // which 32-feature half of the chunk
-          const uint32_t row = k & 31u;
-          const uint64_t grow = tile0 + 32ull * gg + row;
-          uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
-          if (grow < r_end) {
-            const uint4* src = reinterpret_cast<const uint4*>(p.bins8 + grow * p.ldb + ch * kChunk + hf * 32u);
-            v0 = src[0];
-            v1 = src[1];
-          }
-          const uint32_t words[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-          uint32_t* dst = S + gg * (kChunk / 2) * 32 + (hf * 16u) * 32 + row;
-          const uint32_t fbase = (ch * kChunk + hf * 32u) * (kTBins * 4);
+      for (int k = 0; k < 5; ++k) s.a[k] = s.b[k] = 0;
+      uint32_t hia[NH], hib[NH];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            // byte offsets (f*16 + b)*4 of 4 features (f < F16 <= 1023 keeps them < 2^16)
-            const uint32_t v = words[q];
-            const uint32_t b0 = fbase + q * 256u;
-            const uint32_t o0 = b0 + ((v & 0xFFu) << 2);
-            const uint32_t o1 = b0 + 64u + (((v >> 8) & 0xFFu) << 2);
-            const uint32_t o2 = b0 + 128u + (((v >> 16) & 0xFFu) << 2);
-            const uint32_t o3 = b0 + 192u + ((v >> 24) << 2);
-            dst[(2 * q) * 32] = o0 | (o1 << 16);
-            dst[(2 * q + 1) * 32] = o2 | (o3 << 16);
+      for (int k = 0; k < NH; ++k) hia[k] = hib[k] = 0;
+
+      // prefetch chunk 0 into registers, store, barrier
+      const uint4* st_src[SPT];
+      bool st_valid[SPT];
+      uint32_t* st_dst[SPT];
+      uint4 r0[SPT], r1[SPT];
+#pragma unroll
+      for (int i = 0; i < SPT; ++i) {
+        const uint32_t k = threadIdx.x + i * nthreads;
+        const uint32_t sg = k >> 6, sh = (k >> 5) & 1u, sr = k & 31u;
+        const uint64_t grow = tile0 + 32ull * sg + sr;
+        st_valid[i] = k < G * 64u && grow < r_end;
+        st_src[i] = reinterpret_cast<const uint4*>(p.bins8 + (st_valid[i] ? grow : 0) * p.ldb + sh * 32u);
+        st_dst[i] = S + (k < G * 64u ? sg : 0) * kStage + (sh * 8u) * 32 + sr;
+        r0[i] = r1[i] = make_uint4(0, 0, 0, 0);
+        if (st_valid[i]) {
+          r0[i] = st_src[i][0];
+          r1[i] = st_src[i][1];
+        }
+      }
+      auto stage = [&](uint32_t buf) {
+#pragma unroll
+        for (int i = 0; i < SPT; ++i) {
+          if (threadIdx.x + i * nthreads < G * 64u) {
+            uint32_t* dst = st_dst[i] + buf * G * kStage;
+            dst[0 * 32] = r0[i].x;
+            dst[1 * 32] = r0[i].y;
+            dst[2 * 32] = r0[i].z;
+            dst[3 * 32] = r0[i].w;
+            dst[4 * 32] = r1[i].x;
+            dst[5 * 32] = r1[i].y;
+            dst[6 * 32] = r1[i].z;
+            dst[7 * 32] = r1[i].w;
           }
         }
-        __syncthreads();
-        const uint32_t nf = min(static_cast<uint32_t>(kChunk), p.F16 - ch * kChunk);  // multiple of 16
-        uint32_t pair = 0;
-        uint32_t cur = 0;
-        int half = 0;
-        auto ld = [&]() -> uint32_t {
-          if (half == 0) {
-            cur = Sg[pair * 32 + lane];
-            ++pair;
+      };
+      stage(0);  // buffer 0 is free: the previous tile ended with a barrier
+      __syncthreads();
+      for (uint32_t ch = 0; ch < nchunks; ++ch) {
+        const uint32_t buf = ch & 1u;
+        const bool more = ch + 1 < nchunks;
+        if (more) {  // issue the next chunk's loads; they land during the counting below
+#pragma unroll
+          for (int i = 0; i < SPT; ++i) {
+            if (st_valid[i]) {
+              r0[i] = st_src[i][(ch + 1) * (kChunk / 16)];
+              r1[i] = st_src[i][(ch + 1) * (kChunk / 16) + 1];
+            }
           }
-          const uint32_t off = half ? (cur >> 16) : (cur & 0xFFFFu);
-          half ^= 1;
-          return *reinterpret_cast<const uint32_t*>(Tc + off);
+        }
+        const uint32_t* Sg = S + (buf * G + g) * kStage;
+        const char* Tch = Tp + static_cast<size_t>(ch) * kChunk * kTBins * 8;
+        const uint32_t nf = min(static_cast<uint32_t>(kChunk), p.F16 - ch * kChunk);  // multiple of 16
+        uint32_t q = 0, word = 0;
+        int t = 0;
+        auto ld = [&]() -> uint2 {
+          if (t == 0) word = Sg[q * 32 + lane];
+          const uint32_t b = __byte_perm(word, 0, 0x4440 | t);
+          const uint2 v = *reinterpret_cast<const uint2*>(Tch + (q * 4 + t) * (kTBins * 8) + b * 8);
+          if (++t == 4) {
+            t = 0;
+            ++q;
+          }
+          return v;
         };
         if (nf == kChunk) {
 #pragma unroll
           for (int h32 = 0; h32 < 2; ++h32) {
-            uint32_t carry = hs_tree<5>(acc, ld);
-#pragma unroll
-            for (int k = 0; k < NH; ++k) {
-              const uint32_t t = hi[k] & carry;
-              hi[k] ^= carry;
-              carry = t;
-            }
+            const uint2 carry = hs_tree2<5>(s, ld);
+            ripple<NH>(hia, carry.x);
+            ripple<NH>(hib, carry.y);
           }
         } else {
-          // tail: blocks of 16 features, carry of weight 16 rippled from acc[4]
           for (uint32_t f16 = 0; f16 < nf; f16 += 16) {
-            uint32_t carry = hs_tree<4>(acc, ld);
-            const uint32_t t = acc[4] & carry;
-            acc[4] ^= carry;
-            carry = t;
-#pragma unroll
-            for (int k = 0; k < NH; ++k) {
-              const uint32_t u = hi[k] & carry;
-              hi[k] ^= carry;
-              carry = u;
-            }
+            uint2 carry = hs_tree2<4>(s, ld);
+            const uint32_t ta = s.a[4] & carry.x, tb = s.b[4] & carry.y;
+            s.a[4] ^= carry.x;
+            s.b[4] ^= carry.y;
+            ripple<NH>(hia, ta);
+            ripple<NH>(hib, tb);
           }
         }
+        if (more) stage(buf ^ 1u);
+        __syncthreads();
       }
-      // majority against F: bit = 2c > F ? 1 : 2c < F ? 0 : tie (planes: acc[0..4], hi[0..NH))
       const uint64_t row = tile0 + 32ull * g + lane;
-      if (w < p.W && row < r_end) {
-        const uint32_t half_f = p.F >> 1;
-        uint32_t gt = 0u, eq = 0xFFFFFFFFu;
-#pragma unroll
-        for (int k = 4 + NH; k >= 0; --k) {
-          const uint32_t pl = k >= 5 ? hi[k - 5] : acc[k];
-          if ((half_f >> k) & 1u) {
-            eq &= pl;
-          } else {
-            gt |= eq & pl;
-            eq &= ~pl;
-          }
-        }
-        const uint32_t bit = gt | ((p.F & 1u) ? 0u : (eq & __ldg(p.tie + w)));
-        p.out[row * p.W + w] = bit & valid_mask(w, p.D);
+      if (row < r_end) {
+        uint32_t* o = p.out + row * p.W;
+        if (w0 < p.W) o[w0] = majority_bits<NH>(s.a, hia, p.F, __ldg(p.tie + w0)) & valid_mask(w0, p.D);
+        if (w0 + 1 < p.W) o[w0 + 1] = majority_bits<NH>(s.b, hib, p.F, __ldg(p.tie + w0 + 1)) & valid_mask(w0 + 1, p.D);
       }
     }
   }
@@ -212,19 +253,19 @@ __global__ void __launch_bounds__(NC * G * 32, 2) encode_tt2_kernel(TT2Params p)
 
 namespace {
 
-template <int NC, int G, int NH>
-void launch_tt2_inst(hv_context* ctx, cudaStream_t st, TT2Params p, size_t smem) {
-  auto kern = encode_tt2_kernel<NC, G, NH>;
+template <int NP, int G, int NH>
+void launch_tt3_inst(hv_context* ctx, cudaStream_t st, TT3Params p, size_t smem) {
+  auto kern = encode_tt3_kernel<NP, G, NH>;
   ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
      "cudaFuncSetAttribute");
   int per_sm = 0;
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NC * G * 32, smem), "occupancy");
-  if (per_sm < 1) fail(HV_ERR_CUDA, "encode_tt2_kernel: configuration does not fit on an SM");
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NP * G * 32, smem), "occupancy");
+  if (per_sm < 1) fail(HV_ERR_CUDA, "encode_tt3_kernel: configuration does not fit on an SM");
   const uint64_t items = static_cast<uint64_t>(p.slices) * p.blocks;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(ctx->sm_count) * per_sm));
   ck(cudaMemsetAsync(p.counter, 0, sizeof(unsigned int), st), "counter reset");
-  kern<<<grid, NC * G * 32, smem, st>>>(p);
-  launched("encode_tt2_kernel");
+  kern<<<grid, NP * G * 32, smem, st>>>(p);
+  launched("encode_tt3_kernel");
 }
 
 }  // namespace
@@ -235,47 +276,42 @@ bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
   if (B > static_cast<uint32_t>(kTBins) || F == 0 || rows == 0) return false;
   if (ldb % kChunk != 0 || (reinterpret_cast<uintptr_t>(bins8) & 15u)) return false;
   const uint32_t F16 = (F + 15) / 16 * 16;
-  if (static_cast<uint64_t>(F16) * kTBins * 4 > 0xFFFF) return false;  // 16-bit table offsets
   // planes beyond the 5 HS levels: counts < 32 * 2^NH
   int nh = 1;
   while ((32ull << nh) <= F) ++nh;
-  if (nh > 5) return false;
-  const size_t table = static_cast<size_t>(F16) * kTBins * 4;
-  const size_t stage = static_cast<size_t>(kChunk / 2) * 32 * 4;  // per group
-  const size_t per_sm_smem = 227 * 1024;
-  // prefer the widest slice that still fits two CTAs per SM, else one CTA
-  struct Shape { int nc, g; };
-  const Shape shapes[] = {{4, 4}, {2, 8}, {1, 16}};
+  if (nh > 6) return false;
+  const size_t table = static_cast<size_t>(F16) * kTBins * 8;
+  const size_t stage = 2ull * 16 * 32 * 4;  // double-buffered raw bins per group
+  // Shapes (word pairs x row groups), most warps per SM first; two CTAs per SM
+  // when they fit (a second CTA covers the other's chunk barriers).
+  struct Shape { int np, g; };
+  const Shape shapes[] = {{2, 4}, {1, 8}, {2, 8}, {1, 16}, {1, 4}};
+  const size_t two = 113 * 1024, one = std::min<size_t>(ctx->smem_optin, 225 * 1024);
   int pick = -1;
-  for (int pass = 0; pass < 2 && pick < 0; ++pass) {
-    for (int i = 0; i < 3; ++i) {
-      const size_t smem = shapes[i].nc * table + shapes[i].g * stage;
-      const size_t limit = pass == 0 ? per_sm_smem / 2 - 2048 : std::min<size_t>(ctx->smem_optin, per_sm_smem - 2048);
-      if (smem <= limit) {
-        pick = i;
-        break;
-      }
-    }
+  for (int i = 0; i < 5 && pick < 0; ++i) {
+    if (shapes[i].np * table + shapes[i].g * stage <= (i < 2 ? two : one)) pick = i;
   }
   if (pick < 0) return false;
   const Shape s = shapes[pick];
-  const size_t smem = s.nc * table + s.g * stage;
+  const size_t smem = s.np * table + s.g * stage;
   // one work counter per launch from the context's ring (concurrent launches on
   // the context's two streams must not share one)
   unsigned int* counter = ctx->d_counters + (ctx->next_counter++ % hv_context::kCounters);
-  TT2Params p{bins8, ldb, rows, F, F16, D, W, B, id, val, tie, out,
-              static_cast<uint32_t>((W + s.nc - 1) / s.nc), (rows + kBlockRows - 1) / kBlockRows, counter};
-#define HV_TT2(NC, G, N)                                  \
-  if (s.nc == NC && nh == N) {                            \
-    launch_tt2_inst<NC, G, N>(ctx, st, p, smem);          \
+  TT3Params p{bins8, ldb, rows, F, F16, D, W, B, id, val, tie, out,
+              static_cast<uint32_t>((W + 2 * s.np - 1) / (2 * s.np)), (rows + kBlockRows - 1) / kBlockRows, counter};
+#define HV_TT3(NP, G, N)                                  \
+  if (s.np == NP && s.g == G && nh == N) {                \
+    launch_tt3_inst<NP, G, N>(ctx, st, p, smem);          \
     return true;                                          \
   }
-#define HV_TT2_NH(NC, G) HV_TT2(NC, G, 1) HV_TT2(NC, G, 2) HV_TT2(NC, G, 3) HV_TT2(NC, G, 4) HV_TT2(NC, G, 5)
-  HV_TT2_NH(4, 4)
-  HV_TT2_NH(2, 8)
-  HV_TT2_NH(1, 16)
-#undef HV_TT2_NH
-#undef HV_TT2
+#define HV_TT3_NH(NP, G) HV_TT3(NP, G, 1) HV_TT3(NP, G, 2) HV_TT3(NP, G, 3) HV_TT3(NP, G, 4) HV_TT3(NP, G, 5) HV_TT3(NP, G, 6)
+  HV_TT3_NH(2, 4)
+  HV_TT3_NH(1, 8)
+  HV_TT3_NH(2, 8)
+  HV_TT3_NH(1, 16)
+  HV_TT3_NH(1, 4)
+#undef HV_TT3_NH
+#undef HV_TT3
   return false;
 }
 
