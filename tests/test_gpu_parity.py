@@ -166,6 +166,25 @@ def test_encode_random_vs_oracle(F, B, D, rows):
     np.testing.assert_array_equal(got.words, want)
 
 
+@pytest.mark.parametrize("env", [{"HVB200_TT_SHAPE": "4,8,1"}, {"HVB200_TT_SHAPE": "3,8,1"},
+                                 {"HVB200_TT_SHAPE": "2,8,1"}, {"HVB200_TT_SHAPE": "1,8,2"},
+                                 {"HVB200_TT_BLOCK_ROWS": "64"}])
+@pytest.mark.parametrize("F,D", [(342, 10000), (617, 1000), (40, 333), (130, 64)])
+def test_encode_fast_variants_vs_oracle(env, F, D, monkeypatch):
+    """Every instantiated shape of the table-lookup encoder against the oracle: tail chunks of 16/32/48 features, F < 64,
+    partial word slices, partial row tiles and (small blocks) table rebuilds."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    B, rows = 16, 700
+    rng = np.random.default_rng(F + D)
+    bins = rng.integers(0, B, (rows, F)).astype(np.uint32)
+    cb = hv.make_codebook(0, 0, F, B, D, 77 + F)
+    tb = hv.generate_random(1, D, 78 + D)
+    got = hv.encode_batch(bins, rows, cb, tb)
+    want = O.encode_batch(bins, cb.id_vectors.words, cb.value_vectors.words, B, D, O.BIND_ID_LEVEL, tb.words)
+    np.testing.assert_array_equal(got.words, want)
+
+
 @pytest.mark.parametrize("binding", [1, 2])
 @pytest.mark.parametrize("D", [33, 1000, 10240])
 def test_permutation_and_appending_vs_oracle(binding, D):
