@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "hv_internal.cuh"
+#include "hv_stage.h"
 #include "hvb200_synth.h"
 
 namespace hvb {
@@ -351,32 +352,23 @@ hv_status hv_encode_batch(hv_context* ctx, const uint32_t* bin_rows, size_t rows
     d_val.upload(value_vectors);
     d_tie.upload(tiebreak);
     sync(ctx);
-    // Chunked, double-buffered pipeline: H2D of chunk k+1 and D2H of chunk k-1
-    // overlap the encode of chunk k (two streams, one buffer set each).
-    const size_t chunk = std::max<size_t>(1, std::min<size_t>(rows, (size_t(64) << 20) / (features * 4 + 1)));
-    cudaStream_t streams[2] = {ctx->stream, ctx->aux};
-    DevBuf<uint32_t> b32[2] = {DevBuf<uint32_t>(chunk * features, ctx->stream), DevBuf<uint32_t>(chunk * features, ctx->stream)};
+    // Host narrowing into pinned slots -> H2D -> encode -> D2H, chunked over
+    // the context's two streams (hv_stage.cu).
+    const size_t chunk = stage_chunk_rows(rows, features);
     DevBuf<uint8_t> b8[2] = {DevBuf<uint8_t>(chunk * ldb, ctx->stream), DevBuf<uint8_t>(chunk * ldb, ctx->stream)};
     DevBuf<uint32_t> o[2] = {DevBuf<uint32_t>(chunk * W, ctx->stream), DevBuf<uint32_t>(chunk * W, ctx->stream)};
     sync(ctx);
     size_t k = 0;
-    for (size_t r0 = 0; r0 < rows; r0 += chunk, ++k) {
-      const size_t n = std::min(chunk, rows - r0);
-      cudaStream_t st = streams[k & 1];
-      ck(cudaMemcpyAsync(b32[k & 1].ptr, bin_rows + r0 * features, n * features * 4, cudaMemcpyHostToDevice, st), "H2D bins");
-      narrow_device(ctx, st, b32[k & 1].ptr, n, features, bins, b8[k & 1].ptr, ldb, r0 * features);
-      encode_device(ctx, st, b8[k & 1].ptr, ldb, n, features, d_id.ptr, d_val.ptr, bins, dim, binding, d_tie.ptr,
-                    o[k & 1].ptr);
-      ck(cudaMemcpyAsync(out + r0 * W, o[k & 1].ptr, n * W * 4, cudaMemcpyDeviceToHost, st), "D2H encoded");
-    }
+    const uint64_t bad = encode_host_bins(
+        ctx, bin_rows, rows, features, bins, dim, binding, d_id.ptr, d_val.ptr, d_tie.ptr,
+        [&](size_t, size_t kk) { return o[kk & 1].ptr; }, b8, chunk, k,
+        [&](size_t r0, size_t n, size_t kk, cudaStream_t st) {
+          ck(cudaMemcpyAsync(out + r0 * W, o[kk & 1].ptr, n * W * 4, cudaMemcpyDeviceToHost, st), "D2H encoded");
+        });
     ck(cudaStreamSynchronize(ctx->aux), "sync aux");
     sync(ctx);
-    unsigned long long l[kErrKinds];
-    read_latch(ctx, l);
-    if (l[kErrBin] != ~0ull) {
-      reset_latch(ctx);
-      const size_t f = l[kErrBin] % features;
-      invalid("encode: feature " + std::to_string(f) + " bin index " + std::to_string(bin_rows[l[kErrBin]]) +
+    if (bad != ~0ull) {
+      invalid("encode: feature " + std::to_string(bad % features) + " bin index " + std::to_string(bin_rows[bad]) +
               " out of range (bins = " + std::to_string(bins) + ")");
     }
   });

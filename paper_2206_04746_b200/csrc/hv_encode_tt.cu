@@ -312,10 +312,17 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
   if (pick < 0) return false;
   const Shape s = shapes[pick];
   const size_t smem = s.npr * pair_table + s.g * wstage;
-  const char* br_env = getenv("HVB200_TT_BLOCK_ROWS");
-  const uint32_t block_rows = br_env ? static_cast<uint32_t>(atoi(br_env)) : 16384u;
-  TT6Params p{bins8, ldb, rows, F, F16, D, W, B, id, val, tie, out,
-              static_cast<uint32_t>((W + 2 * s.npr - 1) / (2 * s.npr)), block_rows,
+  const uint32_t slices = static_cast<uint32_t>((W + 2 * s.npr - 1) / (2 * s.npr));
+  // 16k-row blocks (bins of a block stay in L2 while its slices run), smaller
+  // when that would leave fewer than ~4 items per CTA (chunked host pipelines)
+  uint32_t block_rows = 16384u;
+  const uint64_t want_items = 4ull * ctx->sm_count * s.minb;
+  if (((rows + block_rows - 1) / block_rows) * slices < want_items) {
+    const uint64_t br = (rows * slices + want_items - 1) / want_items;
+    block_rows = static_cast<uint32_t>(std::max<uint64_t>(256, (br + 255) / 256 * 256));
+  }
+  if (const char* br_env = getenv("HVB200_TT_BLOCK_ROWS")) block_rows = static_cast<uint32_t>(atoi(br_env));
+  TT6Params p{bins8, ldb, rows, F, F16, D, W, B, id, val, tie, out, slices, block_rows,
               (rows + block_rows - 1) / block_rows, counter};
 #define HV_TT6(NPR, G, MB, N)                                            \
   if (s.npr == NPR && s.g == G && s.minb == MB && nh == N) {             \

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "hv_internal.cuh"
+#include "hv_stage.h"
 
 namespace hvb {
 
@@ -201,6 +202,8 @@ void hv_context_destroy(hv_context* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  cudaStreamSynchronize(ctx->aux);
+  destroy_stager(ctx);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_counters);
   cudaStreamDestroy(ctx->aux);

@@ -67,6 +67,8 @@ __device__ __forceinline__ void latch(unsigned long long* err, int kind, unsigne
   atomicMin(err + kind, index);
 }
 
+struct HostStager;
+
 }  // namespace hvb
 
 struct hv_context {
@@ -80,6 +82,7 @@ struct hv_context {
   static constexpr unsigned kCounters = 64;
   unsigned int* d_counters = nullptr;   // dynamic-scheduling counters (ring)
   unsigned next_counter = 0;
+  hvb::HostStager* stager = nullptr;    // host narrowing pool + pinned slots (lazy)
 };
 
 namespace hvb {

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "hv_internal.cuh"
+#include "hv_stage.h"
 
 namespace hvb {
 
@@ -870,20 +871,6 @@ namespace hvb {
 namespace {
 
 // Chunked, double-buffered upload + narrow + encode of host uint32 bins into `out`.
-void encode_host_rows(hv_context* ctx, const uint32_t* bins, size_t rows, size_t F, size_t B, size_t D,
-                      const uint32_t* d_id, const uint32_t* d_val, const uint32_t* d_tie, uint32_t* out,
-                      uint64_t flat_base, DevBuf<uint32_t>* b32, DevBuf<uint8_t>* b8, size_t chunk, size_t& k) {
-  const size_t W = words_per_row(D), ldb = bins_pitch(F);
-  cudaStream_t streams[2] = {ctx->stream, ctx->aux};
-  for (size_t r0 = 0; r0 < rows; r0 += chunk, ++k) {
-    const size_t n = std::min(chunk, rows - r0);
-    cudaStream_t st = streams[k & 1];
-    ck(cudaMemcpyAsync(b32[k & 1].ptr, bins + r0 * F, n * F * 4, cudaMemcpyHostToDevice, st), "H2D bins");
-    narrow_device(ctx, st, b32[k & 1].ptr, n, F, B, b8[k & 1].ptr, ldb, flat_base + r0 * F);
-    encode_device(ctx, st, b8[k & 1].ptr, ldb, n, F, d_id, d_val, B, D, HV_BIND_ID_LEVEL, d_tie, out + r0 * W);
-  }
-}
-
 }  // namespace
 }  // namespace hvb
 
@@ -919,37 +906,40 @@ hv_status hv_fold_encode_train(hv_context* ctx, const uint32_t* train_bins, size
     d_val.upload(value_vectors);
     d_tie.upload(encode_tiebreak);
     d_y.upload(train_labels);
-    const size_t chunk = std::max<size_t>(1, std::min<size_t>(std::max<size_t>(rows, 1), (size_t(128) << 20) / (features * 4)));
-    DevBuf<uint32_t> b32[2] = {DevBuf<uint32_t>(chunk * features, st), DevBuf<uint32_t>(chunk * features, st)};
+    const size_t chunk = stage_chunk_rows(rows, features);
     DevBuf<uint8_t> b8[2] = {DevBuf<uint8_t>(chunk * ldb, st), DevBuf<uint8_t>(chunk * ldb, st)};
     sync(ctx);
     size_t k = 0;
-    encode_host_rows(ctx, train_bins, train_rows, features, bins, dim, d_id.ptr, d_val.ptr, d_tie.ptr, fold->enc.ptr,
-                     0, b32, b8, chunk, k);
-    // classical counts of the train rows overlap the upload/encode of the test rows
-    cudaEvent_t ev;
-    ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
-    ck(cudaEventRecord(ev, ctx->aux), "event");
-    ck(cudaStreamWaitEvent(ctx->stream, ev, 0), "wait");
-    cudaEventDestroy(ev);
-    class_counts_device(ctx, ctx->stream, fold->enc.ptr, train_rows, W, d_y.ptr, class_count, fold->counts.ptr,
-                        fold->class_rows.ptr);
-    encode_host_rows(ctx, test_bins, test_rows, features, bins, dim, d_id.ptr, d_val.ptr, d_tie.ptr,
-                     fold->enc.ptr + train_rows * W, train_rows * features, b32, b8, chunk, k);
+    uint32_t* enc = fold->enc.ptr;
+    uint64_t bad = encode_host_bins(ctx, train_bins, train_rows, features, bins, dim, HV_BIND_ID_LEVEL, d_id.ptr,
+                                    d_val.ptr, d_tie.ptr, [&](size_t r0, size_t) { return enc + r0 * W; }, b8, chunk, k);
+    if (bad == ~0ull) {
+      // classical counts of the train rows overlap the staging/encode of the test rows
+      cudaEvent_t ev;
+      ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+      ck(cudaEventRecord(ev, ctx->aux), "event");
+      ck(cudaStreamWaitEvent(ctx->stream, ev, 0), "wait");
+      cudaEventDestroy(ev);
+      class_counts_device(ctx, ctx->stream, enc, train_rows, W, d_y.ptr, class_count, fold->counts.ptr,
+                          fold->class_rows.ptr);
+      bad = encode_host_bins(ctx, test_bins, test_rows, features, bins, dim, HV_BIND_ID_LEVEL, d_id.ptr, d_val.ptr,
+                             d_tie.ptr, [&](size_t r0, size_t) { return enc + (train_rows + r0) * W; }, b8, chunk, k);
+      if (bad != ~0ull) bad += train_rows * features;
+    }
     ck(cudaStreamSynchronize(ctx->aux), "sync aux");
     sync(ctx);
     unsigned long long l[kErrKinds];
     read_latch(ctx, l);
-    if (l[kErrBin] != ~0ull || l[kErrLabel] != ~0ull) {
-      reset_latch(ctx);
-      if (l[kErrLabel] != ~0ull) {
-        invalid("train_classical: label " + std::to_string(train_labels[l[kErrLabel]]) + " at row " +
-                std::to_string(l[kErrLabel]) + " out of range (classes = " + std::to_string(class_count) + ")");
-      }
-      const uint64_t idx = l[kErrBin];
-      const uint32_t b = idx < train_rows * features ? train_bins[idx] : test_bins[idx - train_rows * features];
-      invalid("encode: feature " + std::to_string(idx % features) + " bin index " + std::to_string(b) +
+    if (l[kErrLabel] != ~0ull) reset_latch(ctx);
+    // reference order (experiment.cpp:159-177): encode train, encode test, then train_classical
+    if (bad != ~0ull) {
+      const uint32_t b = bad < train_rows * features ? train_bins[bad] : test_bins[bad - train_rows * features];
+      invalid("encode: feature " + std::to_string(bad % features) + " bin index " + std::to_string(b) +
               " out of range (bins = " + std::to_string(bins) + ")");
+    }
+    if (l[kErrLabel] != ~0ull) {
+      invalid("train_classical: label " + std::to_string(train_labels[l[kErrLabel]]) + " at row " +
+              std::to_string(l[kErrLabel]) + " out of range (classes = " + std::to_string(class_count) + ")");
     }
     *out = fold.release();
   });

@@ -1,0 +1,75 @@
+// hv_stage.h — host thread pool and pinned staging of uint32 bin rows
+// (hv_stage.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "hv_internal.cuh"
+
+namespace hvb {
+
+// Persistent workers for data-parallel host loops; the calling thread joins in.
+class ThreadPool {
+ public:
+  explicit ThreadPool(unsigned workers);
+  ~ThreadPool();
+  ThreadPool(const ThreadPool&) = delete;
+  ThreadPool& operator=(const ThreadPool&) = delete;
+  void parallel_for(size_t n, const std::function<void(size_t)>& fn);
+  unsigned size() const { return static_cast<unsigned>(workers_.size()); }
+
+ private:
+  void loop();
+  void drain();
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(size_t)>* job_ = nullptr;
+  size_t n_ = 0;
+  std::atomic<size_t> next_{0}, left_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// Pinned staging slots (ring of kSlots) + the pool that fills them.
+struct HostStager {
+  static constexpr int kSlots = 3;
+  ThreadPool pool;
+  uint8_t* slot[kSlots] = {};
+  cudaEvent_t done[kSlots] = {};  // recorded after the slot's H2D copy
+  size_t cap = 0;
+
+  HostStager();
+  ~HostStager();
+  void reserve(size_t bytes);
+  // Narrows rows x F uint32 bins into slot s (pitch ldb, zero padded);
+  // returns the first flat index whose bin is >= B, or ~0.
+  uint64_t narrow(const uint32_t* in, size_t rows, size_t F, size_t B, size_t ldb, int s);
+};
+
+HostStager& stager(hv_context* ctx);
+void destroy_stager(hv_context* ctx);
+size_t stage_chunk_rows(size_t rows, size_t F);
+
+// Host uint32 bin rows -> (narrow on host, pinned slot, H2D, encode) in chunks
+// alternating the context's two streams. Chunk k (rows r0 .. r0+n) is encoded
+// into out_for(r0, k); b8 = two device chunk buffers of chunk * bins_pitch(F)
+// bytes; `after(r0, n, k, stream)` runs per chunk (e.g. to enqueue a D2H of it
+// on its stream). Returns the first offending flat bin index (relative to
+// `bins`) or ~0; on an error the remaining chunks are not enqueued.
+using ChunkOut = std::function<uint32_t*(size_t r0, size_t k)>;
+using ChunkAfter = std::function<void(size_t r0, size_t n, size_t k, cudaStream_t st)>;
+uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, size_t F, size_t B, size_t D,
+                          hv_binding binding, const uint32_t* d_id, const uint32_t* d_val, const uint32_t* d_tie,
+                          const ChunkOut& out_for, DevBuf<uint8_t>* b8, size_t chunk, size_t& k,
+                          const ChunkAfter& after = {});
+
+}  // namespace hvb
