@@ -240,6 +240,35 @@ hv_status hv_dev_apply_online_delta(hv_context* ctx, size_t class_count, size_t 
                                     const uint64_t* delta_counts, const uint32_t* touched,
                                     const uint32_t* tiebreak, double* acc, double* weight,
                                     uint64_t* counts, uint32_t* class_vectors);
+/* Encode only output words [word_begin, word_begin + word_count) of every row
+ * into out (row stride ldo words) — the column slice a rank owns in D-sliced
+ * training (encoding.cpp:266-271 is independent per output position). */
+hv_status hv_dev_encode_words(hv_context* ctx, const uint8_t* bins8, size_t ldb, size_t rows,
+                              size_t features, const uint32_t* id_vectors,
+                              const uint32_t* value_vectors, size_t bins, size_t dim,
+                              hv_binding binding, const uint32_t* tiebreak, size_t word_begin,
+                              size_t word_count, uint32_t* out, size_t ldo);
+/* ---- D-sliced exact online training (model.cpp:250-301 across ranks) -----
+ * Rank r owns words [word_begin, word_begin + words) of every hypervector:
+ * batch rows are its slice (row stride `words`), acc is C x slice_bits fp64
+ * (slice_bits = min(dim, 32*(word_begin+words)) - 32*word_begin), class_vectors
+ * C x words; weight/counts (C) are replicated and evolve identically.
+ * Per batch: hv_dev_online_partial_popc -> all-reduce(sum) of popc (rows x C
+ * uint32) -> hv_dev_online_slice_update. Every fp64 element sees the
+ * reference's sample-ordered in-place additions: bit-identical to one GPU. */
+hv_status hv_dev_online_slice_init(hv_context* ctx, const uint32_t* batch0, size_t rows0,
+                                   const int32_t* labels, size_t class_count, size_t dim,
+                                   size_t word_begin, size_t words, const uint32_t* tiebreak,
+                                   double* acc, double* weight, uint64_t* counts,
+                                   uint32_t* class_vectors);
+hv_status hv_dev_online_partial_popc(hv_context* ctx, const uint32_t* class_vectors,
+                                     size_t class_count, size_t words, const uint32_t* batch,
+                                     size_t rows, uint32_t* popc);
+hv_status hv_dev_online_slice_update(hv_context* ctx, const uint32_t* popc, size_t class_count,
+                                     size_t dim, size_t word_begin, size_t words,
+                                     const uint32_t* batch, size_t rows, const int32_t* labels,
+                                     double gamma, const uint32_t* tiebreak, double* acc,
+                                     double* weight, uint64_t* counts, uint32_t* class_vectors);
 /* Synthetic workload (include/hvb200_synth.h) generated on device for rows
  * [row0, row0+rows): bins8 (pitch ldb) and labels. */
 hv_status hv_dev_synth(hv_context* ctx, uint64_t row0, size_t rows, size_t features,

@@ -110,6 +110,10 @@ SIGNATURES = {
     "hv_dev_online_delta": (ST, [vp, vp, sz, sz, vp, sz, vp, dbl, vp, vp, vp, vp]),
     "hv_dev_apply_online_delta": (ST, [vp, sz, sz, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "hv_dev_synth": (ST, [vp, u64, sz, sz, sz, sz, ci, u64, vp, sz, vp]),
+    "hv_dev_encode_words": (ST, [vp, vp, sz, sz, sz, vp, vp, sz, sz, ci, vp, sz, sz, vp, sz]),
+    "hv_dev_online_slice_init": (ST, [vp, vp, sz, vp, sz, sz, sz, sz, vp, vp, vp, vp, vp]),
+    "hv_dev_online_partial_popc": (ST, [vp, vp, sz, sz, vp, sz, vp]),
+    "hv_dev_online_slice_update": (ST, [vp, vp, sz, sz, sz, sz, vp, sz, vp, dbl, vp, vp, vp, vp, vp]),
     "hv_fold_encode_train": (ST, [vp, vp, sz, vp, vp, sz, sz, vp, vp, sz, sz, vp, sz, C.POINTER(vp)]),
     "hv_fold_counts": (ST, [vp, C.POINTER(vp), C.POINTER(vp)]),
     "hv_fold_predict": (ST, [vp, vp, vp, vp]),

@@ -225,14 +225,36 @@ void launch_generic(hv_context* ctx, cudaStream_t st, int nh, const uint8_t* bin
 // Encodes validated uint8 bins on stream `st`.
 void encode_device(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, size_t ldb, size_t rows, size_t F,
                    const uint32_t* id, const uint32_t* val, size_t B, size_t D, hv_binding binding,
-                   const uint32_t* tie, uint32_t* out, bool allow_fast) {
+                   const uint32_t* tie, uint32_t* out, bool allow_fast, size_t w0, size_t wcount, size_t ldo) {
   const size_t W = words_per_row(D);
   if (rows == 0 || W == 0) return;
   if (D > 0xFFFFFFFFull || F > 0xFFFFFFFFull) invalid("encode: shape too large");
+  if (wcount == 0) {
+    w0 = 0;
+    wcount = W;
+    ldo = W;
+  }
+  if (w0 + wcount > W || ldo < wcount) invalid("encode: word range outside the row");
+  if (wcount != W || ldo != W) {
+    // a column slice: the fused encoder writes it directly; other bindings
+    // encode whole rows into scratch and copy the slice out
+    if (binding == HV_BIND_ID_LEVEL && allow_fast &&
+        launch_tt(ctx, st, bins8, static_cast<uint32_t>(ldb), rows, static_cast<uint32_t>(F), id, val,
+                  static_cast<uint32_t>(B), static_cast<uint32_t>(D), static_cast<uint32_t>(W), tie, out,
+                  static_cast<uint32_t>(w0), static_cast<uint32_t>(wcount), static_cast<uint32_t>(ldo))) {
+      return;
+    }
+    DevBuf<uint32_t> full(rows * W, st);
+    encode_device(ctx, st, bins8, ldb, rows, F, id, val, B, D, binding, tie, full.ptr, allow_fast);
+    ck(cudaMemcpy2DAsync(out, ldo * 4, full.ptr + w0, W * 4, wcount * 4, rows, cudaMemcpyDeviceToDevice, st),
+       "slice copy");
+    return;
+  }
   switch (binding) {
     case HV_BIND_ID_LEVEL:
       if (allow_fast && launch_tt(ctx, st, bins8, static_cast<uint32_t>(ldb), rows, static_cast<uint32_t>(F), id, val,
-                                  static_cast<uint32_t>(B), static_cast<uint32_t>(D), static_cast<uint32_t>(W), tie, out)) {
+                                  static_cast<uint32_t>(B), static_cast<uint32_t>(D), static_cast<uint32_t>(W), tie, out,
+                                  0u, static_cast<uint32_t>(W), static_cast<uint32_t>(W))) {
         return;
       }
       launch_generic<false>(ctx, st, hs_high_planes(F), bins8, static_cast<uint32_t>(ldb), rows,
@@ -393,6 +415,21 @@ hv_status hv_dev_encode(hv_context* ctx, const uint8_t* bins8, size_t ldb, size_
     const char* env = getenv("HVB200_ENCODE_GENERIC");
     encode_device(ctx, ctx->stream, bins8, ldb, rows, features, id_vectors, value_vectors, bins, dim, binding, tiebreak,
                   out, !(env && env[0] == '1'));
+  });
+}
+
+hv_status hv_dev_encode_words(hv_context* ctx, const uint8_t* bins8, size_t ldb, size_t rows, size_t features,
+                              const uint32_t* id_vectors, const uint32_t* value_vectors, size_t bins, size_t dim,
+                              hv_binding binding, const uint32_t* tiebreak, size_t word_begin, size_t word_count,
+                              uint32_t* out, size_t ldo) {
+  return guarded([&] {
+    require(ctx);
+    if (features == 0 || dim == 0) invalid("encode: features and dim must be >= 1");
+    if (ldb < features) invalid("encode: ldb < features");
+    if (word_count == 0) invalid("encode_words: word_count must be >= 1");
+    const char* env = getenv("HVB200_ENCODE_GENERIC");
+    encode_device(ctx, ctx->stream, bins8, ldb, rows, features, id_vectors, value_vectors, bins, dim, binding, tiebreak,
+                  out, !(env && env[0] == '1'), word_begin, word_count, ldo);
   });
 }
 

@@ -51,7 +51,9 @@ struct TT6Params {
   const uint32_t* val;
   const uint32_t* tie;
   uint32_t* out;
-  uint32_t slices;      // ceil(W / NW)
+  uint32_t w0, wcount;  // output words [w0, w0 + wcount) of the W-word codebook rows
+  uint32_t ldo;         // output row stride (words); word w0 + k goes to out[row * ldo + k]
+  uint32_t slices;      // ceil(wcount / NW)
   uint32_t block_rows;  // rows per work item
   uint64_t blocks;      // ceil(rows / block_rows)
   unsigned int* counter;
@@ -122,16 +124,16 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
     if (item >= items) break;
     const uint32_t slice = static_cast<uint32_t>(item % p.slices);
     const uint64_t block = item / p.slices;
-    const uint32_t wb = slice * NW;
+    const uint32_t wb = slice * NW;  // first local output word of the slice
     if (slice != cur_slice) {
-      // entry (f, b): NW words ID_f[wb+j] ^ V_b[wb+j]; zero for f >= F, b >= B, w >= W
+      // entry (f, b): NW words ID_f[w] ^ V_b[w], w = w0+wb+j; zero for f >= F, b >= B, past the range
       for (uint32_t k = threadIdx.x; k < p.F16 * kTBins; k += nthreads) {
         const uint32_t f = k / kTBins, b = k % kTBins;
         uint32_t e[NW];
 #pragma unroll
         for (int j = 0; j < NW; ++j) {
-          const uint32_t w = wb + j;
-          e[j] = (w < p.W && f < p.F && b < p.B)
+          const uint32_t w = p.w0 + wb + j;
+          e[j] = (wb + j < p.wcount && f < p.F && b < p.B)
                      ? __ldg(p.id + static_cast<uint64_t>(f) * p.W + w) ^ __ldg(p.val + static_cast<uint64_t>(b) * p.W + w)
                      : 0u;
         }
@@ -245,17 +247,17 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
       }
       const uint64_t row = wrow0 + lane;
       if (row < r_end) {
-        uint32_t* o = p.out + row * p.W;
+        uint32_t* o = p.out + row * p.ldo;
 #pragma unroll
         for (int j = 0; j < NW; ++j) {
-          const uint32_t w = wb + j;
-          if (w < p.W) {
+          const uint32_t w = p.w0 + wb + j;
+          if (wb + j < p.wcount) {
             uint32_t pl[6 + NH];
 #pragma unroll
             for (int k = 0; k < 6; ++k) pl[k] = s[k][j];
 #pragma unroll
             for (int k = 0; k < NH; ++k) pl[6 + k] = hi[k][j];
-            o[w] = majority6<NH>(pl, p.F, __ldg(p.tie + w)) & valid_mask(w, p.D);
+            o[wb + j] = majority6<NH>(pl, p.F, __ldg(p.tie + w)) & valid_mask(w, p.D);
           }
         }
       }
@@ -283,7 +285,7 @@ void launch_tt6_inst(hv_context* ctx, cudaStream_t st, TT6Params p, size_t smem)
 
 bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
                const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
-               uint32_t* out, uint32_t* counter) {
+               uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo, uint32_t* counter) {
   const uint32_t F16 = (F + 15) / 16 * 16;
   // planes above the six HS levels: counts < 64 * 2^NH; instantiated NH in {3, 4, 6}
   int nh = 0;
@@ -312,7 +314,7 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
   if (pick < 0) return false;
   const Shape s = shapes[pick];
   const size_t smem = s.npr * pair_table + s.g * wstage;
-  const uint32_t slices = static_cast<uint32_t>((W + 2 * s.npr - 1) / (2 * s.npr));
+  const uint32_t slices = static_cast<uint32_t>((wcount + 2 * s.npr - 1) / (2 * s.npr));
   // 16k-row blocks (bins of a block stay in L2 while its slices run), smaller
   // when that would leave fewer than ~4 items per CTA (chunked host pipelines)
   uint32_t block_rows = 16384u;
@@ -322,7 +324,7 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
     block_rows = static_cast<uint32_t>(std::max<uint64_t>(256, (br + 255) / 256 * 256));
   }
   if (const char* br_env = getenv("HVB200_TT_BLOCK_ROWS")) block_rows = static_cast<uint32_t>(atoi(br_env));
-  TT6Params p{bins8, ldb, rows, F, F16, D, W, B, id, val, tie, out, slices, block_rows,
+  TT6Params p{bins8, ldb, rows, F, F16, D, W, B, id, val, tie, out, w0, wcount, ldo, slices, block_rows,
               (rows + block_rows - 1) / block_rows, counter};
 #define HV_TT6(NPR, G, MB, N)                                            \
   if (s.npr == NPR && s.g == G && s.minb == MB && nh == N) {             \
@@ -343,13 +345,13 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
 
 bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
                const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
-               uint32_t* out) {
-  if (B > static_cast<uint32_t>(kTBins) || F == 0 || rows == 0) return false;
+               uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo) {
+  if (B > static_cast<uint32_t>(kTBins) || F == 0 || rows == 0 || wcount == 0) return false;
   if (ldb % kChunk != 0 || (reinterpret_cast<uintptr_t>(bins8) & 15u)) return false;
   // one work counter per launch from the context's ring (concurrent launches on
   // the context's two streams must not share one)
   unsigned int* counter = ctx->d_counters + (ctx->next_counter++ % hv_context::kCounters);
-  return launch_v6(ctx, st, bins8, ldb, rows, F, id, val, B, D, W, tie, out, counter);
+  return launch_v6(ctx, st, bins8, ldb, rows, F, id, val, B, D, W, tie, out, w0, wcount, ldo, counter);
 }
 
 }  // namespace hvb

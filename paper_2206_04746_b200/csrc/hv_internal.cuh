@@ -149,16 +149,19 @@ inline unsigned grid_for(size_t n, unsigned block, unsigned cap = 1u << 30) {
 void launch_column_count_u32(cudaStream_t st, const uint32_t* m, uint32_t W, const uint32_t* perm,
                              const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, uint32_t* counts);
 
-// Encoder entry points shared with the fold pipeline (hv_encode.cu).
+// Encoder entry points shared with the fold pipeline (hv_encode.cu). Words
+// [w0, w0 + wcount) of every row are written to out[row * ldo + k]; wcount = 0
+// means the whole row (w0 = 0, wcount = ldo = W).
 void encode_device(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, size_t ldb, size_t rows, size_t F,
                    const uint32_t* id, const uint32_t* val, size_t B, size_t D, hv_binding binding,
-                   const uint32_t* tie, uint32_t* out, bool allow_fast = true);
+                   const uint32_t* tie, uint32_t* out, bool allow_fast = true, size_t w0 = 0, size_t wcount = 0,
+                   size_t ldo = 0);
 void narrow_device(hv_context* ctx, cudaStream_t st, const uint32_t* bins32, size_t rows, size_t F, size_t B,
                    uint8_t* bins8, size_t ldb, uint64_t flat_base);
 inline size_t bins_pitch(size_t F) { return (F + 63) / 64 * 64; }
 bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
                const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
-               uint32_t* out);
+               uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo);
 
 // Host-side codebook helpers shared by several entry points (hv_host.cpp).
 void generate_random_words(size_t count, size_t dim, uint64_t seed, uint32_t* out);

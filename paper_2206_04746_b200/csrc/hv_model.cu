@@ -279,6 +279,54 @@ __global__ void online_score_hamming_kernel(const uint32_t* __restrict__ cv, uin
   }
 }
 
+// D-sliced online training (SURVEY.md §8e exact mode): partial Hamming
+// popcounts of each batch row against each class over this rank's word slice
+// (warp per row), summed across ranks by the caller's all-reduce.
+__global__ void online_partial_popc_kernel(const uint32_t* __restrict__ cv, uint32_t C, uint32_t Ws,
+                                           const uint32_t* __restrict__ batch, uint64_t rows,
+                                           uint32_t* __restrict__ popc) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += stride) {
+    const uint32_t* q = batch + r * Ws;
+    for (uint32_t c = 0; c < C; ++c) {
+      uint32_t a = 0;
+      for (uint32_t w = lane; w < Ws; w += 32u) a += __popc(q[w] ^ cv[static_cast<uint64_t>(c) * Ws + w]);
+      a = __reduce_add_sync(FULL, a);
+      if (lane == 0) popc[r * C + c] = a;
+    }
+  }
+}
+
+// Scores from full-row popcounts (rows x C): the same argmin (strict <, lowest
+// class on ties, model.cpp:96-104) and doubles as online_score_hamming_kernel.
+__global__ void online_score_popc_kernel(const uint32_t* __restrict__ popc, uint32_t C, uint32_t D, uint64_t rows,
+                                         const int32_t* __restrict__ labels, double gamma, int32_t* __restrict__ pred,
+                                         double* __restrict__ dtrue, double* __restrict__ pen,
+                                         unsigned long long* __restrict__ err) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows; r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t* pc = popc + r * C;
+    const int32_t y = labels[r];
+    uint32_t best = 0, bestp = pc[0];
+    for (uint32_t c = 1; c < C; ++c) {
+      if (pc[c] < bestp) {
+        bestp = pc[c];
+        best = c;
+      }
+    }
+    uint32_t truep = 0;
+    if (y < 0 || static_cast<uint32_t>(y) >= C) {
+      latch(err, kErrLabel, r);
+    } else {
+      truep = pc[y];
+    }
+    pred[r] = static_cast<int32_t>(best);
+    dtrue[r] = static_cast<double>(truep) / static_cast<double>(D);
+    const double dw = static_cast<double>(bestp) / static_cast<double>(D);
+    pen[r] = __dmul_rn(-gamma, __dsub_rn(1.0, dw));
+  }
+}
+
 // Cosine variant: scores already computed (rows x C); model.cpp:109-113 score_to_delta.
 __global__ void online_score_cosine_kernel(const double* __restrict__ scores, uint32_t C, uint64_t rows,
                                            const int32_t* __restrict__ labels, double gamma,
@@ -838,6 +886,67 @@ hv_status hv_dev_online_delta(hv_context* ctx, const uint32_t* class_vectors, si
     OnlineScratch s(C, rows, false, st);
     online_batch<true>(ctx, st, s, HV_METRIC_HAMMING, class_vectors, nullptr, C, D, batch, rows, labels, gamma, nullptr,
                        delta_acc, delta_weight, delta_counts, nullptr, delta_touched);
+  });
+}
+
+// ---- D-sliced exact online training (one word slice per rank) ----
+hv_status hv_dev_online_slice_init(hv_context* ctx, const uint32_t* batch0, size_t rows0, const int32_t* labels,
+                                   size_t class_count, size_t dim, size_t word_begin, size_t words,
+                                   const uint32_t* tiebreak, double* acc, double* weight, uint64_t* counts,
+                                   uint32_t* class_vectors) {
+  return guarded([&] {
+    require(ctx);
+    cudaStream_t st = ctx->stream;
+    const size_t C = class_count, W = words_per_row(dim);
+    if (C == 0 || dim == 0) invalid("train_online: empty model");
+    if (words == 0 || word_begin + words > W) invalid("online slice: word range outside the row");
+    const size_t Ds = std::min(dim, 32 * (word_begin + words)) - 32 * word_begin;
+    DevBuf<uint32_t> cnt(C * 32 * words, st);
+    DevBuf<uint64_t> crow(C, st);
+    cnt.zero();
+    crow.zero();
+    class_counts_device(ctx, st, batch0, rows0, words, labels, C, cnt.ptr, crow.ptr);
+    init_from_counts_kernel<<<sgrid(ctx, C * Ds, 256), 256, 0, st>>>(cnt.ptr, crow.ptr, C, Ds, words, acc, weight,
+                                                                      counts);
+    launched("init_from_counts_kernel");
+    binarize_counts_device(ctx, st, cnt.ptr, crow.ptr, C, Ds, tiebreak + word_begin, class_vectors);
+  });
+}
+
+hv_status hv_dev_online_partial_popc(hv_context* ctx, const uint32_t* class_vectors, size_t class_count, size_t words,
+                                     const uint32_t* batch, size_t rows, uint32_t* popc) {
+  return guarded([&] {
+    require(ctx);
+    if (rows == 0 || class_count == 0) return;
+    online_partial_popc_kernel<<<sgrid(ctx, rows * 32, 256, 8), 256, 0, ctx->stream>>>(
+        class_vectors, static_cast<uint32_t>(class_count), static_cast<uint32_t>(words), batch, rows, popc);
+    launched("online_partial_popc_kernel");
+  });
+}
+
+hv_status hv_dev_online_slice_update(hv_context* ctx, const uint32_t* popc, size_t class_count, size_t dim,
+                                     size_t word_begin, size_t words, const uint32_t* batch, size_t rows,
+                                     const int32_t* labels, double gamma, const uint32_t* tiebreak, double* acc,
+                                     double* weight, uint64_t* counts, uint32_t* class_vectors) {
+  return guarded([&] {
+    require(ctx);
+    cudaStream_t st = ctx->stream;
+    const size_t C = class_count, W = words_per_row(dim);
+    if (words == 0 || word_begin + words > W) invalid("online slice: word range outside the row");
+    if (rows == 0) return;
+    const size_t Ds = std::min(dim, 32 * (word_begin + words)) - 32 * word_begin;
+    OnlineScratch s(C, rows, false, st);
+    online_score_popc_kernel<<<sgrid(ctx, rows, 128), 128, 0, st>>>(popc, static_cast<uint32_t>(C),
+                                                                    static_cast<uint32_t>(dim), rows, labels, gamma,
+                                                                    s.pred.ptr, s.dtrue.ptr, s.pen.ptr, ctx->d_err);
+    launched("online_score_popc_kernel");
+    online_lists_kernel<<<C, 32, 0, st>>>(labels, s.pred.ptr, s.dtrue.ptr, s.pen.ptr, rows, C, s.cap, s.idx.ptr,
+                                          s.val.ptr, s.len.ptr, weight, counts, nullptr);
+    launched("online_lists_kernel");
+    dim3 grid((Ds + 255) / 256, C);
+    online_update_kernel<false><<<grid, 256, 0, st>>>(batch, Ds, words, s.cap, s.idx.ptr, s.val.ptr, s.len.ptr, weight,
+                                                      tiebreak + word_begin, acc, class_vectors);
+    launched("online_update_kernel");
   });
 }
 

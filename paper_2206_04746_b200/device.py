@@ -131,6 +131,19 @@ class Engine:
                                       _ptr(self.cb.encode_tiebreak), _ptr(out)))
         return out
 
+    def encode_words(self, bins8: torch.Tensor, word_begin: int, words: int,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+        """Encode only output words [word_begin, word_begin + words) of every row
+        (the column slice a rank owns in D-sliced training)."""
+        rows, ldb = bins8.shape
+        if out is None:
+            out = torch.empty((rows, words), dtype=I32, device=self.dev)
+        N.check(N.lib().hv_dev_encode_words(self.dc.h, _ptr(bins8), ldb, rows, self.cb.features,
+                                            _ptr(self.cb.id_vectors), _ptr(self.cb.value_vectors), self.cb.bins,
+                                            self.D, self.cb.binding, _ptr(self.cb.encode_tiebreak), word_begin,
+                                            words, _ptr(out), out.stride(0)))
+        return out
+
     # -- classical -----------------------------------------------------------
     def zero_counts(self):
         return (torch.zeros((self.C, 32 * self.W), dtype=I32, device=self.dev),
@@ -229,7 +242,80 @@ class Engine:
         return acc, weight, cnt, cv
 
 
+class DSlicedOnline:
+    """Exact multi-GPU online training by output-word slices.
+
+    Rank r owns words [w0, w0 + words) of every hypervector (`word_slice`) and
+    the matching columns of the fp64 accumulators; class weights and counts
+    are replicated. Per batch the only collective is the all-reduce of the
+    rows x C partial Hamming popcounts, after which every rank derives the
+    same predictions and deltas and replays the reference's sample-ordered
+    in-place additions (model.cpp:54-63, 250-280) on its own columns — so
+    accumulators, class vectors and labels are bit-identical to the
+    single-GPU trainer for any number of ranks.
+
+    `enc_slice` is this rank's rows x words slice of ALL rows (Engine.encode_words);
+    labels are replicated.
+    """
+
+    def __init__(self, engine: "Engine", enc_slice: torch.Tensor, labels: torch.Tensor, batch_size: int, w0: int,
+                 gamma: float = 1.0):
+        if batch_size < 1:
+            raise ValueError("train_online: batch_size must be >= 1")
+        self.e, self.enc, self.labels = engine, enc_slice, labels
+        self.rows, self.words = enc_slice.shape
+        self.bsz, self.w0, self.gamma = batch_size, w0, gamma
+        e = engine
+        self.slice_bits = min(e.D, 32 * (w0 + self.words)) - 32 * w0
+        self.acc = torch.empty((e.C, self.slice_bits), dtype=torch.float64, device=e.dev)
+        self.weight = torch.empty(e.C, dtype=torch.float64, device=e.dev)
+        self.counts = torch.empty(e.C, dtype=torch.int64, device=e.dev)
+        self.cv = torch.empty((e.C, self.words), dtype=I32, device=e.dev)
+        self.popc = torch.empty((min(batch_size, max(self.rows, 1)), e.C), dtype=I32, device=e.dev)
+        first = min(batch_size, self.rows)
+        N.check(N.lib().hv_dev_online_slice_init(e.dc.h, _ptr(enc_slice), first, _ptr(labels), e.C, e.D, w0,
+                                                 self.words, _ptr(e.cb.model_tiebreak), _ptr(self.acc),
+                                                 _ptr(self.weight), _ptr(self.counts), _ptr(self.cv)))
+
+    def batches(self):
+        return [(s, min(self.bsz, self.rows - s)) for s in range(0, self.rows, self.bsz)]
+
+    def partial(self, start: int, n: int) -> torch.Tensor:
+        """This rank's partial popcounts of batch [start, start+n) (to be summed over ranks)."""
+        e = self.e
+        out = self.popc[:n]
+        N.check(N.lib().hv_dev_online_partial_popc(e.dc.h, _ptr(self.cv), e.C, self.words,
+                                                   _ptr(self.enc[start:start + n]), n, _ptr(out)))
+        return out
+
+    def update(self, start: int, n: int, popc: torch.Tensor):
+        e = self.e
+        N.check(N.lib().hv_dev_online_slice_update(e.dc.h, _ptr(popc), e.C, e.D, self.w0, self.words,
+                                                   _ptr(self.enc[start:start + n]), n,
+                                                   _ptr(self.labels[start:start + n]), self.gamma,
+                                                   _ptr(e.cb.model_tiebreak), _ptr(self.acc), _ptr(self.weight),
+                                                   _ptr(self.counts), _ptr(self.cv)))
+
+    def run(self, group=None):
+        """All batches; all-reduces the popcounts when torch.distributed has >1 rank."""
+        dist = torch.distributed
+        multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+        for start, n in self.batches():
+            p = self.partial(start, n)
+            if multi:
+                dist.all_reduce(p, group=group)
+            self.update(start, n, p)
+        return self.acc, self.weight, self.counts, self.cv
+
+
 # ------------------------------------------------------------ sharding --
+def word_slice(words: int, rank: int, world: int) -> tuple[int, int]:
+    """Balanced contiguous split of a row's words: (first word, word count) of `rank`."""
+    base, extra = divmod(words, world)
+    w0 = rank * base + min(rank, extra)
+    return w0, base + (1 if rank < extra else 0)
+
+
 def shard_range(rows: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous row shard of rank `rank` (the GPU analogue of parallel_rows, parallel.cpp:10-36)."""
     chunk = (rows + world - 1) // world

@@ -410,3 +410,50 @@ def test_device_online_delta_mode_emulated_ranks():
     bits = O.unpack_rows(diff, D).astype(bool)
     margin = (2.0 * acc_x - w_x[:, None]).abs().cpu().numpy()
     assert np.all(margin[bits] <= 1e-9 * w_x.cpu().numpy()[np.nonzero(bits)[0]]), "flip away from a tie"
+
+
+@pytest.mark.parametrize("F,D,C,rows,bsz,world", [(561, 10000, 6, 3000, 256, 2), (561, 10000, 6, 1500, 1, 3),
+                                                  (342, 1000, 2, 2000, 1024, 3), (617, 10000, 26, 2000, 100, 8)])
+def test_dsliced_online_emulated_ranks_bitexact(F, D, C, rows, bsz, world):
+    """Exact multi-GPU online training (device.DSlicedOnline) with `world`
+    ranks emulated on one GPU: each rank encodes only its word slice, the
+    per-batch partial popcounts are summed (the all-reduce), and the stitched
+    accumulators / class vectors / weights are bit-identical to the
+    single-GPU exact trainer (itself bit-exact vs the reference)."""
+    from paper_2206_04746_b200 import device as dv
+    cbk = dv.DeviceCodebook.make(F, 16, D, seed=F + world)
+    eng = dv.Engine(cbk, C)
+    bins8, labels = eng.synth(0, rows, 0, 7)
+    enc = eng.encode(bins8)
+    acc_x, w_x, c_x, cv_x = eng.train_online(enc, labels, bsz)
+    W = enc.shape[1]
+    ranks = []
+    for r in range(world):
+        w0, nw = dv.word_slice(W, r, world)
+        sl = eng.encode_words(bins8, w0, nw)
+        assert torch.equal(sl, enc[:, w0:w0 + nw])
+        ranks.append(dv.DSlicedOnline(eng, sl, labels, bsz, w0))
+    for start, n in ranks[0].batches():
+        tot = sum(rk.partial(start, n).clone() for rk in ranks)
+        for rk in ranks:
+            rk.update(start, n, tot)
+    eng.dc.check()
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([rk.acc for rk in ranks], dim=1), acc_x)
+    assert torch.equal(torch.cat([rk.cv for rk in ranks], dim=1), cv_x)
+    for rk in ranks:
+        assert torch.equal(rk.weight, w_x) and torch.equal(rk.counts, c_x)
+
+
+def test_encode_words_slices_and_generic_fallback():
+    """hv_dev_encode_words for id-level (fused path) and permutation (whole-row
+    scratch + slice copy) equals the matching columns of a full encode."""
+    from paper_2206_04746_b200 import device as dv
+    import paper_2206_04746_b200._native as N
+    for binding in (N.BIND_ID_LEVEL, N.BIND_PERMUTATION):
+        cbk = dv.DeviceCodebook.make(100, 16, 2000, seed=9, binding=binding)
+        eng = dv.Engine(cbk, 2)
+        bins8, _ = eng.synth(0, 333, 0, 3)
+        full = eng.encode(bins8)
+        for w0, nw in [(0, 63), (5, 1), (17, 46), (62, 1)]:
+            assert torch.equal(eng.encode_words(bins8, w0, nw), full[:, w0:w0 + nw]), (binding, w0, nw)

@@ -158,3 +158,95 @@ def test_online_delta_mode_is_within_tolerance_of_exact(world):
     np.testing.assert_allclose(acc, exact.acc, rtol=1e-5, atol=1e-9)
     np.testing.assert_allclose(weight, exact.weight, rtol=1e-5)
     np.testing.assert_array_equal(cv, exact.cv)
+
+
+def test_word_slices_partition_rows():
+    from paper_2206_04746_b200.device import word_slice
+    for words in (1, 7, 32, 313, 1024):
+        for world in (1, 2, 3, 4, 8):
+            if world > words:
+                continue
+            sl = [word_slice(words, r, world) for r in range(world)]
+            assert sl[0][0] == 0 and sum(n for _, n in sl) == words
+            assert all(a[0] + a[1] == b[0] for a, b in zip(sl, sl[1:]))
+            assert max(n for _, n in sl) - min(n for _, n in sl) <= 1
+
+
+def _dsliced_worker(rank, world, port, enc, y, C, D, bsz, gamma, tb, q):
+    """NumPy restatement of device.DSlicedOnline on one rank: partial popcounts
+    over its words, gloo all-reduce, sample-ordered updates of its columns."""
+    from paper_2206_04746_b200.device import word_slice
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    W = enc.shape[1]
+    w0, nw = word_slice(W, rank, world)
+    j0, j1 = 32 * w0, min(D, 32 * (w0 + nw))
+    dense = O.unpack_rows(enc, D)[:, j0:j1]
+    tbits = O.unpack_rows(tb, D)[0, j0:j1]
+    n = enc.shape[0]
+    first = min(bsz, n)
+    acc = np.zeros((C, j1 - j0))
+    weight = np.zeros(C)
+    counts = np.zeros(C, np.int64)
+    for c in range(C):
+        acc[c] = dense[:first][y[:first] == c].sum(axis=0)
+        weight[c] = counts[c] = (y[:first] == c).sum()
+
+    def binarize():
+        tw = 2.0 * acc
+        return np.where(tw > weight[:, None], 1, np.where(tw < weight[:, None], 0, tbits[None, :])).astype(np.uint8)
+
+    cv = binarize()
+    for start in range(0, n, bsz):
+        m = min(bsz, n - start)
+        part = np.stack([(cv != dense[i][None, :]).sum(axis=1) for i in range(start, start + m)]).astype(np.int32)
+        pt = torch.from_numpy(part)
+        dist.all_reduce(pt)
+        pops = pt.numpy()
+        for k, i in enumerate(range(start, start + m)):
+            pred = int(np.argmin(pops[k]))
+            t = int(y[i])
+            dt = pops[k][t] / D
+            acc[t] = np.where(dense[i] == 1, acc[t] + dt, acc[t])
+            weight[t] += dt
+            counts[t] += 1
+            if pred != t:
+                pen = -gamma * (1.0 - pops[k][pred] / D)
+                acc[pred] = np.where(dense[i] == 1, acc[pred] + pen, acc[pred])
+        cv = binarize()
+    parts = [None] * world
+    dist.all_gather_object(parts, (acc, cv, weight, counts))
+    if rank == 0:
+        q.put(parts)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,D", [(2, 256), (3, 1000)])
+def test_dsliced_online_is_bit_exact_with_one_process(world, D):
+    """The D-sliced multi-GPU online protocol (one all-reduce of integer
+    popcounts per batch) reproduces the exact reference trainer bit for bit."""
+    rng = np.random.default_rng(world + D)
+    C, n, bsz = 3, 150, 32
+    centers = rng.integers(0, 2, (C, D), dtype=np.uint8)
+    y = (np.arange(n) % C).astype(np.int32)
+    enc = O.pack_rows(centers[y] ^ (rng.random((n, D)) < 0.25).astype(np.uint8))
+    tb = O.generate_random(1, D, 13)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dsliced_worker, args=(r, world, port, enc, y, C, D, bsz, 1.0, tb, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    acc = np.concatenate([a for a, _, _, _ in parts], axis=1)
+    cv = np.concatenate([c for _, c, _, _ in parts], axis=1)
+    exact = O.NaiveModel(C, D, tb).train_online(enc, y, bsz)
+    np.testing.assert_array_equal(acc, exact.acc)
+    np.testing.assert_array_equal(cv, exact.cv)
+    for _, _, w, cnt in parts:
+        np.testing.assert_array_equal(w, exact.weight)
+        np.testing.assert_array_equal(cnt, exact.counts.astype(np.int64))
