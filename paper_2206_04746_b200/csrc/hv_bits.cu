@@ -149,19 +149,31 @@ __global__ void __launch_bounds__(128) column_count_kernel(const uint32_t* __res
     const uint64_t e = seg_off ? min(p1, seg_off[s + 1]) : p1;
     if (e > p0) {
       HSCounter<8> h;
-      for (uint64_t p = p0; p < e; p += 16) {
-        uint32_t x[16];
+      // 32 row loads in flight per thread; the permutation of the next batch
+      // is fetched while this one's rows are loaded (two dependent loads per
+      // batch would otherwise serialise)
+      uint32_t rows_nx[32];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          const uint64_t q = p + t;
-          uint32_t v = 0;
-          if (active && q < e) {
-            const uint64_t row = perm ? perm[q] : q;
-            v = m[row * W + w];
+      for (int t = 0; t < 32; ++t) {
+        const uint64_t q = p0 + t;
+        rows_nx[t] = q < e ? (perm ? perm[q] : static_cast<uint32_t>(q)) : 0u;
+      }
+      for (uint64_t p = p0; p < e; p += 32) {
+        uint32_t rr[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) rr[t] = rows_nx[t];
+        uint32_t x[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) x[t] = (active && p + t < e) ? m[static_cast<uint64_t>(rr[t]) * W + w] : 0u;
+        if (p + 32 < e) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const uint64_t q = p + 32 + t;
+            rows_nx[t] = q < e ? (perm ? perm[q] : static_cast<uint32_t>(q)) : 0u;
           }
-          x[t] = v;
         }
         h.add16(x);
+        h.add16(x + 16);
       }
       if (active) {
         CT* dst = counts + s * stride + 32ull * w;
@@ -180,6 +192,7 @@ __global__ void __launch_bounds__(128) column_count_kernel(const uint32_t* __res
 void launch_column_count_u32(cudaStream_t st, const uint32_t* m, uint32_t W, const uint32_t* perm,
                              const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, uint32_t* counts) {
   if (max_pos == 0 || W == 0) return;
+  if (max_pos > 0xFFFFFFFFull) invalid("class counts: more than 2^32 rows per call");
   const uint32_t chunk = 2048;
   dim3 grid(grid_for(W, 128), static_cast<unsigned>((max_pos + chunk - 1) / chunk));
   column_count_kernel<uint32_t><<<grid, 128, 0, st>>>(m, W, perm, seg_off, nseg, max_pos, chunk, counts);
