@@ -163,6 +163,12 @@ bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
                const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
                uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo);
 
+// Online training, Hamming metric: every batch in one persistent cooperative
+// kernel (hv_online.cu); acc/weight/counts/cv hold the bootstrap state.
+void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* enc, size_t rows, size_t D,
+                             const int32_t* labels, size_t C, size_t bsz, double gamma, const uint32_t* tie,
+                             double* acc, double* weight, uint64_t* counts, uint32_t* cv);
+
 // Host-side codebook helpers shared by several entry points (hv_host.cpp).
 void generate_random_words(size_t count, size_t dim, uint64_t seed, uint32_t* out);
 uint64_t derive_seed(uint64_t seed, uint64_t tag);

@@ -17,6 +17,7 @@
 // update of that batch is applied.
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
 #include <memory>
@@ -579,6 +580,11 @@ void train_online_device(hv_context* ctx, cudaStream_t st, hv_metric metric, con
     binarize_counts_device(ctx, st, cnt.ptr, crow.ptr, C, D, tie, cv);
   }
   if (rows == 0) return;
+  const char* legacy = getenv("HVB200_ONLINE_LEGACY");
+  if (metric == HV_METRIC_HAMMING && !(legacy && legacy[0] == '1')) {
+    train_online_persistent(ctx, st, enc, rows, D, labels, C, bsz, gamma, tie, acc, weight, counts, cv);
+    return;
+  }
   OnlineScratch s(C, std::min(bsz, rows), metric == HV_METRIC_COSINE, st);
   DevBuf<double> snap(metric == HV_METRIC_COSINE ? C * D : 0, st);
   for (size_t start = 0; start < rows; start += bsz) {
