@@ -346,6 +346,26 @@ def test_online_random_vs_oracle_bitexact(bsz):
     np.testing.assert_array_equal(on.class_vectors.words, oo.class_vectors)
 
 
+@pytest.mark.parametrize("C,D,n,bsz", [(2, 1000, 900, 300), (1, 333, 600, 64), (3, 1000, 700, 256), (8, 333, 600, 64),
+                                       (26, 2048, 800, 100), (32, 777, 500, 128), (100, 4096, 600, 512),
+                                       (40, 64, 300, 1), (3, 70, 257, 256), (6, 10000, 2100, 1024)])
+def test_online_modes_vs_oracle_bitexact(C, D, n, bsz):
+    """Every path of the persistent online trainer against the oracle:
+    MERGED (C <= 2), LISTS with warp-per-row scoring (2 < C < 32) and with
+    lane-per-class scoring (C >= 32); partial chunks, one-row batches, tails."""
+    rng = np.random.default_rng(C * 1000 + bsz)
+    centers = rng.integers(0, 2, (C, D), dtype=np.uint8)
+    y = rng.integers(0, C, n).astype(np.int32)
+    enc = O.pack_rows(centers[y] ^ (rng.random((n, D)) < 0.35).astype(np.uint8))
+    cfg = hv.ModelConfig(class_count=C, dim=D, gamma=0.9, seed=C + D)
+    on = hv.train_online(P(enc, D), y, bsz, cfg)
+    oo = O.NaiveModel(C, D, on.tiebreak.words, O.HAMMING, 0.9).train_online(enc, y, bsz)
+    np.testing.assert_array_equal(on.accumulators.reshape(C, D), oo.acc)
+    np.testing.assert_array_equal(on.class_weight, oo.weight)
+    np.testing.assert_array_equal(on.sample_counts, oo.counts)
+    np.testing.assert_array_equal(on.class_vectors.words, oo.class_vectors)
+
+
 # --------------------------------------------------- device pipeline ----
 def test_device_classical_and_predict_vs_oracle():
     from paper_2206_04746_b200 import device as dv
