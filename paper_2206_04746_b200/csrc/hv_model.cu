@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "hv_internal.cuh"
+#include "hv_scan.cuh"
 #include "hv_stage.h"
 
 namespace hvb {
@@ -185,6 +186,48 @@ __global__ void __launch_bounds__(256) predict_hamming_kernel(const uint32_t* __
       }
     }
     if (lane == 0 && labels) labels[r] = static_cast<int32_t>(best);
+  }
+}
+
+// Many classes (C >= 32): CTA-tiled scan (hv_scan.cuh), 32 rows x 32 classes
+// per tile, tiles ordered class-block-minor so the CTAs sharing a row tile run
+// together (the rows stay in L2). Per-row argmin merged across class blocks
+// with a 64-bit atomicMin on (popc << 32 | class) = the reference's strict-<
+// argmin.
+__global__ void __launch_bounds__(256) predict_tiled_kernel(const uint32_t* __restrict__ cv, uint32_t C, uint32_t D,
+                                                            uint32_t W, const uint32_t* __restrict__ enc,
+                                                            uint64_t rows, unsigned long long* __restrict__ best,
+                                                            double* __restrict__ dist, uint32_t* __restrict__ pops) {
+  __shared__ ScanSmem s;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t ncb = (C + kScanCls - 1) / kScanCls;
+  const uint64_t ntiles = (rows + kScanRows - 1) / kScanRows;
+  for (uint64_t it = blockIdx.x; it < ntiles * ncb; it += gridDim.x) {
+    const uint32_t cb = static_cast<uint32_t>(it % ncb);
+    const uint64_t row0 = (it / ncb) * kScanRows;
+    const uint32_t nr = static_cast<uint32_t>(min(static_cast<uint64_t>(kScanRows), rows - row0));
+    uint32_t a[kScanRowsPerWarp];
+    scan_tile<256>(enc, row0, nr, W, cv, C, cb * kScanCls, s, a);
+    const uint32_t c = cb * kScanCls + lane;
+#pragma unroll
+    for (int k = 0; k < kScanRowsPerWarp; ++k) {
+      const uint32_t r = warp * kScanRowsPerWarp + k;
+      if (r >= nr) break;
+      const uint64_t row = row0 + r;
+      if (c < C) {
+        if (pops) pops[row * C + c] = a[k];
+        if (dist) dist[row * C + c] = static_cast<double>(a[k]) / static_cast<double>(D);
+      }
+      const unsigned long long key = warp_min_u64(c < C ? scan_key(a[k], c) : ~0ull);
+      if (lane == 0) atomicMin(best + row, key);
+    }
+  }
+}
+
+__global__ void best_to_labels_kernel(const unsigned long long* __restrict__ best, uint64_t rows,
+                                      int32_t* __restrict__ labels) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows; r += (uint64_t)gridDim.x * blockDim.x) {
+    labels[r] = static_cast<int32_t>(static_cast<uint32_t>(best[r]));
   }
 }
 
@@ -496,6 +539,23 @@ void predict_hamming_device(hv_context* ctx, cudaStream_t st, const uint32_t* cv
                             const uint32_t* enc, size_t rows, int32_t* labels, double* dist, uint32_t* pops) {
   if (rows == 0) return;
   const size_t W = words_per_row(D);
+  if (C >= static_cast<size_t>(kScanCls) && getenv("HVB200_PREDICT_WARP") == nullptr) {
+    DevBuf<unsigned long long> best(rows, st);
+    ck(cudaMemsetAsync(best.ptr, 0xFF, rows * sizeof(unsigned long long), st), "memset");
+    int per_sm = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, predict_tiled_kernel, 256, 0), "occupancy");
+    const uint64_t items = ((rows + kScanRows - 1) / kScanRows) * ((C + kScanCls - 1) / kScanCls);
+    const unsigned g = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>(items, static_cast<uint64_t>(ctx->sm_count) * std::max(per_sm, 1))));
+    predict_tiled_kernel<<<g, 256, 0, st>>>(cv, static_cast<uint32_t>(C), static_cast<uint32_t>(D),
+                                            static_cast<uint32_t>(W), enc, rows, best.ptr, dist, pops);
+    launched("predict_tiled_kernel");
+    if (labels) {
+      best_to_labels_kernel<<<sgrid(ctx, rows, 256), 256, 0, st>>>(best.ptr, rows, labels);
+      launched("best_to_labels_kernel");
+    }
+    return;
+  }
   const unsigned grid = sgrid(ctx, rows * 32, 256, 8);
   if (C <= 2) {
     predict_hamming_kernel<2><<<grid, 256, 0, st>>>(cv, C, D, W, enc, rows, labels, dist, pops);

@@ -12,13 +12,14 @@
 // score   (all warps)  per row: Hamming popcount against every class vector,
 //         argmin (strict <, lowest class on ties, model.cpp:96-104) packed as
 //         best = popc << 32 | class, plus the true class's popcount.
-//         C < 32: warp per row, lanes over words. C >= 32: lane = class over a
-//         transposed copy of the class vectors (coalesced), 4 rows per warp,
-//         per-row argmin merged across class blocks with a 64-bit atomicMin.
+//         C < 32: warp per row, lanes over words. C >= 32: CTA-tiled scan
+//         (hv_scan.cuh: 32 rows x 32 classes per tile, lane = class, words
+//         through shared memory), per-row argmin merged across class blocks
+//         with a 64-bit atomicMin.
 //
-// Two classes (C <= kMergedMaxC) — MERGED:
-//   replay  item = (class c, 8-word block): the batch is streamed in 256-row
-//           chunks; each chunk's labels/scores and the 8 words of every row
+// Two classes (C <= kMergedMaxC) or batches of <= 32 rows — MERGED:
+//   replay  item = (class c, 32-word block, 4 bit columns per thread): the
+//           batch is streamed in 64-row chunks; each chunk's labels/scores and the 8 words of every row
 //           are loaded one chunk ahead into registers (the next chunk's loads
 //           fly while this chunk is replayed), thread j replays the chunk's
 //           entries of class c in row order on its register-held acc[c][j]
@@ -30,7 +31,7 @@
 // Many classes — LISTS:
 //   lists   CTA per class: the batch's entries compacted in row order (block
 //           ballot + prefix) into a global list, weight chain, sample counts.
-//   replay  item = (class, 8-word block) over its own list only (classes
+//   replay  item = (class, 32-word block) over its own list only (classes
 //           untouched by the batch are skipped), chunks prefetched as above.
 //
 // Touched classes are re-binarised with the batch's final weight
@@ -40,6 +41,7 @@
 #include <algorithm>
 
 #include "hv_internal.cuh"
+#include "hv_scan.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -47,11 +49,21 @@ namespace hvb {
 namespace {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
-constexpr int kOWords = 8;                  // words per replay item
-constexpr int kOChunk = 256;                // rows (MERGED) / list entries (LISTS) per chunk
-constexpr int kOReplay = kOWords * 32;      // replay threads: one per bit column
+// A replay item is (class, block of 8*COLS words); each of its 256 replay
+// threads owns COLS bit columns (independent accumulator chains) and the
+// staged tile holds 256/COLS entries x 8*COLS words (2,048 words) either way.
+// COLS = 1 suits long per-class lists (the chain length binds: fewer, longer
+// chunks), COLS = 4 short ones (many classes: 4x fewer items per batch).
+constexpr int kOReplay = 256;               // replay threads
 constexpr int kOThreads = kOReplay + 32;    // + one warp for the weight chain
-constexpr int kLoadsPer = (kOChunk * kOWords + kOThreads - 1) / kOThreads;  // word loads per thread per chunk
+constexpr int kOTile = 2048;                // staged words per chunk
+constexpr int kLChunk = 256;                // rows per compaction chunk (list building)
+constexpr int kLoadsPer = (kOTile + kOThreads - 1) / kOThreads;  // word loads per thread per chunk
+template <int COLS>
+struct RTile {
+  static constexpr int kWords = 8 * COLS;         // words per item
+  static constexpr int kChunk = kOTile / kWords;  // entries per chunk
+};
 constexpr uint32_t kMergedMaxC = 2;  // more classes: per-class lists skip the other classes' rows
 constexpr uint32_t kLaneClassMinC = 32;
 
@@ -67,8 +79,7 @@ struct OnlineParams {
   double* weight;              // 2 x C (MERGED: batch-parity ping-pong; LISTS: row 0)
   uint64_t* counts;            // C
   uint32_t* cv;                // C x W
-  uint32_t* cvt;               // W x C transposed class vectors (lane-class scoring)
-  unsigned long long* best;    // bsz: popc << 32 | class
+  unsigned long long* best;    // 2 x bsz (batch parity): popc << 32 | class
   uint32_t* truep;             // bsz
   uint32_t* lidx;              // C x bsz (LISTS)
   double* lval;                // C x bsz (LISTS)
@@ -84,8 +95,8 @@ __device__ __forceinline__ double penalty_of(unsigned long long best, double gam
 }
 
 // ---------------------------------------------------------------- score ----
-__device__ void score_warp_per_row(const OnlineParams& p, uint64_t b0, uint32_t n, uint64_t gwarp, uint64_t gwarps,
-                                   uint32_t lane) {
+__device__ void score_warp_per_row(const OnlineParams& p, unsigned long long* best_out, uint64_t b0, uint32_t n,
+                                   uint64_t gwarp, uint64_t gwarps, uint32_t lane) {
   for (uint64_t r = gwarp; r < n; r += gwarps) {
     const uint32_t* q = p.enc + (b0 + r) * p.W;
     const int32_t y = p.labels[b0 + r];
@@ -102,85 +113,115 @@ __device__ void score_warp_per_row(const OnlineParams& p, uint64_t b0, uint32_t 
       if (static_cast<int32_t>(c) == y) truep = a;
     }
     if (lane == 0) {
-      p.best[r] = (static_cast<unsigned long long>(bestp) << 32) | best;
+      best_out[r] = (static_cast<unsigned long long>(bestp) << 32) | best;
       p.truep[r] = truep;
     }
   }
 }
 
-constexpr int kLcRows = 4;
-
-__device__ void score_lane_class(const OnlineParams& p, uint64_t b0, uint32_t n, uint64_t gwarp, uint64_t gwarps,
-                                 uint32_t lane) {
-  const uint32_t ncb = (p.C + 31) / 32;
-  const uint64_t ngr = (n + kLcRows - 1) / kLcRows;
-  for (uint64_t it = gwarp; it < ngr * ncb; it += gwarps) {
+// C >= 32: CTA-tiled scan (hv_scan.cuh) over (32-row tile, 32-class block)
+// items; per-row argmin merged across class blocks with a 64-bit atomicMin.
+__device__ void score_tiled(const OnlineParams& p, unsigned long long* best_out, ScanSmem& s, uint64_t b0, uint32_t n,
+                            uint32_t lane, uint32_t warp) {
+  const uint32_t ncb = (p.C + kScanCls - 1) / kScanCls;
+  const uint64_t ntiles = (n + kScanRows - 1) / kScanRows;
+  for (uint64_t it = blockIdx.x; it < ntiles * ncb; it += gridDim.x) {
     const uint32_t cb = static_cast<uint32_t>(it % ncb);
-    const uint64_t r0 = (it / ncb) * kLcRows;
-    const uint32_t c = cb * 32 + lane;
-    const bool cok = c < p.C;
-    const uint32_t* q[kLcRows];
+    const uint64_t t0 = (it / ncb) * kScanRows;
+    const uint32_t nr = static_cast<uint32_t>(min(static_cast<uint64_t>(kScanRows), n - t0));
+    uint32_t a[kScanRowsPerWarp];
+    scan_tile<kOThreads>(p.enc, b0 + t0, nr, p.W, p.cv, p.C, cb * kScanCls, s, a);
+    if (warp < kScanRows / kScanRowsPerWarp) {
+      const uint32_t c = cb * kScanCls + lane;
 #pragma unroll
-    for (int k = 0; k < kLcRows; ++k) q[k] = p.enc + (b0 + min(r0 + k, static_cast<uint64_t>(n) - 1)) * p.W;
-    uint32_t a[kLcRows] = {};
-#pragma unroll 4
-    for (uint32_t w = 0; w < p.W; ++w) {
-      const uint32_t cw = cok ? p.cvt[static_cast<uint64_t>(w) * p.C + c] : 0u;
-#pragma unroll
-      for (int k = 0; k < kLcRows; ++k) a[k] += __popc(__ldg(q[k] + w) ^ cw);
-    }
-#pragma unroll
-    for (int k = 0; k < kLcRows; ++k) {
-      const uint64_t r = r0 + k;
-      if (r >= n) break;
-      unsigned long long key = cok ? (static_cast<unsigned long long>(a[k]) << 32) | c : ~0ull;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long other = __shfl_xor_sync(kFull, key, o);
-        key = other < key ? other : key;
+      for (int k = 0; k < kScanRowsPerWarp; ++k) {
+        const uint32_t r = warp * kScanRowsPerWarp + k;
+        if (r >= nr) break;
+        const uint64_t row = t0 + r;
+        const unsigned long long key = warp_min_u64(c < p.C ? scan_key(a[k], c) : ~0ull);
+        if (lane == 0) atomicMin(best_out + row, key);
+        if (c < p.C && static_cast<int32_t>(c) == p.labels[b0 + row]) p.truep[row] = a[k];
       }
-      if (lane == 0) atomicMin(p.best + r, key);
-      if (cok && static_cast<int32_t>(c) == p.labels[b0 + r]) p.truep[r] = a[k];
     }
   }
 }
 
 // ------------------------------------------------------------- binarise ----
-__device__ __forceinline__ void binarize_store(const OnlineParams& p, uint32_t c, uint32_t j, bool col, double a,
-                                               double total, uint32_t lane) {
-  if (col) p.acc[static_cast<uint64_t>(c) * p.D + j] = a;
-  const uint32_t wi = min(j >> 5, p.W - 1);
-  uint32_t bit = 0;
-  if (col) {
-    const double twice = 2.0 * a;
-    bit = twice > total ? 1u : (twice < total ? 0u : ((p.tie[wi] >> lane) & 1u));
+// Thread (warp ww, lane l) of a replay item owns bit l of words
+// wb*8*COLS + ww + 8i, i < COLS. Stores its accumulators and, for touched classes, the re-binarised
+// class words (model.cpp:139-163).
+template <int COLS>
+__device__ __forceinline__ void store_columns(const OnlineParams& p, uint32_t c, uint32_t wb, const double (&a)[COLS],
+                                              double total, bool binarize) {
+  const uint32_t lane = threadIdx.x & 31u, ww = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < COLS; ++i) {
+    const uint32_t w = wb * RTile<COLS>::kWords + ww + 8u * i;
+    const uint32_t j = w * 32u + lane;
+    const bool col = w < p.W && j < p.D;
+    if (col) p.acc[static_cast<uint64_t>(c) * p.D + j] = a[i];
+    if (binarize) {
+      uint32_t bit = 0;
+      if (col) {
+        const double twice = 2.0 * a[i];
+        bit = twice > total ? 1u : (twice < total ? 0u : ((p.tie[w] >> lane) & 1u));
+      }
+      const uint32_t word = __ballot_sync(kFull, bit);
+      if (lane == 0 && w < p.W) p.cv[static_cast<uint64_t>(c) * p.W + w] = word;
+    }
   }
-  const uint32_t word = __ballot_sync(kFull, bit);
-  if (lane == 0 && (j >> 5) < p.W) {
-    p.cv[static_cast<uint64_t>(c) * p.W + (j >> 5)] = word;
-    if (p.cvt) p.cvt[static_cast<uint64_t>(j >> 5) * p.C + c] = word;
+}
+
+template <int COLS>
+__device__ __forceinline__ void load_columns(const OnlineParams& p, uint32_t c, uint32_t wb, double (&a)[COLS]) {
+  const uint32_t lane = threadIdx.x & 31u, ww = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < COLS; ++i) {
+    const uint32_t w = wb * RTile<COLS>::kWords + ww + 8u * i;
+    const uint32_t j = w * 32u + lane;
+    a[i] = (w < p.W && j < p.D) ? p.acc[static_cast<uint64_t>(c) * p.D + j] : 0.0;
+  }
+}
+
+// a[i] += v for the entries whose word (ww + 8i) has this lane's bit set, in
+// entry order; branch-free: an unset bit adds +0.0, which leaves every
+// accumulator bit-identical (acc is never -0.0: it starts from counts and
+// x + y == 0 rounds to +0.0).
+template <int COLS>
+__device__ __forceinline__ void replay_chunk(const uint32_t* words, const double* val, uint32_t m, double (&a)[COLS]) {
+  const uint32_t lane = threadIdx.x & 31u, ww = threadIdx.x >> 5;
+  constexpr int kUnroll = COLS == 1 ? 8 : 2;  // enough independent loads in flight ahead of the chain
+#pragma unroll kUnroll
+  for (uint32_t k = 0; k < m; ++k) {
+    const double v = val[k];
+#pragma unroll
+    for (int i = 0; i < COLS; ++i) {
+      const uint32_t wd = words[k * RTile<COLS>::kWords + ww + 8 * i];
+      a[i] = __dadd_rn(a[i], ((wd >> lane) & 1u) ? v : 0.0);
+    }
   }
 }
 
 struct Smem {
-  uint32_t words[2][kOChunk][kOWords];
-  double val[2][kOChunk];
-  uint8_t flag[2][kOChunk];  // MERGED: bit0 listed, bit1 true sample
-  uint32_t warpcnt[kOReplay / 32];
+  uint32_t words[2][kOTile];
+  double val[2][kLChunk];
+  uint8_t flag[2][kLChunk];  // MERGED: bit0 listed, bit1 true sample; lists: true sample
+  uint32_t warpcnt[kLChunk / 32];
   double weight;
 };
 
 // ------------------------------------------------------- MERGED replay ----
-__device__ void replay_merged(const OnlineParams& p, Smem& s, uint64_t b0, uint32_t n, uint32_t par) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  const uint32_t nwb = (p.W + kOWords - 1) / kOWords;
+template <int COLS>
+__device__ void replay_merged(const OnlineParams& p, const unsigned long long* bestv, Smem& s, uint64_t b0, uint32_t n,
+                              uint32_t par) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31u;
+  const uint32_t nwb = (p.W + RTile<COLS>::kWords - 1) / RTile<COLS>::kWords;
   const uint64_t items = static_cast<uint64_t>(p.C) * nwb;
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const uint32_t c = static_cast<uint32_t>(item / nwb);
     const uint32_t wb = static_cast<uint32_t>(item % nwb);
-    const uint32_t j = wb * kOReplay + tid;
-    const bool col = tid < kOReplay && j < p.D;
-    double a = col ? p.acc[static_cast<uint64_t>(c) * p.D + j] : 0.0;
+    double a[COLS];
+    if (tid < kOReplay) load_columns<COLS>(p, c, wb, a);
     double wsum = p.weight[par * p.C + c];
     uint64_t ntrue = 0;
     uint32_t mine = 0;  // this thread staged a listed row
@@ -192,9 +233,9 @@ __device__ void replay_merged(const OnlineParams& p, Smem& s, uint64_t b0, uint3
       const uint32_t r = ch + tid;
       rf = 0;
       rv = 0.0;
-      if (tid < kOChunk && r < n) {
+      if (tid < RTile<COLS>::kChunk && r < n) {
         const int32_t y = p.labels[b0 + r];
-        const unsigned long long bst = p.best[r];
+        const unsigned long long bst = bestv[r];
         const bool is_t = y == static_cast<int32_t>(c);
         const bool is_p = !is_t && static_cast<uint32_t>(bst) == c;
         if (is_t) rv = delta_of(p.truep[r], p.D);
@@ -204,13 +245,13 @@ __device__ void replay_merged(const OnlineParams& p, Smem& s, uint64_t b0, uint3
 #pragma unroll
       for (int i = 0; i < kLoadsPer; ++i) {
         const uint32_t e = tid + i * kOThreads;
-        const uint32_t k = e / kOWords, ww = e % kOWords;
-        const uint32_t w = wb * kOWords + ww;
-        rw[i] = (k < kOChunk && ch + k < n && w < p.W) ? __ldg(p.enc + (b0 + ch + k) * p.W + w) : 0u;
+        const uint32_t k = e / RTile<COLS>::kWords, ww = e % RTile<COLS>::kWords;
+        const uint32_t w = wb * RTile<COLS>::kWords + ww;
+        rw[i] = (k < RTile<COLS>::kChunk && ch + k < n && w < p.W) ? __ldg(p.enc + (b0 + ch + k) * p.W + w) : 0u;
       }
     };
     auto store_chunk = [&](uint32_t buf) {
-      if (tid < kOChunk) {
+      if (tid < RTile<COLS>::kChunk) {
         s.val[buf][tid] = rv;
         s.flag[buf][tid] = rf;
       }
@@ -218,29 +259,20 @@ __device__ void replay_merged(const OnlineParams& p, Smem& s, uint64_t b0, uint3
 #pragma unroll
       for (int i = 0; i < kLoadsPer; ++i) {
         const uint32_t e = tid + i * kOThreads;
-        const uint32_t k = e / kOWords, ww = e % kOWords;
-        if (k < kOChunk) s.words[buf][k][ww] = rw[i];
+        const uint32_t k = e / RTile<COLS>::kWords, ww = e % RTile<COLS>::kWords;
+        if (k < RTile<COLS>::kChunk) s.words[buf][k * RTile<COLS>::kWords + ww] = rw[i];
       }
     };
     load_chunk(0);
     store_chunk(0);
     __syncthreads();
     uint32_t buf = 0;
-    for (uint32_t ch = 0; ch < n; ch += kOChunk, buf ^= 1u) {
-      const bool more = ch + kOChunk < n;
-      if (more) load_chunk(ch + kOChunk);  // in flight during the replay below
-      const uint32_t m = min(static_cast<uint32_t>(kOChunk), n - ch);
-      // branch-free replay: non-listed rows carry value +0.0, and adding +0.0
-      // leaves every accumulator bit-identical (acc is never -0.0: it starts
-      // from counts and x + y == 0 rounds to +0.0)
+    for (uint32_t ch = 0; ch < n; ch += RTile<COLS>::kChunk, buf ^= 1u) {
+      const bool more = ch + RTile<COLS>::kChunk < n;
+      if (more) load_chunk(ch + RTile<COLS>::kChunk);  // in flight during the replay below
+      const uint32_t m = min(static_cast<uint32_t>(RTile<COLS>::kChunk), n - ch);
       if (tid < kOReplay) {
-        const uint32_t ww = warp, sh = lane;
-#pragma unroll 8
-        for (uint32_t k = 0; k < m; ++k) {
-          const uint32_t wd = s.words[buf][k][ww];
-          const double v = s.val[buf][k];
-          a = __dadd_rn(a, ((wd >> sh) & 1u) ? v : 0.0);
-        }
+        replay_chunk<COLS>(s.words[buf], s.val[buf], m, a);  // non-listed rows carry +0.0
       } else if (lane == 0) {
 #pragma unroll 8
         for (uint32_t k = 0; k < m; ++k) {
@@ -254,7 +286,7 @@ __device__ void replay_merged(const OnlineParams& p, Smem& s, uint64_t b0, uint3
     }
     if (tid == kOReplay) s.weight = wsum;
     const int touched = __syncthreads_or(mine);
-    if (touched && tid < kOReplay) binarize_store(p, c, j, col, a, s.weight, lane);
+    if (tid < kOReplay) store_columns<COLS>(p, c, wb, a, s.weight, touched != 0);
     if (wb == 0 && tid == kOReplay) {
       p.weight[(par ^ 1u) * p.C + c] = wsum;
       p.counts[c] += ntrue;
@@ -264,19 +296,19 @@ __device__ void replay_merged(const OnlineParams& p, Smem& s, uint64_t b0, uint3
 }
 
 // -------------------------------------------------------- LISTS phases ----
-__device__ void build_lists(const OnlineParams& p, Smem& s, uint64_t b0, uint32_t n) {
+__device__ void build_lists(const OnlineParams& p, const unsigned long long* bestv, Smem& s, uint64_t b0, uint32_t n) {
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   for (uint32_t c = blockIdx.x; c < p.C; c += gridDim.x) {
     double wsum = p.weight[c];
     uint64_t ntrue = 0;
     uint32_t len = 0;
-    for (uint32_t ch = 0; ch < n; ch += kOChunk) {
+    for (uint32_t ch = 0; ch < n; ch += kLChunk) {
       bool is_t = false, is_p = false;
       double v = 0.0;
       const uint32_t r = ch + tid;
-      if (tid < kOChunk && r < n) {
+      if (tid < kLChunk && r < n) {
         const int32_t y = p.labels[b0 + r];
-        const unsigned long long bst = p.best[r];
+        const unsigned long long bst = bestv[r];
         is_t = y == static_cast<int32_t>(c);
         is_p = !is_t && static_cast<uint32_t>(bst) == c;
         if (is_t) v = delta_of(p.truep[r], p.D);
@@ -284,11 +316,11 @@ __device__ void build_lists(const OnlineParams& p, Smem& s, uint64_t b0, uint32_
       }
       const bool flag = is_t || is_p;
       const uint32_t bal = __ballot_sync(kFull, flag);
-      if (warp < kOChunk / 32 && lane == 0) s.warpcnt[warp] = __popc(bal);
+      if (warp < kLChunk / 32 && lane == 0) s.warpcnt[warp] = __popc(bal);
       __syncthreads();
       uint32_t m = 0, off = 0;
 #pragma unroll
-      for (int k = 0; k < kOChunk / 32; ++k) {
+      for (int k = 0; k < kLChunk / 32; ++k) {
         off += (static_cast<uint32_t>(k) < warp) ? s.warpcnt[k] : 0u;
         m += s.warpcnt[k];
       }
@@ -319,70 +351,68 @@ __device__ void build_lists(const OnlineParams& p, Smem& s, uint64_t b0, uint32_
   }
 }
 
+template <int COLS>
 __device__ void replay_lists(const OnlineParams& p, Smem& s, uint64_t b0) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  const uint32_t nwb = (p.W + kOWords - 1) / kOWords;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t nwb = (p.W + RTile<COLS>::kWords - 1) / RTile<COLS>::kWords;
   const uint64_t items = static_cast<uint64_t>(p.C) * nwb;
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const uint32_t c = static_cast<uint32_t>(item / nwb);
     const uint32_t len = p.llen[c];
     if (len == 0) continue;  // untouched class: acc and class vector unchanged
     const uint32_t wb = static_cast<uint32_t>(item % nwb);
-    const uint32_t j = wb * kOReplay + tid;
-    const bool col = tid < kOReplay && j < p.D;
-    double a = col ? p.acc[static_cast<uint64_t>(c) * p.D + j] : 0.0;
+    double a[COLS];
+    if (tid < kOReplay) load_columns<COLS>(p, c, wb, a);
     const uint32_t* li = p.lidx + static_cast<uint64_t>(c) * p.bsz;
     const double* lv = p.lval + static_cast<uint64_t>(c) * p.bsz;
     uint32_t rw[kLoadsPer];
     double rv = 0.0;
     auto load_chunk = [&](uint32_t k0) {
-      const uint32_t m = min(static_cast<uint32_t>(kOChunk), len - k0);
+      const uint32_t m = min(static_cast<uint32_t>(RTile<COLS>::kChunk), len - k0);
       if (tid < m) rv = lv[k0 + tid];
 #pragma unroll
       for (int i = 0; i < kLoadsPer; ++i) {
         const uint32_t e = tid + i * kOThreads;
-        const uint32_t k = e / kOWords, ww = e % kOWords;
-        const uint32_t w = wb * kOWords + ww;
+        const uint32_t k = e / RTile<COLS>::kWords, ww = e % RTile<COLS>::kWords;
+        const uint32_t w = wb * RTile<COLS>::kWords + ww;
         rw[i] = (k < m && w < p.W) ? __ldg(p.enc + (b0 + li[k0 + k]) * p.W + w) : 0u;
       }
     };
     auto store_chunk = [&](uint32_t buf) {
-      if (tid < kOChunk) s.val[buf][tid] = rv;
+      if (tid < RTile<COLS>::kChunk) s.val[buf][tid] = rv;
 #pragma unroll
       for (int i = 0; i < kLoadsPer; ++i) {
         const uint32_t e = tid + i * kOThreads;
-        const uint32_t k = e / kOWords, ww = e % kOWords;
-        if (k < kOChunk) s.words[buf][k][ww] = rw[i];
+        const uint32_t k = e / RTile<COLS>::kWords, ww = e % RTile<COLS>::kWords;
+        if (k < RTile<COLS>::kChunk) s.words[buf][k * RTile<COLS>::kWords + ww] = rw[i];
       }
     };
     load_chunk(0);
     store_chunk(0);
     __syncthreads();
     uint32_t buf = 0;
-    for (uint32_t k0 = 0; k0 < len; k0 += kOChunk, buf ^= 1u) {
-      const bool more = k0 + kOChunk < len;
-      if (more) load_chunk(k0 + kOChunk);
-      const uint32_t m = min(static_cast<uint32_t>(kOChunk), len - k0);
-      if (tid < kOReplay) {
-        const uint32_t ww = warp, sh = lane;
-#pragma unroll 8
-        for (uint32_t k = 0; k < m; ++k) {
-          const uint32_t wd = s.words[buf][k][ww];
-          const double v = s.val[buf][k];
-          a = __dadd_rn(a, ((wd >> sh) & 1u) ? v : 0.0);
-        }
-      }
+    for (uint32_t k0 = 0; k0 < len; k0 += RTile<COLS>::kChunk, buf ^= 1u) {
+      const bool more = k0 + RTile<COLS>::kChunk < len;
+      if (more) load_chunk(k0 + RTile<COLS>::kChunk);
+      const uint32_t m = min(static_cast<uint32_t>(RTile<COLS>::kChunk), len - k0);
+      if (tid < kOReplay) replay_chunk<COLS>(s.words[buf], s.val[buf], m, a);
       if (more) store_chunk(buf ^ 1u);
       __syncthreads();
     }
-    if (tid < kOReplay) binarize_store(p, c, j, col, a, p.weight[c], lane);
+    if (tid < kOReplay) store_columns<COLS>(p, c, wb, a, p.weight[c], true);
   }
 }
 
-template <bool MERGED>
-__global__ void __launch_bounds__(kOThreads) online_persistent_kernel(OnlineParams p) {
+union OnlineSmem {
+  Smem replay;
+  ScanSmem scan;  // used only between the batch-start and the next grid barrier
+};
+
+template <bool MERGED, int COLS>
+__global__ void __launch_bounds__(kOThreads, 3) online_persistent_kernel(OnlineParams p) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ Smem s;
+  __shared__ OnlineSmem u;
+  Smem& s = u.replay;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint64_t gwarps = static_cast<uint64_t>(gridDim.x) * (kOThreads / 32);
   const uint64_t gwarp = static_cast<uint64_t>(blockIdx.x) * (kOThreads / 32) + warp;
@@ -390,32 +420,28 @@ __global__ void __launch_bounds__(kOThreads) online_persistent_kernel(OnlinePara
   uint32_t par = 0;
   for (uint64_t b0 = 0; b0 < p.rows; b0 += p.bsz, par ^= 1u) {
     const uint32_t n = static_cast<uint32_t>(min(p.bsz, p.rows - b0));
+    // per-row argmin keys, double-buffered by batch parity: the atomicMin
+    // targets of the next batch are reset while this batch still reads its own
+    unsigned long long* bestv = p.best + par * p.bsz;
     if (lane_class) {
-      score_lane_class(p, b0, n, gwarp, gwarps, lane);
+      score_tiled(p, bestv, u.scan, b0, n, lane, warp);
     } else {
-      score_warp_per_row(p, b0, n, gwarp, gwarps, lane);
+      score_warp_per_row(p, bestv, b0, n, gwarp, gwarps, lane);
     }
     grid.sync();
     if constexpr (MERGED) {
-      replay_merged(p, s, b0, n, par);
+      replay_merged<COLS>(p, bestv, s, b0, n, par);
     } else {
-      build_lists(p, s, b0, n);
+      build_lists(p, bestv, s, b0, n);
       grid.sync();
-      replay_lists(p, s, b0);
+      replay_lists<COLS>(p, s, b0);
     }
-    if (lane_class) {  // the atomicMin targets of the next batch
+    if (lane_class) {
+      unsigned long long* nxt = p.best + (par ^ 1u) * p.bsz;
       const uint64_t gt = static_cast<uint64_t>(blockIdx.x) * kOThreads + threadIdx.x;
-      for (uint64_t r = gt; r < p.bsz; r += static_cast<uint64_t>(gridDim.x) * kOThreads) p.best[r] = ~0ull;
+      for (uint64_t r = gt; r < p.bsz; r += static_cast<uint64_t>(gridDim.x) * kOThreads) nxt[r] = ~0ull;
     }
     grid.sync();
-  }
-}
-
-__global__ void transpose_cv_kernel(const uint32_t* __restrict__ cv, uint32_t C, uint32_t W, uint32_t* __restrict__ cvt) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < static_cast<uint64_t>(C) * W;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t c = i / W, w = i % W;
-    cvt[w * C + c] = cv[i];
   }
 }
 
@@ -424,10 +450,10 @@ __global__ void weight_copy_kernel(const double* __restrict__ src, double* __res
   if (c < C) dst[c] = src[c];
 }
 
-template <bool MERGED>
+template <bool MERGED, int COLS>
 unsigned cooperative_grid(hv_context* ctx, uint64_t want) {
   int per_sm = 0;
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, online_persistent_kernel<MERGED>, kOThreads, 0),
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, online_persistent_kernel<MERGED, COLS>, kOThreads, 0),
      "occupancy");
   if (per_sm < 1) fail(HV_ERR_CUDA, "online_persistent_kernel does not fit on an SM");
   return static_cast<unsigned>(std::max<uint64_t>(
@@ -444,36 +470,35 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   if (rows == 0) return;
   const size_t W = words_per_row(D);
   const size_t n = std::min(bsz, rows);
-  const bool merged = C <= kMergedMaxC;
+  // MERGED also for tiny batches: streaming a few rows per item is cheaper
+  // than the extra grid barrier of the list phase
+  const bool merged = C <= kMergedMaxC || n <= 32;
   const bool lane_class = C >= kLaneClassMinC;
   DevBuf<double> wts(2 * C, st), lval(merged ? 0 : C * n, st);
-  DevBuf<unsigned long long> best(n, st);
-  DevBuf<uint32_t> truep(n, st), lidx(merged ? 0 : C * n, st), llen(merged ? 0 : C, st), cvt(lane_class ? C * W : 0, st);
+  DevBuf<unsigned long long> best(2 * n, st);
+  DevBuf<uint32_t> truep(n, st), lidx(merged ? 0 : C * n, st), llen(merged ? 0 : C, st);
   weight_copy_kernel<<<grid_for(C, 128), 128, 0, st>>>(weight, wts.ptr, static_cast<uint32_t>(C));
   launched("weight_copy_kernel");
-  if (lane_class) {
-    ck(cudaMemsetAsync(best.ptr, 0xFF, n * sizeof(unsigned long long), st), "memset");
-    transpose_cv_kernel<<<grid_for(C * W, 256, ctx->sm_count * 8), 256, 0, st>>>(cv, static_cast<uint32_t>(C),
-                                                                                static_cast<uint32_t>(W), cvt.ptr);
-    launched("transpose_cv_kernel");
-  }
-  const uint64_t items = static_cast<uint64_t>(C) * ((W + kOWords - 1) / kOWords);
+  if (lane_class) ck(cudaMemsetAsync(best.ptr, 0xFF, 2 * n * sizeof(unsigned long long), st), "memset");
+  // long per-class lists (few classes): one chain per thread; short ones: four
+  const bool cols4 = !merged && n < 64 * C;
+  const uint64_t items = static_cast<uint64_t>(C) * ((W + (cols4 ? 32 : 8) - 1) / (cols4 ? 32 : 8));
   const uint64_t score_ctas = (n + kOThreads / 32 - 1) / (kOThreads / 32);
   const uint64_t want = std::max<uint64_t>(items, score_ctas);
   OnlineParams p{enc,     labels,   rows,     static_cast<uint32_t>(D), static_cast<uint32_t>(W),
-                 static_cast<uint32_t>(C), n, gamma, tie, acc, wts.ptr, counts, cv, lane_class ? cvt.ptr : nullptr,
-                 best.ptr, truep.ptr, lidx.ptr, lval.ptr, llen.ptr};
+                 static_cast<uint32_t>(C), n, gamma, tie, acc, wts.ptr, counts, cv, best.ptr, truep.ptr, lidx.ptr,
+                 lval.ptr, llen.ptr};
   void* args[] = {&p};
+  auto launch = [&](auto kern, unsigned grid) {
+    ck(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kOThreads), args, 0, st),
+       "online_persistent_kernel");
+  };
   if (merged) {
-    const unsigned grid = cooperative_grid<true>(ctx, want);
-    ck(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(online_persistent_kernel<true>), dim3(grid),
-                                   dim3(kOThreads), args, 0, st),
-       "online_persistent_kernel");
+    launch(online_persistent_kernel<true, 1>, cooperative_grid<true, 1>(ctx, want));
+  } else if (cols4) {
+    launch(online_persistent_kernel<false, 4>, cooperative_grid<false, 4>(ctx, want));
   } else {
-    const unsigned grid = cooperative_grid<false>(ctx, want);
-    ck(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(online_persistent_kernel<false>), dim3(grid),
-                                   dim3(kOThreads), args, 0, st),
-       "online_persistent_kernel");
+    launch(online_persistent_kernel<false, 1>, cooperative_grid<false, 1>(ctx, want));
   }
   launched("online_persistent_kernel");
   // MERGED leaves the final weights in the parity row after the last batch

@@ -348,7 +348,8 @@ def test_online_random_vs_oracle_bitexact(bsz):
 
 @pytest.mark.parametrize("C,D,n,bsz", [(2, 1000, 900, 300), (1, 333, 600, 64), (3, 1000, 700, 256), (8, 333, 600, 64),
                                        (26, 2048, 800, 100), (32, 777, 500, 128), (100, 4096, 600, 512),
-                                       (40, 64, 300, 1), (3, 70, 257, 256), (6, 10000, 2100, 1024)])
+                                       (40, 64, 300, 1), (3, 70, 257, 256), (6, 10000, 2100, 1024), (6, 2000, 300, 32),
+                                       (100, 1500, 400, 7)])
 def test_online_modes_vs_oracle_bitexact(C, D, n, bsz):
     """Every path of the persistent online trainer against the oracle:
     MERGED (C <= 2), LISTS with warp-per-row scoring (2 < C < 32) and with
@@ -364,6 +365,27 @@ def test_online_modes_vs_oracle_bitexact(C, D, n, bsz):
     np.testing.assert_array_equal(on.class_weight, oo.weight)
     np.testing.assert_array_equal(on.sample_counts, oo.counts)
     np.testing.assert_array_equal(on.class_vectors.words, oo.class_vectors)
+
+
+@pytest.mark.parametrize("C,D,n", [(32, 1000, 257), (33, 64, 100), (100, 4096, 300), (64, 10000, 70), (40, 31, 33)])
+def test_predict_many_classes_tiled_vs_oracle(C, D, n):
+    """The CTA-tiled Hamming scan (C >= 32): labels and fp64 distances
+    bit-exact vs the oracle, including ties between classes (duplicated class
+    vectors must resolve to the lowest class)."""
+    rng = np.random.default_rng(C + D + n)
+    W = (D + 31) // 32
+    cvb = rng.integers(0, 2, (C, D), dtype=np.uint8)
+    cvb[C // 2] = cvb[1]  # a duplicate class: ties must pick class 1
+    y = rng.integers(0, C, n).astype(np.int32)
+    enc = O.pack_rows(cvb[y] ^ (rng.random((n, D)) < 0.3).astype(np.uint8))
+    m = O.NaiveModel(C, D, O.generate_random(1, D, 3)).train_classical(enc, y)
+    model = hv.make_empty_model(hv.ModelConfig(class_count=C, dim=D, seed=3))
+    model.class_vectors.words[:] = O.pack_rows(cvb)
+    m.cv[:] = cvb
+    labels, dist = hv.predict_arrays(model, P(enc, D))
+    ol, od = m.predict(enc)
+    np.testing.assert_array_equal(labels, ol)
+    np.testing.assert_array_equal(dist, od)
 
 
 # --------------------------------------------------- device pipeline ----
