@@ -39,6 +39,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "hv_internal.cuh"
 #include "hv_scan.cuh"
@@ -84,7 +86,17 @@ struct OnlineParams {
   uint32_t* lidx;              // C x bsz (LISTS)
   double* lval;                // C x bsz (LISTS)
   uint32_t* llen;              // C (LISTS)
+  unsigned long long* prof;    // optional: ns spent per phase (score, lists, replay), CTA 0's view
+  uint32_t ksplit;             // tiled scoring: word range split into this many items per tile
+  uint32_t* pscr;              // bsz x C partial popcounts (ksplit > 1), zero between batches
+  uint32_t* arrive;            // per (row tile, class block) arrival counters (ksplit > 1)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ double delta_of(uint32_t popc, uint32_t D) {
   return static_cast<double>(popc) / static_cast<double>(D);  // model.cpp:69-79 (IEEE division)
@@ -123,16 +135,52 @@ __device__ void score_warp_per_row(const OnlineParams& p, unsigned long long* be
 // items; per-row argmin merged across class blocks with a 64-bit atomicMin.
 __device__ void score_tiled(const OnlineParams& p, unsigned long long* best_out, ScanSmem& s, uint64_t b0, uint32_t n,
                             uint32_t lane, uint32_t warp) {
+  __shared__ int s_last;
   const uint32_t ncb = (p.C + kScanCls - 1) / kScanCls;
   const uint64_t ntiles = (n + kScanRows - 1) / kScanRows;
-  for (uint64_t it = blockIdx.x; it < ntiles * ncb; it += gridDim.x) {
-    const uint32_t cb = static_cast<uint32_t>(it % ncb);
-    const uint64_t t0 = (it / ncb) * kScanRows;
+  const uint32_t ks = p.ksplit;
+  for (uint64_t it = blockIdx.x; it < ntiles * ncb * ks; it += gridDim.x) {
+    // a batch has few row tiles, so the word range is split across CTAs too;
+    // the last of a tile's ks items to arrive owns the argmin
+    const uint32_t kx = static_cast<uint32_t>(it % ks);
+    const uint64_t tc = it / ks;
+    const uint32_t cb = static_cast<uint32_t>(tc % ncb);
+    const uint64_t t0 = (tc / ncb) * kScanRows;
     const uint32_t nr = static_cast<uint32_t>(min(static_cast<uint64_t>(kScanRows), n - t0));
+    const uint32_t kbeg = static_cast<uint32_t>((static_cast<uint64_t>(p.W) * kx / ks) & ~3ull);
+    const uint32_t kend = kx + 1 == ks ? p.W : static_cast<uint32_t>((static_cast<uint64_t>(p.W) * (kx + 1) / ks) & ~3ull);
     uint32_t a[kScanRowsPerWarp];
-    scan_tile<kOThreads>(p.enc, b0 + t0, nr, p.W, p.cv, p.C, cb * kScanCls, s, a);
-    if (warp < kScanRows / kScanRowsPerWarp) {
-      const uint32_t c = cb * kScanCls + lane;
+    scan_tile<kOThreads>(p.enc, b0 + t0, nr, p.W, p.cv, p.C, cb * kScanCls, s, a, kbeg, kend);
+    const uint32_t c = cb * kScanCls + lane;
+    const bool compute = warp < kScanRows / kScanRowsPerWarp;
+    if (ks > 1) {
+      if (compute && c < p.C) {
+#pragma unroll
+        for (int k = 0; k < kScanRowsPerWarp; ++k) {
+          const uint32_t r = warp * kScanRowsPerWarp + k;
+          if (r < nr) atomicAdd(p.pscr + (t0 + r) * p.C + c, a[k]);
+        }
+      }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) s_last = atomicAdd(p.arrive + tc, 1u) == ks - 1;
+      __syncthreads();
+      if (!s_last) continue;  // uniform per CTA
+      __threadfence();
+      if (compute && c < p.C) {
+#pragma unroll
+        for (int k = 0; k < kScanRowsPerWarp; ++k) {
+          const uint32_t r = warp * kScanRowsPerWarp + k;
+          if (r < nr) {
+            uint32_t* slot = p.pscr + (t0 + r) * p.C + c;
+            a[k] = __ldcg(slot);
+            *slot = 0u;  // zero for the next batch
+          }
+        }
+      }
+      if (threadIdx.x == 0) p.arrive[tc] = 0u;
+    }
+    if (compute) {
 #pragma unroll
       for (int k = 0; k < kScanRowsPerWarp; ++k) {
         const uint32_t r = warp * kScanRowsPerWarp + k;
@@ -403,13 +451,13 @@ __device__ void replay_lists(const OnlineParams& p, Smem& s, uint64_t b0) {
   }
 }
 
-union OnlineSmem {
+union __align__(16) OnlineSmem {
   Smem replay;
   ScanSmem scan;  // used only between the batch-start and the next grid barrier
 };
 
 template <bool MERGED, int COLS>
-__global__ void __launch_bounds__(kOThreads, 3) online_persistent_kernel(OnlineParams p) {
+__global__ void __launch_bounds__(kOThreads, 2) online_persistent_kernel(OnlineParams p) {
   cg::grid_group grid = cg::this_grid();
   __shared__ OnlineSmem u;
   Smem& s = u.replay;
@@ -418,6 +466,8 @@ __global__ void __launch_bounds__(kOThreads, 3) online_persistent_kernel(OnlineP
   const uint64_t gwarp = static_cast<uint64_t>(blockIdx.x) * (kOThreads / 32) + warp;
   const bool lane_class = p.C >= kLaneClassMinC;
   uint32_t par = 0;
+  const bool prof = p.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long t0 = prof ? gtimer() : 0ull, t1 = 0, t2 = 0;
   for (uint64_t b0 = 0; b0 < p.rows; b0 += p.bsz, par ^= 1u) {
     const uint32_t n = static_cast<uint32_t>(min(p.bsz, p.rows - b0));
     // per-row argmin keys, double-buffered by batch parity: the atomicMin
@@ -429,11 +479,14 @@ __global__ void __launch_bounds__(kOThreads, 3) online_persistent_kernel(OnlineP
       score_warp_per_row(p, bestv, b0, n, gwarp, gwarps, lane);
     }
     grid.sync();
+    if (prof) t1 = gtimer();
+    t2 = t1;
     if constexpr (MERGED) {
       replay_merged<COLS>(p, bestv, s, b0, n, par);
     } else {
       build_lists(p, bestv, s, b0, n);
       grid.sync();
+      if (prof) t2 = gtimer();
       replay_lists<COLS>(p, s, b0);
     }
     if (lane_class) {
@@ -442,6 +495,13 @@ __global__ void __launch_bounds__(kOThreads, 3) online_persistent_kernel(OnlineP
       for (uint64_t r = gt; r < p.bsz; r += static_cast<uint64_t>(gridDim.x) * kOThreads) nxt[r] = ~0ull;
     }
     grid.sync();
+    if (prof) {
+      const unsigned long long t3 = gtimer();
+      p.prof[0] += t1 - t0;
+      p.prof[1] += t2 - t1;
+      p.prof[2] += t3 - t2;
+      t0 = t3;
+    }
   }
 }
 
@@ -482,25 +542,71 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   if (lane_class) ck(cudaMemsetAsync(best.ptr, 0xFF, 2 * n * sizeof(unsigned long long), st), "memset");
   // long per-class lists (few classes): one chain per thread; short ones: four
   const bool cols4 = !merged && n < 64 * C;
-  const uint64_t items = static_cast<uint64_t>(C) * ((W + (cols4 ? 32 : 8) - 1) / (cols4 ? 32 : 8));
+  const bool cols8 = cols4 && n < 16 * C;
+  const uint64_t iw = cols8 ? 64 : cols4 ? 32 : 8;  // words per replay item
+  const uint64_t items = static_cast<uint64_t>(C) * ((W + iw - 1) / iw);
   const uint64_t score_ctas = (n + kOThreads / 32 - 1) / (kOThreads / 32);
   const uint64_t want = std::max<uint64_t>(items, score_ctas);
   OnlineParams p{enc,     labels,   rows,     static_cast<uint32_t>(D), static_cast<uint32_t>(W),
                  static_cast<uint32_t>(C), n, gamma, tie, acc, wts.ptr, counts, cv, best.ptr, truep.ptr, lidx.ptr,
-                 lval.ptr, llen.ptr};
+                 lval.ptr, llen.ptr, nullptr, 1u, nullptr, nullptr};
+  // HVB200_ONLINE_PROFILE=1: print the time per phase (CTA 0's view, barrier waits included)
+  const char* pe = getenv("HVB200_ONLINE_PROFILE");
+  DevBuf<unsigned long long> prof(pe && pe[0] == '1' ? 3 : 0, st);
+  if (prof.ptr) {
+    prof.zero();
+    p.prof = prof.ptr;
+  }
   void* args[] = {&p};
+  // tiled scoring: split the words so every CTA has a score item
+  DevBuf<uint32_t> pscr, arrive;
+  unsigned grid_est = 0;
+  if (merged) {
+    grid_est = cooperative_grid<true, 1>(ctx, want);
+  } else if (cols8) {
+    grid_est = cooperative_grid<false, 8>(ctx, want);
+  } else if (cols4) {
+    grid_est = cooperative_grid<false, 4>(ctx, want);
+  } else {
+    grid_est = cooperative_grid<false, 1>(ctx, want);
+  }
+  if (lane_class) {
+    const uint64_t tiles = ((n + kScanRows - 1) / kScanRows) * ((C + kScanCls - 1) / kScanCls);
+    // ~3 items per CTA keeps the tail of the score phase short
+    const uint64_t ks = std::min<uint64_t>((3 * grid_est + tiles - 1) / tiles, std::max<size_t>(1, W / kScanK));
+    if (ks > 1) {
+      p.ksplit = static_cast<uint32_t>(ks);
+      pscr = DevBuf<uint32_t>(n * C, st);
+      arrive = DevBuf<uint32_t>(tiles, st);
+      pscr.zero();
+      arrive.zero();
+      p.pscr = pscr.ptr;
+      p.arrive = arrive.ptr;
+    }
+  }
   auto launch = [&](auto kern, unsigned grid) {
     ck(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kOThreads), args, 0, st),
        "online_persistent_kernel");
   };
   if (merged) {
     launch(online_persistent_kernel<true, 1>, cooperative_grid<true, 1>(ctx, want));
+  } else if (cols8) {
+    launch(online_persistent_kernel<false, 8>, cooperative_grid<false, 8>(ctx, want));
   } else if (cols4) {
     launch(online_persistent_kernel<false, 4>, cooperative_grid<false, 4>(ctx, want));
   } else {
     launch(online_persistent_kernel<false, 1>, cooperative_grid<false, 1>(ctx, want));
   }
   launched("online_persistent_kernel");
+  if (prof.ptr) {
+    unsigned long long h[3];
+    ck(cudaMemcpyAsync(h, prof.ptr, sizeof(h), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    const double nb = static_cast<double>((rows + n - 1) / n);
+    fprintf(stderr, "online phases (us/batch, %s, %d cols, ksplit %u): score %.2f lists %.2f replay %.2f\n",
+            merged ? "merged" : "lists", cols8 ? 8 : cols4 ? 4 : 1, p.ksplit, h[0] / nb / 1e3, h[1] / nb / 1e3,
+            h[2] / nb / 1e3);
+  }
   // MERGED leaves the final weights in the parity row after the last batch
   const size_t nb = (rows + n - 1) / n;
   const double* fin = merged ? wts.ptr + (nb & 1) * C : wts.ptr;

@@ -20,20 +20,22 @@ constexpr int kScanCls = 32;         // classes per tile (lane = class)
 constexpr int kScanK = 64;           // words per k-tile
 constexpr int kScanRowsPerWarp = 4;
 
-struct ScanSmem {
+struct __align__(16) ScanSmem {
   uint32_t q[2][kScanRows][kScanK];        // row words
   uint32_t c[2][kScanK][kScanCls + 1];     // class words, transposed, padded
 };
 
-// Popcounts of rows [row0, row0 + nrows) (row stride W, nrows <= 32) against
-// classes [c0, c0 + 32) of cv (C x W). On return, lane l of warp w (w < 8)
+// Popcounts over words [kbeg, kend) of rows [row0, row0 + nrows) (row stride
+// W, nrows <= 32) against classes [c0, c0 + 32) of cv (C x W). On return, lane l of warp w (w < 8)
 // holds in a[k] the popcount of row row0 + 4w + k against class c0 + l (junk
 // for rows/classes out of range). Every thread of the CTA must call it
 // (blockDim.x >= 256); it synchronises the CTA.
 template <int NT>
 __device__ __forceinline__ void scan_tile(const uint32_t* __restrict__ rows, uint64_t row0, uint32_t nrows,
                                           uint32_t W, const uint32_t* __restrict__ cv, uint32_t C, uint32_t c0,
-                                          ScanSmem& s, uint32_t (&a)[kScanRowsPerWarp]) {
+                                          ScanSmem& s, uint32_t (&a)[kScanRowsPerWarp], uint32_t kbeg = 0,
+                                          uint32_t kend = 0xFFFFFFFFu) {
+  if (kend > W) kend = W;
   constexpr int kQ = (kScanRows * kScanK + NT - 1) / NT;
   constexpr int kC = (kScanCls * kScanK + NT - 1) / NT;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -45,14 +47,14 @@ __device__ __forceinline__ void scan_tile(const uint32_t* __restrict__ rows, uin
     for (int i = 0; i < kQ; ++i) {
       const uint32_t e = tid + i * NT;
       const uint32_t r = e / kScanK, w = e % kScanK;
-      rq[i] = (e < kScanRows * kScanK && r < nrows && k0 + w < W) ? __ldg(rows + (row0 + r) * W + k0 + w) : 0u;
+      rq[i] = (e < kScanRows * kScanK && r < nrows && k0 + w < kend) ? __ldg(rows + (row0 + r) * W + k0 + w) : 0u;
     }
 #pragma unroll
     for (int i = 0; i < kC; ++i) {
       const uint32_t e = tid + i * NT;
       const uint32_t c = e / kScanK, w = e % kScanK;
-      rc[i] = (e < kScanCls * kScanK && c0 + c < C && k0 + w < W) ? cv[static_cast<uint64_t>(c0 + c) * W + k0 + w]
-                                                                  : 0u;
+      rc[i] = (e < kScanCls * kScanK && c0 + c < C && k0 + w < kend) ? cv[static_cast<uint64_t>(c0 + c) * W + k0 + w]
+                                                                     : 0u;
     }
   };
   auto store = [&](uint32_t b) {
@@ -67,12 +69,12 @@ __device__ __forceinline__ void scan_tile(const uint32_t* __restrict__ rows, uin
       if (e < kScanCls * kScanK) s.c[b][e % kScanK][e / kScanK] = rc[i];
     }
   };
-  load(0);
+  load(kbeg);
   store(0);
   __syncthreads();
   uint32_t b = 0;
-  for (uint32_t k0 = 0; k0 < W; k0 += kScanK, b ^= 1u) {
-    const bool more = k0 + kScanK < W;
+  for (uint32_t k0 = kbeg; k0 < kend; k0 += kScanK, b ^= 1u) {
+    const bool more = k0 + kScanK < kend;
     if (more) load(k0 + kScanK);
     if (warp < kScanRows / kScanRowsPerWarp) {
       const uint32_t r0 = warp * kScanRowsPerWarp;
