@@ -129,8 +129,14 @@ unsigned host_threads() {
     const int n = atoi(e);
     if (n >= 1) return static_cast<unsigned>(n);
   }
-  const unsigned hc = std::thread::hardware_concurrency();
-  return std::max(1u, std::min(hc ? hc : 1u, 64u));
+  unsigned hc = std::thread::hardware_concurrency();
+  hc = hc ? hc : 1u;
+  // one process per GPU (torchrun sets LOCAL_WORLD_SIZE): share the host cores
+  if (const char* lw = getenv("LOCAL_WORLD_SIZE")) {
+    const int n = atoi(lw);
+    if (n > 1) hc = std::max(1u, hc / static_cast<unsigned>(n));
+  }
+  return std::max(1u, std::min(hc, 64u));
 }
 
 }  // namespace
@@ -212,8 +218,11 @@ uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, si
   HostStager& hs = stager(ctx);
   hs.reserve(chunk * ldb);
   cudaStream_t streams[2] = {ctx->stream, ctx->aux};
-  for (size_t r0 = 0; r0 < rows; r0 += chunk, ++k) {
-    const size_t n = std::min(chunk, rows - r0);
+  // the first chunks of a call ramp up (1/8, 1/4, 1/2 of a slot) so the SMs
+  // start encoding after a short narrow + copy instead of a full slot's
+  size_t step = k == 0 ? std::max<size_t>(1, chunk / 8) : chunk;
+  for (size_t r0 = 0, n = 0; r0 < rows; r0 += n, ++k, step = std::min(chunk, 2 * step)) {
+    n = std::min(step, rows - r0);
     const int s = static_cast<int>(k % HostStager::kSlots);
     cudaStream_t st = streams[k & 1];
     ck(cudaEventSynchronize(hs.done[s]), "stage slot wait");  // its previous H2D has finished
