@@ -122,6 +122,16 @@ def run_ref_bench(rows, threads, reps=1, timeout=600):
     return json.loads(r.stdout.strip().splitlines()[-1])
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(target_s=10.0):
     """Reference CPU implementation on a bounded prefix sample, all host cores."""
     if not REF_BENCH.exists():
@@ -133,7 +143,7 @@ def cpu_baseline(target_s=10.0):
     return {"value": round(res["dp_per_s"], 3), "unit": "datapoints/s", "cores": threads, "kind": "reference",
             "sample": f"first {rows} rows of the workload (80/20 split), reference encode_batch/train_classical/"
                       f"predict with threads={threads}; {res['total_s']:.2f} s",
-            "stages_s": {k: res[k] for k in ("encode_s", "train_s", "predict_s")}}
+            "stages_s": {k: res[k] for k in ("encode_s", "train_s", "predict_s")}, "cpu_model": cpu_model()}
 
 
 def impl_reference(args):
@@ -164,6 +174,7 @@ def impl_reference(args):
             "config": {"workload": w["workload"], "features": w["features"], "classes": w["classes"], "dim": w["dim"],
                        "rows": rows, "full_rows": args.rows, "trainer": "classical"},
             "cpu_baseline": {"value": round(v, 3), "unit": "datapoints/s", "cores": threads, "kind": "reference",
+                             "cpu_model": cpu_model(),
                              "sample": f"first {rows} rows per step (of {args.rows}), threads={threads}"},
             "e2e": {"value": round(v, 3), "unit": "datapoints/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -516,8 +516,9 @@ unsigned cooperative_grid(hv_context* ctx, uint64_t want) {
   ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, online_persistent_kernel<MERGED, COLS>, kOThreads, 0),
      "occupancy");
   if (per_sm < 1) fail(HV_ERR_CUDA, "online_persistent_kernel does not fit on an SM");
-  return static_cast<unsigned>(std::max<uint64_t>(
-      1, std::min<uint64_t>(want, static_cast<uint64_t>(ctx->sm_count) * static_cast<uint64_t>(per_sm))));
+  uint64_t cap = static_cast<uint64_t>(ctx->sm_count) * static_cast<uint64_t>(per_sm);
+  if (const char* g = getenv("HVB200_ONLINE_GRID")) cap = std::min<uint64_t>(cap, std::max(1, atoi(g)));
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, cap)));
 }
 
 }  // namespace
