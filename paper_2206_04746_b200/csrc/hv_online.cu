@@ -12,7 +12,7 @@
 // score   (all warps)  per row: Hamming popcount against every class vector,
 //         argmin (strict <, lowest class on ties, model.cpp:96-104) packed as
 //         best = popc << 32 | class, plus the true class's popcount.
-//         C < 32: warp per row, lanes over words. C >= 32: CTA-tiled scan
+//         C < 16: warp per row, lanes over words. C >= 16: CTA-tiled scan
 //         (hv_scan.cuh: 32 rows x 32 classes per tile, lane = class, words
 //         through shared memory), per-row argmin merged across class blocks
 //         with a 64-bit atomicMin.
@@ -67,7 +67,7 @@ struct RTile {
   static constexpr int kChunk = kOTile / kWords;  // entries per chunk
 };
 constexpr uint32_t kMergedMaxC = 2;  // more classes: per-class lists skip the other classes' rows
-constexpr uint32_t kLaneClassMinC = 32;
+constexpr uint32_t kLaneClassMinC = 16;  // measured: tiled wins at C = 26 (25 -> 17 us), loses at C <= 10
 
 struct OnlineParams {
   const uint32_t* enc;
@@ -87,6 +87,7 @@ struct OnlineParams {
   double* lval;                // C x bsz (LISTS)
   uint32_t* llen;              // C (LISTS)
   unsigned long long* prof;    // optional: ns spent per phase (score, lists, replay), CTA 0's view
+  uint32_t tiled;              // score with the CTA-tiled scan (lane = class) instead of warp per row
   uint32_t ksplit;             // tiled scoring: word range split into this many items per tile
   uint32_t* pscr;              // bsz x C partial popcounts (ksplit > 1), zero between batches
   uint32_t* arrive;            // per (row tile, class block) arrival counters (ksplit > 1)
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(kOThreads, 2) online_persistent_kernel(OnlineP
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint64_t gwarps = static_cast<uint64_t>(gridDim.x) * (kOThreads / 32);
   const uint64_t gwarp = static_cast<uint64_t>(blockIdx.x) * (kOThreads / 32) + warp;
-  const bool lane_class = p.C >= kLaneClassMinC;
+  const bool lane_class = p.tiled != 0;
   uint32_t par = 0;
   const bool prof = p.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   unsigned long long t0 = prof ? gtimer() : 0ull, t1 = 0, t2 = 0;
@@ -534,7 +535,9 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   // MERGED also for tiny batches: streaming a few rows per item is cheaper
   // than the extra grid barrier of the list phase
   const bool merged = C <= kMergedMaxC || n <= 32;
-  const bool lane_class = C >= kLaneClassMinC;
+  uint32_t min_c = kLaneClassMinC;
+  if (const char* e = getenv("HVB200_ONLINE_TILED_MIN_C")) min_c = static_cast<uint32_t>(atoi(e));
+  const bool lane_class = C >= min_c;
   DevBuf<double> wts(2 * C, st), lval(merged ? 0 : C * n, st);
   DevBuf<unsigned long long> best(2 * n, st);
   DevBuf<uint32_t> truep(n, st), lidx(merged ? 0 : C * n, st), llen(merged ? 0 : C, st);
@@ -550,7 +553,7 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   const uint64_t want = std::max<uint64_t>(items, score_ctas);
   OnlineParams p{enc,     labels,   rows,     static_cast<uint32_t>(D), static_cast<uint32_t>(W),
                  static_cast<uint32_t>(C), n, gamma, tie, acc, wts.ptr, counts, cv, best.ptr, truep.ptr, lidx.ptr,
-                 lval.ptr, llen.ptr, nullptr, 1u, nullptr, nullptr};
+                 lval.ptr, llen.ptr, nullptr, lane_class ? 1u : 0u, 1u, nullptr, nullptr};
   // HVB200_ONLINE_PROFILE=1: print the time per phase (CTA 0's view, barrier waits included)
   const char* pe = getenv("HVB200_ONLINE_PROFILE");
   DevBuf<unsigned long long> prof(pe && pe[0] == '1' ? 3 : 0, st);
