@@ -367,7 +367,8 @@ def test_online_modes_vs_oracle_bitexact(C, D, n, bsz):
     np.testing.assert_array_equal(on.class_vectors.words, oo.class_vectors)
 
 
-@pytest.mark.parametrize("C,D,n", [(32, 1000, 257), (33, 64, 100), (100, 4096, 300), (64, 10000, 70), (40, 31, 33)])
+@pytest.mark.parametrize("C,D,n", [(32, 1000, 257), (33, 64, 100), (100, 4096, 300), (64, 10000, 70), (40, 31, 33),
+                                   (129, 500, 40), (200, 96, 77)])
 def test_predict_many_classes_tiled_vs_oracle(C, D, n):
     """The CTA-tiled Hamming scan (C >= 32): labels and fp64 distances
     bit-exact vs the oracle, including ties between classes (duplicated class
