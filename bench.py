@@ -190,9 +190,18 @@ def impl_engine(args):
     from paper_2206_04746_b200 import device as dv
 
     rank, world, local = dist_env()
+    # HVB200_BENCH_SHARE_GPU=1 (testing only): several ranks share the visible
+    # GPUs round-robin and reduce over gloo, so the multi-rank path can be
+    # exercised on a one-GPU box; production runs one rank per GPU over NCCL
+    share = os.environ.get("HVB200_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     # one non-default stream for everything (library kernels, torch ops, NCCL)
     torch.cuda.set_stream(torch.cuda.Stream(local))
     w = WORKLOAD
