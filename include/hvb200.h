@@ -269,6 +269,28 @@ hv_status hv_dev_online_slice_update(hv_context* ctx, const uint32_t* popc, size
                                      const uint32_t* batch, size_t rows, const int32_t* labels,
                                      double gamma, const uint32_t* tiebreak, double* acc,
                                      double* weight, uint64_t* counts, uint32_t* class_vectors);
+/* ---- classical training fused with its all-reduce over peer memory -------
+ * (replaces hv_dev_class_counts + an NCCL all-reduce.) Each
+ * rank shares a device buffer with its peers through CUDA IPC: */
+size_t hv_shared_handle_size(void);  /* bytes of an IPC handle (64) */
+hv_status hv_shared_alloc(hv_context* ctx, size_t bytes, void** dev_ptr, uint8_t* handle);
+hv_status hv_shared_open(hv_context* ctx, const uint8_t* handle, void** dev_ptr);
+hv_status hv_shared_close(hv_context* ctx, void* dev_ptr);
+hv_status hv_shared_free(hv_context* ctx, void* dev_ptr);
+/* Count this rank's rows (like hv_dev_class_counts) and add the exact counts
+ * and class row counts into EVERY rank's buffers: peer_counts / peer_class_rows
+ * are DEVICE arrays of `world` device pointers (C x 32W uint32, C uint64). */
+hv_status hv_dev_class_counts_peers(hv_context* ctx, const uint32_t* encoded, size_t rows, size_t dim,
+                                    const int32_t* labels, size_t class_count,
+                                    uint32_t* const* peer_counts, uint64_t* const* peer_class_rows,
+                                    size_t world);
+/* After the counts: store `epoch` into flag[rank] of every rank (peer_flags:
+ * device array of `world` pointers to each rank's `world` uint32 flags) ... */
+hv_status hv_dev_signal_peers(hv_context* ctx, uint32_t* const* peer_flags, size_t world, size_t rank,
+                              uint32_t epoch);
+/* ... and wait (on the stream) until this rank's flags all reach `epoch`;
+ * a peer missing for 20 s latches an error reported by hv_dev_check. */
+hv_status hv_dev_wait_peers(hv_context* ctx, const uint32_t* flags, size_t world, uint32_t epoch);
 /* Synthetic workload (include/hvb200_synth.h) generated on device for rows
  * [row0, row0+rows): bins8 (pitch ldb) and labels. */
 hv_status hv_dev_synth(hv_context* ctx, uint64_t row0, size_t rows, size_t features,

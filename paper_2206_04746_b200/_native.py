@@ -114,6 +114,14 @@ SIGNATURES = {
     "hv_dev_online_slice_init": (ST, [vp, vp, sz, vp, sz, sz, sz, sz, vp, vp, vp, vp, vp]),
     "hv_dev_online_partial_popc": (ST, [vp, vp, sz, sz, vp, sz, vp]),
     "hv_dev_online_slice_update": (ST, [vp, vp, sz, sz, sz, sz, vp, sz, vp, dbl, vp, vp, vp, vp, vp]),
+    "hv_shared_handle_size": (sz, []),
+    "hv_shared_alloc": (ST, [vp, sz, C.POINTER(vp), vp]),
+    "hv_shared_open": (ST, [vp, vp, C.POINTER(vp)]),
+    "hv_shared_close": (ST, [vp, vp]),
+    "hv_shared_free": (ST, [vp, vp]),
+    "hv_dev_class_counts_peers": (ST, [vp, vp, sz, sz, vp, sz, vp, vp, sz]),
+    "hv_dev_signal_peers": (ST, [vp, vp, sz, sz, u32]),
+    "hv_dev_wait_peers": (ST, [vp, vp, sz, u32]),
     "hv_fold_encode_train": (ST, [vp, vp, sz, vp, vp, sz, sz, vp, vp, sz, sz, vp, sz, C.POINTER(vp)]),
     "hv_fold_counts": (ST, [vp, C.POINTER(vp), C.POINTER(vp)]),
     "hv_fold_predict": (ST, [vp, vp, vp, vp]),

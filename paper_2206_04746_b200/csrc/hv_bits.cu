@@ -132,8 +132,8 @@ template <class CT>
 __global__ void __launch_bounds__(128) column_count_kernel(const uint32_t* __restrict__ m, uint32_t W,
                                                            const uint32_t* __restrict__ perm,
                                                            const uint64_t* __restrict__ seg_off, uint32_t nseg,
-                                                           uint64_t npos_fallback, uint32_t chunk,
-                                                           CT* __restrict__ counts) {
+                                                           uint64_t npos_fallback, uint32_t chunk, CT* single,
+                                                           CT* const* __restrict__ dsts, uint32_t ndst) {
   const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = w < W;
   const uint64_t npos = seg_off ? seg_off[nseg] : npos_fallback;
@@ -176,11 +176,20 @@ __global__ void __launch_bounds__(128) column_count_kernel(const uint32_t* __res
         h.add16(x + 16);
       }
       if (active) {
-        CT* dst = counts + s * stride + 32ull * w;
+        // flush into every destination: the local counts, or — fused with the
+        // all-reduce — the count buffers of all ranks over peer memory
+        for (uint32_t d = 0; d < ndst; ++d) {
+          CT* dst = (dsts ? dsts[d] : single) + s * stride + 32ull * w;
 #pragma unroll 4
-        for (int t = 0; t < 32; ++t) {
-          const uint32_t c = h.count_of(t);
-          if (c) atomicAdd(dst + t, static_cast<CT>(c));
+          for (int t = 0; t < 32; ++t) {
+            const uint32_t c = h.count_of(t);
+            if (c == 0) continue;
+            if (ndst == 1) {
+              atomicAdd(dst + t, static_cast<CT>(c));
+            } else {
+              atomicAdd_system(dst + t, static_cast<CT>(c));  // peer memory: system scope
+            }
+          }
         }
       }
     }
@@ -191,11 +200,18 @@ __global__ void __launch_bounds__(128) column_count_kernel(const uint32_t* __res
 
 void launch_column_count_u32(cudaStream_t st, const uint32_t* m, uint32_t W, const uint32_t* perm,
                              const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, uint32_t* counts) {
+  launch_column_count_peers(st, m, W, perm, seg_off, nseg, max_pos, counts, nullptr, 1);
+}
+
+void launch_column_count_peers(cudaStream_t st, const uint32_t* m, uint32_t W, const uint32_t* perm,
+                               const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, uint32_t* single,
+                               uint32_t* const* dsts_dev, uint32_t ndst) {
   if (max_pos == 0 || W == 0) return;
   if (max_pos > 0xFFFFFFFFull) invalid("class counts: more than 2^32 rows per call");
   const uint32_t chunk = 2048;
   dim3 grid(grid_for(W, 128), static_cast<unsigned>((max_pos + chunk - 1) / chunk));
-  column_count_kernel<uint32_t><<<grid, 128, 0, st>>>(m, W, perm, seg_off, nseg, max_pos, chunk, counts);
+  column_count_kernel<uint32_t><<<grid, 128, 0, st>>>(m, W, perm, seg_off, nseg, max_pos, chunk, single, dsts_dev,
+                                                      dsts_dev ? ndst : 1u);
   launched("column_count_kernel");
 }
 
@@ -352,8 +368,9 @@ hv_status hv_vertical_sum(hv_context* ctx, const uint32_t* m, size_t rows, size_
     d_cnt.zero();
     const uint32_t chunk = 2048;
     dim3 grid(grid_for(W, 128), static_cast<unsigned>((rows + chunk - 1) / chunk));
+    if (rows > 0xFFFFFFFFull) invalid("vertical_sum: more than 2^32 rows");
     column_count_kernel<unsigned long long><<<grid, 128, 0, ctx->stream>>>(d_in.ptr, W, nullptr, nullptr, 1, rows,
-                                                                          chunk, d_cnt.ptr);
+                                                                          chunk, d_cnt.ptr, nullptr, 1);
     launched("column_count_kernel");
     widen_u64_kernel<<<grid_for(dim, 256), 256, 0, ctx->stream>>>(d_cnt.ptr, dim, d_out.ptr);
     launched("widen_u64_kernel");

@@ -148,6 +148,16 @@ inline unsigned grid_for(size_t n, unsigned block, unsigned cap = 1u << 30) {
 // Column counts over a permuted, class-segmented row sequence (hv_bits.cu).
 void launch_column_count_u32(cudaStream_t st, const uint32_t* m, uint32_t W, const uint32_t* perm,
                              const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, uint32_t* counts);
+// Label bucketing for class counts (hv_model.cu): histogram (validated, into
+// a zeroed hist), segment offsets, class-sorted permutation; class_rows += hist.
+void label_bucket_device(hv_context* ctx, cudaStream_t st, const int32_t* labels, size_t rows, size_t C,
+                         uint32_t* hist, uint64_t* offsets, uint32_t* cursor, uint32_t* perm,
+                         uint64_t* class_rows = nullptr);
+// Same, flushing into `single`, or (dsts_dev != nullptr) into the ndst count
+// buffers listed in the device array dsts_dev (every rank's, over peer memory).
+void launch_column_count_peers(cudaStream_t st, const uint32_t* m, uint32_t W, const uint32_t* perm,
+                               const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, uint32_t* single,
+                               uint32_t* const* dsts_dev, uint32_t ndst);
 
 // Encoder entry points shared with the fold pipeline (hv_encode.cu). Words
 // [w0, w0 + wcount) of every row are written to out[row * ldo + k]; wcount = 0

@@ -575,6 +575,19 @@ unsigned sgrid(hv_context* ctx, uint64_t items, unsigned block, unsigned per_sm 
   return static_cast<unsigned>(want == 0 ? 1 : std::min(want, cap));
 }
 
+// labels -> per-class histogram (validated), segment offsets and the
+// class-sorted row permutation; class_rows (nullable) += histogram
+void label_bucket_device(hv_context* ctx, cudaStream_t st, const int32_t* labels, size_t rows, size_t C,
+                         uint32_t* hist, uint64_t* offsets, uint32_t* cursor, uint32_t* perm, uint64_t* class_rows) {
+  label_hist_kernel<<<sgrid(ctx, rows, 256), 256, 0, st>>>(labels, rows, static_cast<uint32_t>(C), hist, ctx->d_err);
+  launched("label_hist_kernel");
+  label_scan_kernel<<<1, 32, 0, st>>>(hist, static_cast<uint32_t>(C), offsets, class_rows, cursor);
+  launched("label_scan_kernel");
+  label_scatter_kernel<<<sgrid(ctx, rows, 256), 256, 0, st>>>(labels, rows, static_cast<uint32_t>(C), offsets, cursor,
+                                                             perm);
+  launched("label_scatter_kernel");
+}
+
 // class counts of `rows` encoded rows into counts (C x 32W, added) and class_rows (added)
 void class_counts_device(hv_context* ctx, cudaStream_t st, const uint32_t* enc, size_t rows, size_t W,
                          const int32_t* labels, size_t C, uint32_t* counts, uint64_t* class_rows) {
@@ -582,13 +595,7 @@ void class_counts_device(hv_context* ctx, cudaStream_t st, const uint32_t* enc, 
   DevBuf<uint32_t> hist(C, st), cursor(C, st), perm(rows, st);
   DevBuf<uint64_t> offsets(C + 1, st);
   hist.zero();
-  label_hist_kernel<<<sgrid(ctx, rows, 256), 256, 0, st>>>(labels, rows, static_cast<uint32_t>(C), hist.ptr, ctx->d_err);
-  launched("label_hist_kernel");
-  label_scan_kernel<<<1, 32, 0, st>>>(hist.ptr, static_cast<uint32_t>(C), offsets.ptr, class_rows, cursor.ptr);
-  launched("label_scan_kernel");
-  label_scatter_kernel<<<sgrid(ctx, rows, 256), 256, 0, st>>>(labels, rows, static_cast<uint32_t>(C), offsets.ptr,
-                                                             cursor.ptr, perm.ptr);
-  launched("label_scatter_kernel");
+  label_bucket_device(ctx, st, labels, rows, C, hist.ptr, offsets.ptr, cursor.ptr, perm.ptr, class_rows);
   launch_column_count_u32(st, enc, static_cast<uint32_t>(W), perm.ptr, offsets.ptr, static_cast<uint32_t>(C), rows,
                           counts);
 }

@@ -242,6 +242,119 @@ class Engine:
         return acc, weight, cnt, cv
 
 
+class PeerCounts:
+    """Classical class counts fused with their all-reduce over peer memory.
+
+    Each rank shares one device buffer with its peers (CUDA IPC): class counts
+    and class row counts double-buffered by epoch parity, plus `world` arrival
+    flags. `reduce` counts this rank's rows straight into every rank's buffer
+    (system-scope atomics over NVLink P2P), signals every peer, and waits for
+    all of them; afterwards each rank holds the exact global counts with no
+    separate collective (csrc/hv_peer.cu). `release` zeroes the parity buffer
+    once the caller has binarised it.
+
+    `buffers`/`peer_ptrs` let a single process emulate several ranks (tests);
+    normally they come from hv_shared_alloc + an all_gather of IPC handles.
+    """
+
+    def __init__(self, engine: "Engine", rank: int, world: int, group=None, local_ranks=None):
+        import ctypes as _C
+        import torch.distributed as dist
+
+        e = engine
+        self.e, self.rank, self.world = e, rank, world
+        self.nc = e.C * 32 * e.W
+        self.n_rows = e.C
+        # layout (bytes): counts[2][nc] u32 | rows[2][C] u64 | flags[world] u32
+        self.off_rows = (2 * self.nc * 4 + 7) // 8 * 8
+        self.off_flags = self.off_rows + 2 * e.C * 8
+        self.bytes = self.off_flags + 4 * world
+        L = N.lib()
+        hs = L.hv_shared_handle_size()
+        self._owned = []
+        self._opened = []
+        if local_ranks is not None:  # single-process emulation: plain buffers, no IPC
+            bases = local_ranks
+        else:
+            base = _C.c_void_p()
+            handle = (_C.c_uint8 * hs)()
+            N.check(L.hv_shared_alloc(e.dc.h, self.bytes, _C.byref(base), handle))
+            self._owned.append(base.value)
+            handles = [None] * world
+            dist.all_gather_object(handles, bytes(handle), group=group)
+            bases = []
+            for q in range(world):
+                if q == rank:
+                    bases.append(base.value)
+                    continue
+                ptr = _C.c_void_p()
+                hq = (_C.c_uint8 * hs).from_buffer_copy(handles[q])
+                N.check(L.hv_shared_open(e.dc.h, hq, _C.byref(ptr)))
+                self._opened.append(ptr.value)
+                bases.append(ptr.value)
+        self.bases = bases
+        dev = e.dev
+        self.counts_ptrs = [torch.tensor([b + par * self.nc * 4 for b in bases], dtype=torch.int64, device=dev)
+                            for par in (0, 1)]
+        self.rows_ptrs = [torch.tensor([b + self.off_rows + par * e.C * 8 for b in bases], dtype=torch.int64,
+                                       device=dev) for par in (0, 1)]
+        self.flags_ptrs = torch.tensor([b + self.off_flags for b in bases], dtype=torch.int64, device=dev)
+        self.epoch = 0
+        if local_ranks is None and world > 1:
+            torch.cuda.synchronize(dev)
+            dist.barrier(group=group)  # every buffer is zeroed and open before anyone adds into it
+
+    def own(self, par: int):
+        """This rank's counts (C x 32W int32 view) and class rows (C int64 view) of parity `par`."""
+        base = self.bases[self.rank]
+        counts = _wrap(base + par * self.nc * 4, (self.e.C, 32 * self.e.W), torch.int32, self.e.dev)
+        rows = _wrap(base + self.off_rows + par * self.e.C * 8, (self.e.C,), torch.int64, self.e.dev)
+        return counts, rows
+
+    def count(self, enc: torch.Tensor, labels: torch.Tensor) -> int:
+        """Add this rank's counts into every rank's buffer and signal; returns the epoch."""
+        self.epoch += 1
+        par = self.epoch & 1
+        L = N.lib()
+        N.check(L.hv_dev_class_counts_peers(self.e.dc.h, _ptr(enc), enc.shape[0], self.e.D, _ptr(labels), self.e.C,
+                                            _ptr(self.counts_ptrs[par]), _ptr(self.rows_ptrs[par]), self.world))
+        N.check(L.hv_dev_signal_peers(self.e.dc.h, _ptr(self.flags_ptrs), self.world, self.rank, self.epoch))
+        return self.epoch
+
+    def wait(self, epoch: int):
+        N.check(N.lib().hv_dev_wait_peers(self.e.dc.h, C.c_void_p(self.bases[self.rank] + self.off_flags), self.world,
+                                          epoch))
+        return self.own(epoch & 1)
+
+    def reduce(self, enc: torch.Tensor, labels: torch.Tensor):
+        """count + wait: the global (counts, class rows) of this epoch."""
+        return self.wait(self.count(enc, labels))
+
+    def release(self, epoch: int):
+        counts, rows = self.own(epoch & 1)
+        counts.zero_()
+        rows.zero_()
+
+    def close(self):
+        L = N.lib()
+        for p in self._opened:
+            L.hv_shared_close(self.e.dc.h, C.c_void_p(p))
+        for p in self._owned:
+            L.hv_shared_free(self.e.dc.h, C.c_void_p(p))
+        self._opened, self._owned = [], []
+
+
+def _wrap(ptr: int, shape, dtype, device):
+    """A torch view of raw device memory (no ownership)."""
+    class _CAI:
+        def __init__(self):
+            typestr = {torch.int32: "<i4", torch.int64: "<i8", torch.float64: "<f8"}[dtype]
+            self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                             "version": 3, "strides": None, "stream": None}
+
+    return torch.as_tensor(_CAI(), device=device)
+
+
 class DSlicedOnline:
     """Exact multi-GPU online training by output-word slices.
 

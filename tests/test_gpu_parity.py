@@ -504,3 +504,36 @@ def test_encode_words_slices_and_generic_fallback():
         full = eng.encode(bins8)
         for w0, nw in [(0, 63), (5, 1), (17, 46), (62, 1)]:
             assert torch.equal(eng.encode_words(bins8, w0, nw), full[:, w0:w0 + nw]), (binding, w0, nw)
+
+
+def test_peer_counts_emulated_ranks_equal_allreduce():
+    """Classical counts fused with their all-reduce over peer memory
+    (device.PeerCounts, csrc/hv_peer.cu) with 3 ranks emulated in one process:
+    every rank's buffer ends with exactly the global counts, over several
+    epochs (parity reuse after release)."""
+    from paper_2206_04746_b200 import device as dv
+    F, B, D, C, rows, world = 342, 16, 1000, 3, 5000, 3
+    cbk = dv.DeviceCodebook.make(F, B, D, seed=2)
+    eng = dv.Engine(cbk, C)
+    bufs = []
+    for _ in range(world):
+        nc = C * 32 * eng.W
+        off_rows = (2 * nc * 4 + 7) // 8 * 8
+        bufs.append(torch.zeros(off_rows + 2 * C * 8 + 4 * world, dtype=torch.uint8, device="cuda"))
+    bases = [b.data_ptr() for b in bufs]
+    pcs = [dv.PeerCounts(eng, r, world, local_ranks=bases) for r in range(world)]
+    for epoch_seed in (7, 8, 9):
+        bins8, labels = eng.synth(0, rows, 0, epoch_seed)
+        enc = eng.encode(bins8)
+        want_c, want_r = eng.zero_counts()
+        eng.class_counts(enc, labels, want_c, want_r)
+        spans = [dv.shard_range(rows, r, world) for r in range(world)]
+        eps = [pcs[r].count(enc[lo:hi], labels[lo:hi]) for r, (lo, hi) in enumerate(spans)]
+        for r in range(world):
+            got_c, got_r = pcs[r].wait(eps[r])
+            eng.dc.check()
+            torch.cuda.synchronize()
+            assert torch.equal(got_c, want_c), (epoch_seed, r)
+            assert torch.equal(got_r, want_r), (epoch_seed, r)
+        for r in range(world):
+            pcs[r].release(eps[r])
