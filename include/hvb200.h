@@ -264,6 +264,13 @@ hv_status hv_dev_online_slice_init(hv_context* ctx, const uint32_t* batch0, size
 hv_status hv_dev_online_partial_popc(hv_context* ctx, const uint32_t* class_vectors,
                                      size_t class_count, size_t words, const uint32_t* batch,
                                      size_t rows, uint32_t* popc);
+/* hv_dev_online_partial_popc fused with the popcount all-reduce over peer
+ * memory: ADDS this rank's partials into every rank's rows x C buffer
+ * (peer_popc: device array of `world` device pointers, zeroed beforehand);
+ * follow with hv_dev_signal_peers / hv_dev_wait_peers as for the counts. */
+hv_status hv_dev_online_partial_popc_peers(hv_context* ctx, const uint32_t* class_vectors,
+                                           size_t class_count, size_t words, const uint32_t* batch,
+                                           size_t rows, uint32_t* const* peer_popc, size_t world);
 hv_status hv_dev_online_slice_update(hv_context* ctx, const uint32_t* popc, size_t class_count,
                                      size_t dim, size_t word_begin, size_t words,
                                      const uint32_t* batch, size_t rows, const int32_t* labels,

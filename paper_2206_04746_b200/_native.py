@@ -113,6 +113,7 @@ SIGNATURES = {
     "hv_dev_encode_words": (ST, [vp, vp, sz, sz, sz, vp, vp, sz, sz, ci, vp, sz, sz, vp, sz]),
     "hv_dev_online_slice_init": (ST, [vp, vp, sz, vp, sz, sz, sz, sz, vp, vp, vp, vp, vp]),
     "hv_dev_online_partial_popc": (ST, [vp, vp, sz, sz, vp, sz, vp]),
+    "hv_dev_online_partial_popc_peers": (ST, [vp, vp, sz, sz, vp, sz, vp, sz]),
     "hv_dev_online_slice_update": (ST, [vp, vp, sz, sz, sz, sz, vp, sz, vp, dbl, vp, vp, vp, vp, vp]),
     "hv_shared_handle_size": (sz, []),
     "hv_shared_alloc": (ST, [vp, sz, C.POINTER(vp), vp]),

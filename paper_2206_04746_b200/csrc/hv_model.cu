@@ -395,7 +395,7 @@ __global__ void online_score_hamming_kernel(const uint32_t* __restrict__ cv, uin
 // (warp per row), summed across ranks by the caller's all-reduce.
 __global__ void online_partial_popc_kernel(const uint32_t* __restrict__ cv, uint32_t C, uint32_t Ws,
                                            const uint32_t* __restrict__ batch, uint64_t rows,
-                                           uint32_t* __restrict__ popc) {
+                                           uint32_t* __restrict__ popc, uint32_t* const* peers, uint32_t npeers) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += stride) {
@@ -404,7 +404,13 @@ __global__ void online_partial_popc_kernel(const uint32_t* __restrict__ cv, uint
       uint32_t a = 0;
       for (uint32_t w = lane; w < Ws; w += 32u) a += __popc(q[w] ^ cv[static_cast<uint64_t>(c) * Ws + w]);
       a = __reduce_add_sync(FULL, a);
-      if (lane == 0) popc[r * C + c] = a;
+      if (lane == 0) {
+        if (peers) {  // fused with the reduction: add into every rank's buffer over peer memory
+          for (uint32_t q = 0; q < npeers; ++q) atomicAdd_system(peers[q] + r * C + c, a);
+        } else {
+          popc[r * C + c] = a;
+        }
+      }
     }
   }
 }
@@ -1086,7 +1092,22 @@ hv_status hv_dev_online_partial_popc(hv_context* ctx, const uint32_t* class_vect
     require(ctx);
     if (rows == 0 || class_count == 0) return;
     online_partial_popc_kernel<<<sgrid(ctx, rows * 32, 256, 8), 256, 0, ctx->stream>>>(
-        class_vectors, static_cast<uint32_t>(class_count), static_cast<uint32_t>(words), batch, rows, popc);
+        class_vectors, static_cast<uint32_t>(class_count), static_cast<uint32_t>(words), batch, rows, popc, nullptr,
+        0u);
+    launched("online_partial_popc_kernel");
+  });
+}
+
+hv_status hv_dev_online_partial_popc_peers(hv_context* ctx, const uint32_t* class_vectors, size_t class_count,
+                                           size_t words, const uint32_t* batch, size_t rows,
+                                           uint32_t* const* peer_popc, size_t world) {
+  return guarded([&] {
+    require(ctx);
+    if (world == 0 || world > 64) invalid("online_partial_popc_peers: world must be 1..64");
+    if (rows == 0 || class_count == 0) return;
+    online_partial_popc_kernel<<<sgrid(ctx, rows * 32, 256, 8), 256, 0, ctx->stream>>>(
+        class_vectors, static_cast<uint32_t>(class_count), static_cast<uint32_t>(words), batch, rows, nullptr,
+        peer_popc, static_cast<uint32_t>(world));
     launched("online_partial_popc_kernel");
   });
 }

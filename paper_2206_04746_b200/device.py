@@ -242,43 +242,34 @@ class Engine:
         return acc, weight, cnt, cv
 
 
-class PeerCounts:
-    """Classical class counts fused with their all-reduce over peer memory.
+class PeerShared:
+    """One device buffer per rank shared with every peer through CUDA IPC:
+    two payload slots (epoch parity) and `world` uint32 arrival flags. Ranks
+    add their contributions straight into every rank's slot of the current
+    parity (system-scope atomics over NVLink P2P), release-store the epoch into
+    every peer's flag, and acquire-wait for all flags (csrc/hv_peer.cu).
 
-    Each rank shares one device buffer with its peers (CUDA IPC): class counts
-    and class row counts double-buffered by epoch parity, plus `world` arrival
-    flags. `reduce` counts this rank's rows straight into every rank's buffer
-    (system-scope atomics over NVLink P2P), signals every peer, and waits for
-    all of them; afterwards each rank holds the exact global counts with no
-    separate collective (csrc/hv_peer.cu). `release` zeroes the parity buffer
-    once the caller has binarised it.
-
-    `buffers`/`peer_ptrs` let a single process emulate several ranks (tests);
-    normally they come from hv_shared_alloc + an all_gather of IPC handles.
+    `local_ranks` (tests): base pointers of zeroed buffers of `nbytes` for
+    ranks emulated in one process; normally buffers come from hv_shared_alloc
+    plus an all_gather of the IPC handles.
     """
 
-    def __init__(self, engine: "Engine", rank: int, world: int, group=None, local_ranks=None):
+    def __init__(self, engine: "Engine", rank: int, world: int, payload_bytes: int, group=None, local_ranks=None):
         import ctypes as _C
         import torch.distributed as dist
 
-        e = engine
-        self.e, self.rank, self.world = e, rank, world
-        self.nc = e.C * 32 * e.W
-        self.n_rows = e.C
-        # layout (bytes): counts[2][nc] u32 | rows[2][C] u64 | flags[world] u32
-        self.off_rows = (2 * self.nc * 4 + 7) // 8 * 8
-        self.off_flags = self.off_rows + 2 * e.C * 8
-        self.bytes = self.off_flags + 4 * world
+        self.e, self.rank, self.world = engine, rank, world
+        self.slot = self.slot_bytes(payload_bytes)
+        self.off_flags = 2 * self.slot
         L = N.lib()
-        hs = L.hv_shared_handle_size()
-        self._owned = []
-        self._opened = []
-        if local_ranks is not None:  # single-process emulation: plain buffers, no IPC
-            bases = local_ranks
+        self._owned, self._opened = [], []
+        if local_ranks is not None:
+            bases = list(local_ranks)
         else:
+            hs = L.hv_shared_handle_size()
             base = _C.c_void_p()
             handle = (_C.c_uint8 * hs)()
-            N.check(L.hv_shared_alloc(e.dc.h, self.bytes, _C.byref(base), handle))
+            N.check(L.hv_shared_alloc(engine.dc.h, self.nbytes(payload_bytes, world), _C.byref(base), handle))
             self._owned.append(base.value)
             handles = [None] * world
             dist.all_gather_object(handles, bytes(handle), group=group)
@@ -288,67 +279,135 @@ class PeerCounts:
                     bases.append(base.value)
                     continue
                 ptr = _C.c_void_p()
-                hq = (_C.c_uint8 * hs).from_buffer_copy(handles[q])
-                N.check(L.hv_shared_open(e.dc.h, hq, _C.byref(ptr)))
+                N.check(L.hv_shared_open(engine.dc.h, (_C.c_uint8 * hs).from_buffer_copy(handles[q]), _C.byref(ptr)))
                 self._opened.append(ptr.value)
                 bases.append(ptr.value)
         self.bases = bases
-        dev = e.dev
-        self.counts_ptrs = [torch.tensor([b + par * self.nc * 4 for b in bases], dtype=torch.int64, device=dev)
-                            for par in (0, 1)]
-        self.rows_ptrs = [torch.tensor([b + self.off_rows + par * e.C * 8 for b in bases], dtype=torch.int64,
-                                       device=dev) for par in (0, 1)]
-        self.flags_ptrs = torch.tensor([b + self.off_flags for b in bases], dtype=torch.int64, device=dev)
-        self.epoch = 0
+        dev = engine.dev
+        self.flags_ptrs = torch.tensor([b_ + self.off_flags for b_ in bases], dtype=torch.int64, device=dev)
+        self._ptrs = {}
         if local_ranks is None and world > 1:
             torch.cuda.synchronize(dev)
             dist.barrier(group=group)  # every buffer is zeroed and open before anyone adds into it
 
-    def own(self, par: int):
-        """This rank's counts (C x 32W int32 view) and class rows (C int64 view) of parity `par`."""
-        base = self.bases[self.rank]
-        counts = _wrap(base + par * self.nc * 4, (self.e.C, 32 * self.e.W), torch.int32, self.e.dev)
-        rows = _wrap(base + self.off_rows + par * self.e.C * 8, (self.e.C,), torch.int64, self.e.dev)
-        return counts, rows
+    @staticmethod
+    def slot_bytes(payload_bytes: int) -> int:
+        return (payload_bytes + 255) // 256 * 256
 
-    def count(self, enc: torch.Tensor, labels: torch.Tensor) -> int:
-        """Add this rank's counts into every rank's buffer and signal; returns the epoch."""
-        self.epoch += 1
-        par = self.epoch & 1
-        L = N.lib()
-        N.check(L.hv_dev_class_counts_peers(self.e.dc.h, _ptr(enc), enc.shape[0], self.e.D, _ptr(labels), self.e.C,
-                                            _ptr(self.counts_ptrs[par]), _ptr(self.rows_ptrs[par]), self.world))
-        N.check(L.hv_dev_signal_peers(self.e.dc.h, _ptr(self.flags_ptrs), self.world, self.rank, self.epoch))
-        return self.epoch
+    @classmethod
+    def nbytes(cls, payload_bytes: int, world: int) -> int:
+        return 2 * cls.slot_bytes(payload_bytes) + 4 * world
+
+    def peer_ptrs(self, par: int, offset: int = 0) -> torch.Tensor:
+        """Device array of every rank's address of (parity slot + offset)."""
+        key = (par, offset)
+        if key not in self._ptrs:
+            self._ptrs[key] = torch.tensor([b_ + par * self.slot + offset for b_ in self.bases], dtype=torch.int64,
+                                           device=self.e.dev)
+        return self._ptrs[key]
+
+    def own(self, par: int, offset: int, shape, dtype) -> torch.Tensor:
+        return _wrap(self.bases[self.rank] + par * self.slot + offset, shape, dtype, self.e.dev)
+
+    def signal(self, epoch: int):
+        N.check(N.lib().hv_dev_signal_peers(self.e.dc.h, _ptr(self.flags_ptrs), self.world, self.rank, epoch))
 
     def wait(self, epoch: int):
-        N.check(N.lib().hv_dev_wait_peers(self.e.dc.h, C.c_void_p(self.bases[self.rank] + self.off_flags), self.world,
-                                          epoch))
-        return self.own(epoch & 1)
+        N.check(N.lib().hv_dev_wait_peers(self.e.dc.h, C.c_void_p(self.bases[self.rank] + self.off_flags),
+                                          self.world, epoch))
 
-    def reduce(self, enc: torch.Tensor, labels: torch.Tensor):
-        """count + wait: the global (counts, class rows) of this epoch."""
-        return self.wait(self.count(enc, labels))
-
-    def release(self, epoch: int):
-        counts, rows = self.own(epoch & 1)
-        counts.zero_()
-        rows.zero_()
+    def zero(self, par: int, nbytes: int):
+        self.own(par, 0, (nbytes,), torch.uint8).zero_()
 
     def close(self):
         L = N.lib()
-        for p in self._opened:
-            L.hv_shared_close(self.e.dc.h, C.c_void_p(p))
-        for p in self._owned:
-            L.hv_shared_free(self.e.dc.h, C.c_void_p(p))
+        for p_ in self._opened:
+            L.hv_shared_close(self.e.dc.h, C.c_void_p(p_))
+        for p_ in self._owned:
+            L.hv_shared_free(self.e.dc.h, C.c_void_p(p_))
         self._opened, self._owned = [], []
+
+
+class PeerCounts(PeerShared):
+    """Classical class counts fused with their all-reduce over peer memory:
+    `count` adds this rank's exact per-bit class counts and class row counts
+    into every rank's buffer and signals; `wait` returns the global counts;
+    `release` zeroes the parity slot once the caller has binarised it."""
+
+    def __init__(self, engine: "Engine", rank: int, world: int, group=None, local_ranks=None):
+        self.nc = engine.C * 32 * engine.W
+        self.off_rows = (self.nc * 4 + 7) // 8 * 8
+        super().__init__(engine, rank, world, self.payload(engine), group, local_ranks)
+        self.epoch = 0
+
+    @staticmethod
+    def payload(engine: "Engine") -> int:
+        nc = engine.C * 32 * engine.W
+        return (nc * 4 + 7) // 8 * 8 + 8 * engine.C
+
+    @classmethod
+    def buffer_bytes(cls, engine: "Engine", world: int) -> int:
+        return cls.nbytes(cls.payload(engine), world)
+
+    def own_counts(self, par: int):
+        e = self.e
+        return (self.own(par, 0, (e.C, 32 * e.W), torch.int32), self.own(par, self.off_rows, (e.C,), torch.int64))
+
+    def count(self, enc: torch.Tensor, labels: torch.Tensor) -> int:
+        self.epoch += 1
+        par = self.epoch & 1
+        N.check(N.lib().hv_dev_class_counts_peers(self.e.dc.h, _ptr(enc), enc.shape[0], self.e.D, _ptr(labels),
+                                                  self.e.C, _ptr(self.peer_ptrs(par)),
+                                                  _ptr(self.peer_ptrs(par, self.off_rows)), self.world))
+        self.signal(self.epoch)
+        return self.epoch
+
+    def wait(self, epoch: int):  # noqa: D102 - returns this rank's global counts of the epoch
+        PeerShared.wait(self, epoch)
+        return self.own_counts(epoch & 1)
+
+    def reduce(self, enc: torch.Tensor, labels: torch.Tensor):
+        return self.wait(self.count(enc, labels))
+
+    def release(self, epoch: int):
+        self.zero(epoch & 1, self.payload(self.e))
+
+
+class PeerPopc(PeerShared):
+    """The per-batch popcount all-reduce of word-sliced online training fused
+    into the partial-popcount kernel (hv_dev_online_partial_popc_peers)."""
+
+    def __init__(self, engine: "Engine", rank: int, world: int, batch_size: int, group=None, local_ranks=None):
+        self.bsz = batch_size
+        super().__init__(engine, rank, world, self.payload(engine, batch_size), group, local_ranks)
+
+    @staticmethod
+    def payload(engine: "Engine", batch_size: int) -> int:
+        return 4 * batch_size * engine.C
+
+    @classmethod
+    def buffer_bytes(cls, engine: "Engine", batch_size: int, world: int) -> int:
+        return cls.nbytes(cls.payload(engine, batch_size), world)
+
+    def partial(self, cv: torch.Tensor, words: int, batch: torch.Tensor, n: int, epoch: int):
+        par = epoch & 1
+        N.check(N.lib().hv_dev_online_partial_popc_peers(self.e.dc.h, _ptr(cv), self.e.C, words, _ptr(batch), n,
+                                                         _ptr(self.peer_ptrs(par)), self.world))
+        self.signal(epoch)
+
+    def summed(self, epoch: int, n: int) -> torch.Tensor:
+        PeerShared.wait(self, epoch)
+        return self.own(epoch & 1, 0, (n, self.e.C), torch.int32)
+
+    def release(self, epoch: int):
+        self.zero(epoch & 1, self.payload(self.e, self.bsz))
 
 
 def _wrap(ptr: int, shape, dtype, device):
     """A torch view of raw device memory (no ownership)."""
     class _CAI:
         def __init__(self):
-            typestr = {torch.int32: "<i4", torch.int64: "<i8", torch.float64: "<f8"}[dtype]
+            typestr = {torch.int32: "<i4", torch.int64: "<i8", torch.float64: "<f8", torch.uint8: "|u1"}[dtype]
             self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
                                              "version": 3, "strides": None, "stream": None}
 
@@ -409,8 +468,15 @@ class DSlicedOnline:
                                                    _ptr(e.cb.model_tiebreak), _ptr(self.acc), _ptr(self.weight),
                                                    _ptr(self.counts), _ptr(self.cv)))
 
-    def run(self, group=None):
-        """All batches; all-reduces the popcounts when torch.distributed has >1 rank."""
+    def run(self, group=None, peers: "PeerPopc | None" = None):
+        """All batches. With `peers` the popcount all-reduce is fused into the
+        partial kernel over peer memory; otherwise, with >1 torch.distributed
+        rank, the popcounts are all-reduced (NCCL)."""
+        if peers is not None:
+            for b, (start, n) in enumerate(self.batches()):
+                self.peer_partial(peers, start, n, b + 1)
+                self.peer_update(peers, start, n, b + 1)
+            return self.acc, self.weight, self.counts, self.cv
         dist = torch.distributed
         multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
         for start, n in self.batches():
@@ -419,6 +485,15 @@ class DSlicedOnline:
                 dist.all_reduce(p, group=group)
             self.update(start, n, p)
         return self.acc, self.weight, self.counts, self.cv
+
+    def peer_partial(self, peers: "PeerPopc", start: int, n: int, epoch: int):
+        """Add this rank's partial popcounts of a batch into every rank's buffer and signal."""
+        peers.partial(self.cv, self.words, self.enc[start:start + n], n, epoch)
+
+    def peer_update(self, peers: "PeerPopc", start: int, n: int, epoch: int):
+        """Wait for every rank's partials, apply the batch, free the parity slot."""
+        self.update(start, n, peers.summed(epoch, n))
+        peers.release(epoch)
 
 
 # ------------------------------------------------------------ sharding --

@@ -515,11 +515,8 @@ def test_peer_counts_emulated_ranks_equal_allreduce():
     F, B, D, C, rows, world = 342, 16, 1000, 3, 5000, 3
     cbk = dv.DeviceCodebook.make(F, B, D, seed=2)
     eng = dv.Engine(cbk, C)
-    bufs = []
-    for _ in range(world):
-        nc = C * 32 * eng.W
-        off_rows = (2 * nc * 4 + 7) // 8 * 8
-        bufs.append(torch.zeros(off_rows + 2 * C * 8 + 4 * world, dtype=torch.uint8, device="cuda"))
+    bufs = [torch.zeros(dv.PeerCounts.buffer_bytes(eng, world), dtype=torch.uint8, device="cuda")
+            for _ in range(world)]
     bases = [b.data_ptr() for b in bufs]
     pcs = [dv.PeerCounts(eng, r, world, local_ranks=bases) for r in range(world)]
     for epoch_seed in (7, 8, 9):
@@ -537,3 +534,36 @@ def test_peer_counts_emulated_ranks_equal_allreduce():
             assert torch.equal(got_r, want_r), (epoch_seed, r)
         for r in range(world):
             pcs[r].release(eps[r])
+
+
+def test_dsliced_online_fused_peer_popcounts_bitexact():
+    """Word-sliced online training with the per-batch popcount all-reduce fused
+    into the partial kernel over peer memory (device.PeerPopc), 3 ranks
+    emulated in one process: bit-identical to the single-GPU exact trainer."""
+    from paper_2206_04746_b200 import device as dv
+    F, D, C, rows, bsz, world = 561, 10000, 6, 1500, 128, 3
+    cbk = dv.DeviceCodebook.make(F, 16, D, seed=11)
+    eng = dv.Engine(cbk, C)
+    bins8, labels = eng.synth(0, rows, 0, 7)
+    enc = eng.encode(bins8)
+    acc_x, w_x, c_x, cv_x = eng.train_online(enc, labels, bsz)
+    W = enc.shape[1]
+    bufs = [torch.zeros(dv.PeerPopc.buffer_bytes(eng, bsz, world), dtype=torch.uint8, device="cuda")
+            for _ in range(world)]
+    bases = [b.data_ptr() for b in bufs]
+    ranks, peers = [], []
+    for r in range(world):
+        w0, nw = dv.word_slice(W, r, world)
+        ranks.append(dv.DSlicedOnline(eng, eng.encode_words(bins8, w0, nw), labels, bsz, w0))
+        peers.append(dv.PeerPopc(eng, r, world, bsz, local_ranks=bases))
+    for b, (start, n) in enumerate(ranks[0].batches()):
+        for rk, pp in zip(ranks, peers):
+            rk.peer_partial(pp, start, n, b + 1)
+        for rk, pp in zip(ranks, peers):
+            rk.peer_update(pp, start, n, b + 1)
+    eng.dc.check()
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([rk.acc for rk in ranks], dim=1), acc_x)
+    assert torch.equal(torch.cat([rk.cv for rk in ranks], dim=1), cv_x)
+    for rk in ranks:
+        assert torch.equal(rk.weight, w_x) and torch.equal(rk.counts, c_x)
