@@ -185,6 +185,25 @@ hv_status hv_fold_counts(hv_fold* fold, void** counts_dev, void** class_rows_dev
 hv_status hv_fold_predict(hv_context* ctx, hv_fold* fold, const uint32_t* model_tiebreak, int32_t* labels_out);
 void hv_fold_destroy(hv_fold* fold);
 
+/* ---- HBM-resident datasets: whole folds from fp64 features ---------------
+ * run_fold_packed (experiment.cpp:148-178) with the feature matrix resident
+ * across folds (time-series / leave-one-out splits re-fit and re-encode per
+ * fold without re-uploading): fit_discretizer on the train rows, discretize
+ * train and test rows, encode, train (classical, or online with batch_size),
+ * predict the test rows. train_idx / test_idx are host arrays of row indices
+ * (any order / subset); labels_out gets n_test labels; min_out / max_out
+ * (nullable, features doubles) the fitted discretizer. */
+typedef struct hv_dataset hv_dataset;
+hv_status hv_dataset_create(hv_context* ctx, const double* X, size_t rows, size_t features,
+                            const int32_t* labels, hv_dataset** out);
+void hv_dataset_destroy(hv_dataset* ds);
+hv_status hv_dataset_fold(hv_context* ctx, const hv_dataset* ds, const uint64_t* train_idx,
+                          size_t n_train, const uint64_t* test_idx, size_t n_test, size_t bins,
+                          const uint32_t* id_vectors, const uint32_t* value_vectors, size_t dim,
+                          hv_binding binding, const uint32_t* encode_tiebreak, size_t class_count,
+                          hv_metric metric, double gamma, const uint32_t* model_tiebreak, int online,
+                          size_t batch_size, int32_t* labels_out, double* min_out, double* max_out);
+
 /* model.hpp:67-70 hamming_distance_words (host-side helper, no device) */
 double hv_hamming_distance_words(const uint32_t* a, const uint32_t* b, size_t dim);
 

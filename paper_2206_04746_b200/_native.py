@@ -123,6 +123,9 @@ SIGNATURES = {
     "hv_dev_class_counts_peers": (ST, [vp, vp, sz, sz, vp, sz, vp, vp, sz]),
     "hv_dev_signal_peers": (ST, [vp, vp, sz, sz, u32]),
     "hv_dev_wait_peers": (ST, [vp, vp, sz, u32]),
+    "hv_dataset_create": (ST, [vp, vp, sz, sz, vp, C.POINTER(vp)]),
+    "hv_dataset_destroy": (None, [vp]),
+    "hv_dataset_fold": (ST, [vp, vp, vp, sz, vp, sz, sz, vp, vp, sz, ci, vp, sz, ci, dbl, vp, ci, sz, vp, vp, vp]),
     "hv_fold_encode_train": (ST, [vp, vp, sz, vp, vp, sz, sz, vp, vp, sz, sz, vp, sz, C.POINTER(vp)]),
     "hv_fold_counts": (ST, [vp, C.POINTER(vp), C.POINTER(vp)]),
     "hv_fold_predict": (ST, [vp, vp, vp, vp]),

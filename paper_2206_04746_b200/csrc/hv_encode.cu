@@ -61,7 +61,7 @@ __global__ void narrow_bins_kernel(const uint32_t* __restrict__ in, uint64_t row
 // move on strict </>, then partials are folded into row 0 in row order.
 __global__ void minmax_partial_kernel(const double* __restrict__ data, uint64_t rows, uint32_t F,
                                       uint64_t rows_per_block, double* __restrict__ pmin,
-                                      double* __restrict__ pmax) {
+                                      double* __restrict__ pmax, const uint64_t* __restrict__ idx = nullptr) {
   const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= F) return;
   const uint64_t r0 = 1 + blockIdx.y * rows_per_block;
@@ -69,7 +69,7 @@ __global__ void minmax_partial_kernel(const double* __restrict__ data, uint64_t 
   double mn = __longlong_as_double(0x7FF0000000000000ll);   // +inf
   double mx = __longlong_as_double(0xFFF0000000000000ull);  // -inf
   for (uint64_t r = r0; r < r1; ++r) {
-    const double v = data[r * F + f];
+    const double v = data[(idx ? idx[r] : r) * F + f];
     if (v < mn) mn = v;
     if (v > mx) mx = v;
   }
@@ -79,10 +79,12 @@ __global__ void minmax_partial_kernel(const double* __restrict__ data, uint64_t 
 
 __global__ void minmax_final_kernel(const double* __restrict__ data, uint32_t F, uint32_t nblocks,
                                     const double* __restrict__ pmin, const double* __restrict__ pmax,
-                                    double* __restrict__ mn_out, double* __restrict__ mx_out) {
+                                    double* __restrict__ mn_out, double* __restrict__ mx_out,
+                                    const uint64_t* __restrict__ idx = nullptr) {
   const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= F) return;
-  double mn = data[f], mx = data[f];
+  const uint64_t r0 = idx ? idx[0] : 0;
+  double mn = data[r0 * F + f], mx = data[r0 * F + f];
   for (uint32_t b = 0; b < nblocks; ++b) {
     const double a = pmin[static_cast<uint64_t>(b) * F + f];
     const double c = pmax[static_cast<uint64_t>(b) * F + f];
@@ -99,15 +101,16 @@ __global__ void minmax_final_kernel(const double* __restrict__ data, uint32_t F,
 template <class OutT>
 __global__ void discretize_kernel(const double* __restrict__ data, uint64_t rows, uint32_t F,
                                   const double* __restrict__ mn, const double* __restrict__ mx, uint32_t B,
-                                  OutT* __restrict__ out, uint32_t ld_out) {
+                                  OutT* __restrict__ out, uint32_t ld_out, const uint64_t* __restrict__ idx = nullptr) {
   const uint64_t total = rows * F;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t r = i / F;
     const uint32_t f = static_cast<uint32_t>(i % F);
     const double lo = mn[f], hi = mx[f];
+    const double x = data[(idx ? idx[r] : r) * F + f];
     uint32_t b = 0;
     if (!(lo == hi)) {
-      const double t = floor(__dmul_rn(__ddiv_rn(__dsub_rn(data[i], lo), __dsub_rn(hi, lo)), static_cast<double>(B)));
+      const double t = floor(__dmul_rn(__ddiv_rn(__dsub_rn(x, lo), __dsub_rn(hi, lo)), static_cast<double>(B)));
       const double top = static_cast<double>(B - 1);
       if (t >= top) b = B - 1;
       else if (t > 0.0) b = static_cast<uint32_t>(t);
@@ -220,6 +223,35 @@ void launch_generic(hv_context* ctx, cudaStream_t st, int nh, const uint8_t* bin
   }
 #undef HV_GEN_CASE
   launched("encode_generic_kernel");
+}
+
+// Device-resident discretizer over an optional row-index subset (datasets kept
+// in HBM across folds): fit = the ordered first-row min/max of encoding.cpp:
+// 93-119 over rows idx[0..n); discretize writes uint8 bins with pitch ldb.
+void fit_discretizer_device(hv_context* ctx, cudaStream_t st, const double* X, size_t F, const uint64_t* idx,
+                            size_t n, double* mn, double* mx) {
+  const uint64_t rpb = 4096;
+  const uint32_t nblocks = static_cast<uint32_t>(n > 1 ? (n - 1 + rpb - 1) / rpb : 0);
+  DevBuf<double> pmin(std::max<size_t>(1, nblocks) * F, st), pmax(std::max<size_t>(1, nblocks) * F, st);
+  if (nblocks) {
+    dim3 grid(grid_for(F, 128), nblocks);
+    minmax_partial_kernel<<<grid, 128, 0, st>>>(X, n, static_cast<uint32_t>(F), rpb, pmin.ptr, pmax.ptr, idx);
+    launched("minmax_partial_kernel");
+  }
+  minmax_final_kernel<<<grid_for(F, 128), 128, 0, st>>>(X, static_cast<uint32_t>(F), nblocks, pmin.ptr, pmax.ptr, mn,
+                                                         mx, idx);
+  launched("minmax_final_kernel");
+}
+
+void discretize_rows_device(hv_context* ctx, cudaStream_t st, const double* X, size_t F, const uint64_t* idx,
+                            size_t n, const double* mn, const double* mx, size_t B, uint8_t* out, size_t ldb) {
+  if (n == 0) return;
+  ck(cudaMemsetAsync(out, 0, n * ldb, st), "memset bins");
+  const uint64_t items = n * F;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((items + 255) / 256, uint64_t(ctx->sm_count) * 16));
+  discretize_kernel<uint8_t><<<grid, 256, 0, st>>>(X, n, static_cast<uint32_t>(F), mn, mx, static_cast<uint32_t>(B),
+                                                   out, static_cast<uint32_t>(ldb), idx);
+  launched("discretize_kernel");
 }
 
 // Encodes validated uint8 bins on stream `st`.

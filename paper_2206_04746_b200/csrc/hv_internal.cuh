@@ -169,6 +169,12 @@ void encode_device(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, size_
 void narrow_device(hv_context* ctx, cudaStream_t st, const uint32_t* bins32, size_t rows, size_t F, size_t B,
                    uint8_t* bins8, size_t ldb, uint64_t flat_base);
 inline size_t bins_pitch(size_t F) { return (F + 63) / 64 * 64; }
+// Discretizer on HBM-resident fp64 features over rows idx[0..n) (idx may be
+// null: rows 0..n): fit (encoding.cpp:93-119) and discretize to uint8 bins.
+void fit_discretizer_device(hv_context* ctx, cudaStream_t st, const double* X, size_t F, const uint64_t* idx,
+                            size_t n, double* mn, double* mx);
+void discretize_rows_device(hv_context* ctx, cudaStream_t st, const double* X, size_t F, const uint64_t* idx,
+                            size_t n, const double* mn, const double* mx, size_t B, uint8_t* out, size_t ldb);
 bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
                const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
                uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo);

@@ -1164,10 +1164,40 @@ struct hv_fold {
   hvb::DevBuf<uint64_t> class_rows;
 };
 
+struct hv_dataset {
+  size_t rows = 0, F = 0;
+  hvb::DevBuf<double> X;
+  hvb::DevBuf<int32_t> y;
+};
+
 namespace hvb {
 namespace {
 
-// Chunked, double-buffered upload + narrow + encode of host uint32 bins into `out`.
+__global__ void gather_labels_kernel(const int32_t* __restrict__ y, const uint64_t* __restrict__ idx, uint64_t n,
+                                     int32_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    out[i] = y[idx[i]];
+  }
+}
+
+// validates labels into the label latch (first offending index)
+void check_labels_device(hv_context* ctx, cudaStream_t st, const int32_t* y, size_t n, size_t C) {
+  if (n == 0) return;
+  DevBuf<uint32_t> hist(C, st);
+  hist.zero();
+  label_hist_kernel<<<sgrid(ctx, n, 256), 256, 0, st>>>(y, n, static_cast<uint32_t>(C), hist.ptr, ctx->d_err);
+  launched("label_hist_kernel");
+}
+
+void check_indices(const uint64_t* idx, size_t n, size_t rows, const char* what) {
+  for (size_t i = 0; i < n; ++i) {
+    if (idx[i] >= rows) {
+      invalid(std::string("dataset_fold: ") + what + " row index " + std::to_string(idx[i]) + " out of range (rows = " +
+              std::to_string(rows) + ")");
+    }
+  }
+}
+
 }  // namespace
 }  // namespace hvb
 
@@ -1267,5 +1297,122 @@ hv_status hv_fold_predict(hv_context* ctx, hv_fold* fold, const uint32_t* model_
 }
 
 void hv_fold_destroy(hv_fold* fold) { delete fold; }
+
+// ---- dataset-resident folds (run_fold_packed, experiment.cpp:148-178) ----
+hv_status hv_dataset_create(hv_context* ctx, const double* X, size_t rows, size_t features, const int32_t* labels,
+                            hv_dataset** out) {
+  return guarded([&] {
+    require(ctx);
+    if (!out) invalid("dataset: null output");
+    *out = nullptr;
+    if (rows == 0 || features == 0) invalid("dataset: empty matrix");
+    auto ds = std::make_unique<hv_dataset>();
+    ds->rows = rows;
+    ds->F = features;
+    ds->X = DevBuf<double>(rows * features, ctx->stream);
+    ds->y = DevBuf<int32_t>(rows, ctx->stream);
+    upload_host(ctx, X, rows * features * sizeof(double), ds->X.ptr);
+    upload_host(ctx, labels, rows * sizeof(int32_t), ds->y.ptr);
+    sync(ctx);
+    *out = ds.release();
+  });
+}
+
+void hv_dataset_destroy(hv_dataset* ds) { delete ds; }
+
+hv_status hv_dataset_fold(hv_context* ctx, const hv_dataset* ds, const uint64_t* train_idx, size_t n_train,
+                          const uint64_t* test_idx, size_t n_test, size_t bins, const uint32_t* id_vectors,
+                          const uint32_t* value_vectors, size_t dim, hv_binding binding,
+                          const uint32_t* encode_tiebreak, size_t class_count, hv_metric metric, double gamma,
+                          const uint32_t* model_tiebreak, int online, size_t batch_size, int32_t* labels_out,
+                          double* min_out, double* max_out) {
+  return guarded([&] {
+    require(ctx);
+    if (!ds) invalid("dataset_fold: null dataset");
+    // reference order: fit_discretizer, discretize, encode, train, predict
+    if (n_train == 0) invalid("fit_discretizer: empty training matrix");
+    if (bins < 2) invalid("fit_discretizer: need at least 2 bins");
+    if (class_count == 0 || dim == 0) invalid("dataset_fold: classes and dim must be >= 1");
+    if (online && batch_size == 0) invalid("train_online: batch_size must be >= 1");
+    if (metric != HV_METRIC_HAMMING && metric != HV_METRIC_COSINE) fail(HV_ERR_LOGIC, "bad Metric");
+    check_indices(train_idx, n_train, ds->rows, "train");
+    check_indices(test_idx, n_test, ds->rows, "test");
+    cudaStream_t st = ctx->stream;
+    const size_t F = ds->F, C = class_count, D = dim, W = words_per_row(D), ldb = bins_pitch(F);
+    const size_t n = n_train + n_test;
+    DevBuf<uint64_t> idx(n, st);
+    ck(cudaMemcpyAsync(idx.ptr, train_idx, n_train * sizeof(uint64_t), cudaMemcpyHostToDevice, st), "H2D idx");
+    if (n_test) {
+      ck(cudaMemcpyAsync(idx.ptr + n_train, test_idx, n_test * sizeof(uint64_t), cudaMemcpyHostToDevice, st), "H2D idx");
+    }
+    DevBuf<double> mn(F, st), mx(F, st);
+    fit_discretizer_device(ctx, st, ds->X.ptr, F, idx.ptr, n_train, mn.ptr, mx.ptr);
+    DevBuf<uint8_t> b8(n * ldb, st);
+    discretize_rows_device(ctx, st, ds->X.ptr, F, idx.ptr, n, mn.ptr, mx.ptr, bins, b8.ptr, ldb);
+    DevBuf<uint32_t> d_id(F * W, st), d_val(bins * W, st), d_etb(W, st), d_mtb(W, st);
+    d_id.upload(id_vectors);
+    d_val.upload(value_vectors);
+    d_etb.upload(encode_tiebreak);
+    d_mtb.upload(model_tiebreak);
+    DevBuf<uint32_t> enc(n * W, st);
+    encode_device(ctx, st, b8.ptr, ldb, n, F, d_id.ptr, d_val.ptr, bins, D, binding, d_etb.ptr, enc.ptr);
+    DevBuf<int32_t> ytr(n_train, st), lab(std::max<size_t>(n_test, 1), st);
+    gather_labels_kernel<<<sgrid(ctx, n_train, 256), 256, 0, st>>>(ds->y.ptr, idx.ptr, n_train, ytr.ptr);
+    launched("gather_labels_kernel");
+    DevBuf<double> acc(C * D, st), weight(C, st);
+    DevBuf<uint64_t> counts(C, st);
+    DevBuf<uint32_t> cv(C * W, st);
+    if (online) {
+      // labels are validated by the bootstrap's classical counts (first batch)
+      // and, for later batches, below against the label latch
+      check_labels_device(ctx, st, ytr.ptr, n_train, C);
+      train_online_device(ctx, st, metric, enc.ptr, n_train, D, ytr.ptr, C, batch_size, gamma, d_mtb.ptr, acc.ptr,
+                          weight.ptr, counts.ptr, cv.ptr);
+    } else {
+      DevBuf<uint32_t> cnt(C * 32 * W, st);
+      cnt.zero();
+      counts.zero();
+      class_counts_device(ctx, st, enc.ptr, n_train, W, ytr.ptr, C, cnt.ptr, counts.ptr);
+      binarize_counts_device(ctx, st, cnt.ptr, counts.ptr, C, D, d_mtb.ptr, cv.ptr);
+      if (metric == HV_METRIC_COSINE) {
+        init_from_counts_kernel<<<sgrid(ctx, C * D, 256), 256, 0, st>>>(cnt.ptr, counts.ptr, C, D, W, acc.ptr,
+                                                                        weight.ptr, counts.ptr);
+        launched("init_from_counts_kernel");
+      }
+    }
+    if (n_test) {
+      const uint32_t* q = enc.ptr + n_train * W;
+      if (metric == HV_METRIC_HAMMING) {
+        predict_hamming_device(ctx, st, cv.ptr, C, D, q, n_test, lab.ptr, nullptr, nullptr);
+      } else {
+        DevBuf<double> sc(n_test * C, st);
+        cosine_scores_device(ctx, st, acc.ptr, C, D, q, n_test, sc.ptr, 0);
+        argmax_kernel<<<sgrid(ctx, n_test, 128), 128, 0, st>>>(sc.ptr, n_test, static_cast<uint32_t>(C), lab.ptr);
+        launched("argmax_kernel");
+      }
+      ck(cudaMemcpyAsync(labels_out, lab.ptr, n_test * sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H labels");
+    }
+    if (min_out) mn.download(min_out);
+    if (max_out) mx.download(max_out);
+    sync(ctx);
+    unsigned long long l[kErrKinds];
+    read_latch(ctx, l);
+    if (l[kErrLabel] != ~0ull || l[kErrZeroQuery] != ~0ull) {
+      reset_latch(ctx);
+      if (l[kErrLabel] != ~0ull) {
+        int32_t bad = 0;
+        const uint64_t k = l[kErrLabel];
+        ck(cudaMemcpy(&bad, ytr.ptr + k, sizeof(int32_t), cudaMemcpyDeviceToHost), "D2H label");
+        // model.cpp:282-301: the bootstrap batch is checked by train_classical,
+        // every batch again by online_update (row index within the batch)
+        const bool boot = !online || k < std::min(batch_size, n_train);
+        const uint64_t row = boot ? k : k - (k / batch_size) * batch_size;
+        invalid(std::string(boot ? "train_classical" : "online_update") + ": label " + std::to_string(bad) + " at row " +
+                std::to_string(row) + " out of range (classes = " + std::to_string(C) + ")");
+      }
+      fail(HV_ERR_DOMAIN, "cosine_similarity: zero query vector");
+    }
+  });
+}
 
 }  // extern "C"

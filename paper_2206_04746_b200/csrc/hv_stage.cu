@@ -20,6 +20,7 @@
 #include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <functional>
 #include <mutex>
 #include <thread>
@@ -234,6 +235,28 @@ uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, si
     if (after) after(r0, n, k, st);
   }
   return ~0ull;
+}
+
+void upload_host(hv_context* ctx, const void* src, size_t bytes, void* dst) {
+  if (bytes == 0) return;
+  HostStager& hs = stager(ctx);
+  const size_t chunk = std::min<size_t>(bytes, size_t(64) << 20);
+  hs.reserve(chunk);
+  const uint8_t* in = static_cast<const uint8_t*>(src);
+  uint8_t* out = static_cast<uint8_t*>(dst);
+  size_t k = 0;
+  for (size_t off = 0; off < bytes; off += chunk, ++k) {
+    const size_t n = std::min(chunk, bytes - off);
+    const int slot = static_cast<int>(k % HostStager::kSlots);
+    ck(cudaEventSynchronize(hs.done[slot]), "stage slot wait");
+    const size_t parts = (hs.pool.size() + 1) * 2, per = (n + parts - 1) / parts;
+    hs.pool.parallel_for((n + per - 1) / per, [&](size_t i) {
+      const size_t a = i * per, b = std::min(n, a + per);
+      std::memcpy(hs.slot[slot] + a, in + off + a, b - a);
+    });
+    ck(cudaMemcpyAsync(out + off, hs.slot[slot], n, cudaMemcpyHostToDevice, ctx->stream), "H2D upload");
+    ck(cudaEventRecord(hs.done[slot], ctx->stream), "cudaEventRecord");
+  }
 }
 
 }  // namespace hvb

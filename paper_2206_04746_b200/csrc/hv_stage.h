@@ -72,4 +72,9 @@ uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, si
                           const ChunkOut& out_for, DevBuf<uint8_t>* b8, size_t chunk, size_t& k,
                           const ChunkAfter& after = {});
 
+// Copies `bytes` of (pageable) host memory to the device on the context
+// stream through the pinned staging ring (host threads fill a slot while the
+// previous one is in flight).
+void upload_host(hv_context* ctx, const void* src, size_t bytes, void* dst);
+
 }  // namespace hvb

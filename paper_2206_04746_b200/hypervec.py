@@ -412,3 +412,47 @@ def hamming_distance(a: PackedBitMatrix, row_a: int, b: PackedBitMatrix, row_b: 
     if a.dim != b.dim:
         raise InvalidArgument(f"hamming_distance: dimensions {a.dim} vs {b.dim}")
     return hamming_distance_words(a.words[row_a], b.words[row_b], a.dim)
+
+
+class Dataset:
+    """An HBM-resident feature matrix for repeated folds (run_fold_packed,
+    experiment.cpp:148-178, with the discretizer re-fit per fold on device)."""
+
+    def __init__(self, X, labels):
+        X = np.ascontiguousarray(X, np.float64)
+        y = np.ascontiguousarray(labels, np.int32)
+        if X.ndim != 2 or y.shape[0] != X.shape[0]:
+            raise InvalidArgument("dataset: X must be rows x features with one label per row")
+        self.rows, self.features = X.shape
+        h = C.c_void_p()
+        N.check(N.lib().hv_dataset_create(_ctx(), _p(X), self.rows, self.features, _p(y), C.byref(h)))
+        self._h = h
+
+    def fold(self, train_idx, test_idx, codebook: Codebook, encode_tiebreak: PackedBitMatrix, cfg: ModelConfig,
+             trainer: str = "classical", batch_size: int = 1024):
+        """Labels of the test rows, plus the fitted (min, max) of the train rows."""
+        tr = np.ascontiguousarray(train_idx, np.uint64)
+        te = np.ascontiguousarray(test_idx, np.uint64)
+        labels = np.zeros(max(te.size, 1), np.int32)
+        mn = np.zeros(self.features)
+        mx = np.zeros(self.features)
+        mtb = PackedBitMatrix(1, cfg.dim)
+        N.check(N.lib().hv_generate_random(1, cfg.dim, N.lib().hv_derive_seed(cfg.seed, 3), _p(mtb.words)))
+        N.check(N.lib().hv_dataset_fold(_ctx(), self._h, _p(tr), tr.size, _p(te), te.size,
+                                        codebook.bin_count(), _p(codebook.id_vectors.words),
+                                        _p(codebook.value_vectors.words), cfg.dim, codebook.binding,
+                                        _p(encode_tiebreak.words), cfg.class_count, cfg.metric, cfg.gamma,
+                                        _p(mtb.words), 1 if trainer == "online" else 0, batch_size, _p(labels),
+                                        _p(mn), _p(mx)))
+        return labels[:te.size], mn, mx
+
+    def close(self):
+        if self._h:
+            N.lib().hv_dataset_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -567,3 +567,56 @@ def test_dsliced_online_fused_peer_popcounts_bitexact():
     assert torch.equal(torch.cat([rk.cv for rk in ranks], dim=1), cv_x)
     for rk in ranks:
         assert torch.equal(rk.weight, w_x) and torch.equal(rk.counts, c_x)
+
+
+@pytest.mark.parametrize("trainer,metric,split", [("classical", 0, "tscv"), ("online", 0, "tscv"),
+                                                  ("classical", 1, "subset"), ("online", 0, "subset"),
+                                                  ("online", 1, "tscv")])
+def test_dataset_fold_matches_reference_pipeline(trainer, metric, split):
+    """run_fold_packed (experiment.cpp:148-178) on an HBM-resident fp64 dataset:
+    discretizer fit on the train rows, discretize, encode, train, predict —
+    labels and fitted min/max bit-identical to the oracle pipeline, for
+    contiguous (time-series) and arbitrary (leave-one-out style) row subsets,
+    over several folds of the same resident dataset."""
+    rng = np.random.default_rng(17 + metric)
+    n, F, C, B, D = 900, 37, 4, 16, 1000
+    y = rng.integers(0, C, n).astype(np.int32)
+    centers = rng.normal(size=(C, F))
+    X = centers[y] + 0.7 * rng.normal(size=(n, F))
+    X[5, 3] = np.nan
+    ds = hv.Dataset(X, y)
+    cb = hv.make_codebook(0, 0, F, B, D, 123)
+    etb = hv.generate_random(1, D, 456)
+    cfg = hv.ModelConfig(class_count=C, dim=D, metric=metric, gamma=0.8, seed=9)
+    mtb = hv.generate_random(1, D, hv.derive_seed(9, 3))
+    for k in range(3):
+        if split == "tscv":
+            tr = np.arange(0, 300 + 200 * k)
+            te = np.arange(300 + 200 * k, 400 + 200 * k)
+        else:
+            perm = rng.permutation(n)
+            tr, te = np.sort(perm[:500]), perm[500:650]
+        labels, mn, mx = ds.fold(tr, te, cb, etb, cfg, trainer, 64)
+        omn, omx = O.fit_discretizer(X[tr], B)
+        np.testing.assert_array_equal(mn, omn)
+        np.testing.assert_array_equal(mx, omx)
+        bins = O.discretize_matrix(X[np.concatenate([tr, te])], omn, omx, B)
+        enc = O.encode_batch(bins, cb.id_vectors.words, cb.value_vectors.words, B, D, O.BIND_ID_LEVEL, etb.words)
+        m = O.NaiveModel(C, D, mtb.words, metric, 0.8)
+        if trainer == "online":
+            m.train_online(enc[:tr.size], y[tr], 64)
+        else:
+            m.train_classical(enc[:tr.size], y[tr])
+        want, _ = m.predict(enc[tr.size:])
+        np.testing.assert_array_equal(labels, want)
+    bad = y.copy()
+    bad[250] = C
+    ds2 = hv.Dataset(X, bad)
+    with pytest.raises(hv.InvalidArgument, match=r"online_update: label 4 at row 58 out of range \(classes = 4\)"):
+        ds2.fold(np.arange(300), np.arange(300, 400), cb, etb, cfg, "online", 64)
+    with pytest.raises(hv.InvalidArgument, match=r"train_classical: label 4 at row 250 out of range"):
+        ds2.fold(np.arange(300), np.arange(300, 400), cb, etb, cfg, "classical", 64)
+    with pytest.raises(hv.InvalidArgument, match="fit_discretizer: empty training matrix"):
+        ds.fold(np.arange(0), np.arange(10), cb, etb, cfg)
+    ds.close()
+    ds2.close()
