@@ -367,16 +367,19 @@ def test_online_modes_vs_oracle_bitexact(C, D, n, bsz):
     np.testing.assert_array_equal(on.class_vectors.words, oo.class_vectors)
 
 
-@pytest.mark.parametrize("popc", ["0", "1"])
+@pytest.mark.parametrize("popc", ["0", "1", "imma"])
 @pytest.mark.parametrize("C,D,n", [(32, 1000, 257), (33, 64, 100), (100, 4096, 300), (64, 10000, 70), (40, 31, 33),
                                    (129, 500, 40), (200, 96, 77), (64, 33, 300), (100, 1000, 129)])
 def test_predict_many_classes_tiled_vs_oracle(C, D, n, popc, monkeypatch):
-    """The many-class Hamming scans (C >= 32) — tensor-core (default from 64
-    classes) and the CTA-tiled POPC scan (HVB200_PREDICT_POPC): labels and fp64 distances
+    """The many-class Hamming scans (C >= 32) — tcgen05 tensor cores (default
+    from 64 classes), legacy mma.sync (HVB200_PREDICT_IMMA) and the CTA-tiled
+    POPC scan (HVB200_PREDICT_POPC): labels and fp64 distances
     bit-exact vs the oracle, including ties between classes (duplicated class
     vectors must resolve to the lowest class) and several class tiles."""
     if popc == "1":
         monkeypatch.setenv("HVB200_PREDICT_POPC", "1")
+    if popc == "imma":
+        monkeypatch.setenv("HVB200_PREDICT_IMMA", "1")
     rng = np.random.default_rng(C + D + n)
     W = (D + 31) // 32
     cvb = rng.integers(0, 2, (C, D), dtype=np.uint8)
