@@ -207,6 +207,13 @@ hv_status hv_dataset_fold(hv_context* ctx, const hv_dataset* ds, const uint64_t*
 /* model.hpp:67-70 hamming_distance_words (host-side helper, no device) */
 double hv_hamming_distance_words(const uint32_t* a, const uint32_t* b, size_t dim);
 
+/* Host-only (no device): narrow rows x features uint32 bins to uint8 rows of
+ * pitch ldb (zero padded) on the library's host threads, as the host-pointer
+ * calls do before their H2D copies; *first_bad = first flat index with a bin
+ * >= bins, or UINT64_MAX. */
+hv_status hv_host_narrow_bins(const uint32_t* bins32, size_t rows, size_t features, size_t bins,
+                              uint8_t* out, size_t ldb, uint64_t* first_bad);
+
 /* ---- device-resident API (device pointers, async on the context stream) -- */
 /* Latched data errors of earlier hv_dev_* calls (synchronises the stream). */
 hv_status hv_dev_check(hv_context* ctx);

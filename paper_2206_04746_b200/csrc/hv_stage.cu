@@ -125,7 +125,9 @@ NarrowFn narrow_fn() {
   return fn;
 }
 
-unsigned host_threads() {
+}  // namespace
+
+unsigned host_thread_count() {
   if (const char* e = getenv("HVB200_HOST_THREADS")) {
     const int n = atoi(e);
     if (n >= 1) return static_cast<unsigned>(n);
@@ -140,9 +142,7 @@ unsigned host_threads() {
   return std::max(1u, std::min(hc, 64u));
 }
 
-}  // namespace
-
-HostStager::HostStager() : pool(host_threads() - 1) {
+HostStager::HostStager() : pool(host_thread_count() - 1) {
   for (int i = 0; i < kSlots; ++i) {
     ck(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming), "cudaEventCreate");
   }
@@ -172,8 +172,9 @@ void HostStager::reserve(size_t bytes) {
   cap = bytes;
 }
 
-uint64_t HostStager::narrow(const uint32_t* in, size_t rows, size_t F, size_t B, size_t ldb, int s) {
-  uint8_t* out = slot[s];
+uint64_t narrow_rows_host(ThreadPool& pool, const uint32_t* in, size_t rows, size_t F, size_t B, uint8_t* out,
+                          size_t ldb) {
+  if (rows == 0) return ~0ull;
   const unsigned parts = std::max<unsigned>(1, (pool.size() + 1) * 4);
   const size_t per = (rows + parts - 1) / parts;
   const size_t pieces = (rows + per - 1) / per;
@@ -192,6 +193,10 @@ uint64_t HostStager::narrow(const uint32_t* in, size_t rows, size_t F, size_t B,
     }
   }
   return ~0ull;
+}
+
+uint64_t HostStager::narrow(const uint32_t* in, size_t rows, size_t F, size_t B, size_t ldb, int s) {
+  return narrow_rows_host(pool, in, rows, F, B, slot[s], ldb);
 }
 
 HostStager& stager(hv_context* ctx) {
@@ -260,3 +265,20 @@ void upload_host(hv_context* ctx, const void* src, size_t bytes, void* dst) {
 }
 
 }  // namespace hvb
+
+extern "C" {
+
+// Host-only narrowing (no device, no context): the staging kernel of the host
+// pipeline, exposed for callers that stage bins themselves and for CPU tests.
+hv_status hv_host_narrow_bins(const uint32_t* bins32, size_t rows, size_t features, size_t bins, uint8_t* out,
+                              size_t ldb, uint64_t* first_bad) {
+  return hvb::guarded([&] {
+    if (ldb < features) hvb::invalid("narrow_bins: ldb must be >= features");
+    if (bins > 256) hvb::invalid("narrow_bins: bins must be <= 256");
+    static hvb::ThreadPool pool(hvb::host_thread_count() - 1);
+    const uint64_t bad = hvb::narrow_rows_host(pool, bins32, rows, features, bins, out, ldb);
+    if (first_bad) *first_bad = bad;
+  });
+}
+
+}  // extern "C"

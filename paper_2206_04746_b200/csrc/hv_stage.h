@@ -55,6 +55,11 @@ struct HostStager {
   uint64_t narrow(const uint32_t* in, size_t rows, size_t F, size_t B, size_t ldb, int s);
 };
 
+unsigned host_thread_count();
+// rows x F uint32 bins -> uint8 rows of pitch ldb (zero padded) on the pool;
+// returns the first flat index whose bin is >= B, or ~0.
+uint64_t narrow_rows_host(ThreadPool& pool, const uint32_t* in, size_t rows, size_t F, size_t B, uint8_t* out,
+                          size_t ldb);
 HostStager& stager(hv_context* ctx);
 void destroy_stager(hv_context* ctx);
 size_t stage_chunk_rows(size_t rows, size_t F);

@@ -105,3 +105,29 @@ def test_hamming_distance_words_host_helper():
     a = O.pack_rows(np.array([[1, 1, 0, 0, 1]], np.uint8))
     b = O.pack_rows(np.array([[1, 0, 0, 1, 1]], np.uint8))
     assert hv.hamming_distance_words(a[0], b[0], 5) == 2.0 / 5.0
+
+
+def test_host_narrowing_matches_numpy_and_finds_first_bad_bin():
+    """The host staging kernel of hv_encode_batch / hv_fold_* (csrc/hv_stage.cu),
+    callable without a device: uint32 -> uint8 rows of pitch ldb, zero padding,
+    and the first offending flat index (encoding.cpp:43-55 check order)."""
+    import ctypes as C
+    import numpy as np
+    from paper_2206_04746_b200 import _native as N
+    rng = np.random.default_rng(3)
+    for rows, F, B, ldb in [(1, 1, 2, 64), (1000, 342, 16, 384), (777, 65, 7, 128), (0, 5, 4, 64)]:
+        bins = rng.integers(0, B, (rows, F)).astype(np.uint32)
+        out = np.full((max(rows, 1), ldb), 0xAB, np.uint8)
+        bad = C.c_uint64()
+        N.check(N.lib().hv_host_narrow_bins(bins.ctypes.data, rows, F, B, out.ctypes.data, ldb, C.byref(bad)))
+        assert bad.value == 2**64 - 1
+        if rows:
+            np.testing.assert_array_equal(out[:rows, :F], bins.astype(np.uint8))
+            assert not out[:rows, F:].any()
+    bins = rng.integers(0, 16, (5000, 30)).astype(np.uint32)
+    bins[4321, 7] = 16
+    bins[4999, 0] = 99
+    out = np.zeros((5000, 64), np.uint8)
+    bad = C.c_uint64()
+    N.check(N.lib().hv_host_narrow_bins(bins.ctypes.data, 5000, 30, 16, out.ctypes.data, 64, C.byref(bad)))
+    assert bad.value == 4321 * 30 + 7
