@@ -294,7 +294,12 @@ __global__ void __launch_bounds__(kMmaThreads) predict_imma_kernel(const uint32_
 }
 
 // tcgen05 variant (hv_scan_tc.cuh): 128 rows x 128 classes per tile, the dot
-// products accumulated in TMEM by single-thread-issued UMMAs.
+// products accumulated in TMEM by single-thread-issued UMMAs. Lanes l and l+16
+// of a warp load the two 16-byte halves of one row's (class's) 32-byte chunk
+// sector, so a warp's load touches 16 sectors instead of 32 (VEC: one 16-byte
+// load per thread when rows are 16-byte aligned, W % 4 == 0), and each
+// quarter-warp's 16-byte shared stores hit 8 distinct rows (conflict-free).
+template <bool VEC>
 __global__ void __launch_bounds__(tc::kThreads, 1) predict_tc_kernel(const uint32_t* __restrict__ cv, uint32_t C,
                                                                      uint32_t D, uint32_t W,
                                                                      const uint32_t* __restrict__ enc, uint64_t rows,
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) predict_tc_kernel(const uint3
                                                                      uint32_t* __restrict__ pops) {
   extern __shared__ uint8_t tc_raw[];
   tc::Smem& s = *reinterpret_cast<tc::Smem*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&s.tmem)),
                  "n"(tc::kN));
@@ -327,28 +332,38 @@ __global__ void __launch_bounds__(tc::kThreads, 1) predict_tc_kernel(const uint3
   // (indexed arrays would live in local memory)
   uint32_t phase_bits = 0, pending_bits = 0;
   uint32_t g = 0;  // global chunk counter (stage = g & 1)
-  // staging: thread -> row/class sr, words kPer*part .. of each 4-word chunk
   constexpr uint32_t kWords = tc::kKBytes / 32;  // words per chunk
   constexpr uint32_t kSplit = tc::kThreads / tc::kM, kPer = kWords / kSplit;
-  const uint32_t sr = tid & (tc::kM - 1), part = tid / tc::kM, half = part;
+  static_assert(kSplit == 2 && kPer == 4, "two staging threads per row, 16 bytes each");
+  const uint32_t sr = (warp << 4) | (tid & 15u), part = (tid >> 4) & 1u;  // staging: row/class sr, words 4*part..+3
+  const uint32_t er = tid;                         // epilogue (tid < 128): TMEM lane = row er
   __shared__ uint32_t s_rowpop[tc::kM];
   if (tid < tc::kM) s_rowpop[tid] = 0;
+  __syncthreads();
   for (uint64_t it = blockIdx.x; it < nrt * nct; it += gridDim.x) {
     const uint32_t c0 = static_cast<uint32_t>(it % nct) * tc::kN;
     const uint64_t row0 = (it / nct) * tc::kM;
-    const uint64_t row = row0 + sr;
-    const bool rok = row < rows, cok = c0 + sr < C;
-    const uint32_t* rsrc = enc + (rok ? row : 0) * W;
-    const uint32_t* csrc = cv + static_cast<uint64_t>(cok ? c0 + sr : 0) * W;
+    const bool rok = row0 + sr < rows, cok = c0 + sr < C;
+    const uint32_t* rsrc = enc + (rok ? row0 + sr : 0) * W + kPer * part;
+    const uint32_t* csrc = cv + static_cast<uint64_t>(cok ? c0 + sr : 0) * W + kPer * part;
     uint32_t rowpop = 0;
     // packed words prefetched two chunks ahead (DRAM latency exceeds one chunk's staging + MMAs)
     uint32_t nx[2][kPer], ny[2][kPer];
     auto load = [&](uint32_t kc, uint32_t slot) {
+      const uint32_t w = kc * kWords;
+      if (VEC) {  // W % 4 == 0: the whole 16-byte half is in range or out of range
+        const bool in = w + kPer * part < W;
+        const uint4 x = (rok && in) ? __ldg(reinterpret_cast<const uint4*>(rsrc + w)) : make_uint4(0, 0, 0, 0);
+        const uint4 y = (cok && in) ? __ldg(reinterpret_cast<const uint4*>(csrc + w)) : make_uint4(0, 0, 0, 0);
+        nx[slot][0] = x.x, nx[slot][1] = x.y, nx[slot][2] = x.z, nx[slot][3] = x.w;
+        ny[slot][0] = y.x, ny[slot][1] = y.y, ny[slot][2] = y.z, ny[slot][3] = y.w;
+      } else {
 #pragma unroll
-      for (uint32_t i = 0; i < kPer; ++i) {
-        const uint32_t w = kc * kWords + kPer * part + i;
-        nx[slot][i] = (rok && w < W) ? __ldg(rsrc + w) : 0u;
-        ny[slot][i] = (cok && w < W) ? __ldg(csrc + w) : 0u;
+        for (uint32_t i = 0; i < kPer; ++i) {
+          const bool in = w + kPer * part + i < W;
+          nx[slot][i] = (rok && in) ? __ldg(rsrc + w + i) : 0u;
+          ny[slot][i] = (cok && in) ? __ldg(csrc + w + i) : 0u;
+        }
       }
     };
     load(0, 0);
@@ -379,8 +394,8 @@ __global__ void __launch_bounds__(tc::kThreads, 1) predict_tc_kernel(const uint3
 #pragma unroll
       for (uint32_t i = 0; i < kPer; ++i) {
         rowpop += __popc(cx[i]);
-        tc::stage_word(s.a[st], sr, kPer * part + i, cx[i]);
-        tc::stage_word(s.b[st], sr, kPer * part + i, cy[i]);
+        tc::stage_word(tc::smem_u32(s.a[st]), sr, kPer * part + i, cx[i]);
+        tc::stage_word(tc::smem_u32(s.b[st]), sr, kPer * part + i, cy[i]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core reads
       __syncthreads();
@@ -396,7 +411,9 @@ __global__ void __launch_bounds__(tc::kThreads, 1) predict_tc_kernel(const uint3
       }
       pending_bits |= 1u << st;
     }
-    if (part != 0) atomicAdd(&s_rowpop[sr], rowpop);
+    // |row|: the two staging threads of a row are lanes l and l+16
+    rowpop += __shfl_xor_sync(0xFFFFFFFFu, rowpop, 16);
+    if (part == 0) s_rowpop[sr] = rowpop;
     for (uint32_t st = 0; st < tc::kStages; ++st) {  // every MMA of the tile has landed in TMEM
       if ((pending_bits >> st) & 1u) {
         tc::mbar_wait(tc::smem_u32(&s.mbar[st]), (phase_bits >> st) & 1u);
@@ -407,41 +424,42 @@ __global__ void __launch_bounds__(tc::kThreads, 1) predict_tc_kernel(const uint3
     __syncthreads();  // s_rowpop
     asm volatile("tcgen05.fence::after_thread_sync;");
     // epilogue: warp w < 4 owns TMEM lanes (rows) 32w..32w+31; thread = row
-    unsigned long long key = ~0ull;
-    if (half == 0) rowpop += s_rowpop[sr];
-    __syncthreads();
-    if (tid < tc::kM) s_rowpop[tid] = 0;  // for the next tile (read above, before this barrier)
+    if (tid < tc::kM) {
+      const uint64_t row = row0 + er;
+      const bool eok = row < rows;
+      const uint32_t epop = s_rowpop[er];
+      unsigned long long key = ~0ull;
 #pragma unroll 1
-    for (uint32_t cb = 0; cb < (half == 0 ? tc::kN / 32 : 0u); ++cb) {
-      uint32_t v[32];
-      const uint32_t taddr = tmem + ((32u * warp) << 16) + 32u * cb;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (rok) {
+      for (uint32_t cb = 0; cb < tc::kN / 32; ++cb) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((32u * warp) << 16) + 32u * cb;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (eok) {
 #pragma unroll
-        for (uint32_t i = 0; i < 32; ++i) {
-          const uint32_t c = c0 + 32 * cb + i;
-          if (c < C) {
-            const uint32_t ham = rowpop + cpop[c] - 2u * v[i];
-            const unsigned long long k = (static_cast<unsigned long long>(ham) << 32) | c;
-            key = k < key ? k : key;
-            if (pops) pops[row * C + c] = ham;
-            if (dist) dist[row * C + c] = static_cast<double>(ham) / static_cast<double>(D);
+          for (uint32_t i = 0; i < 32; ++i) {
+            const uint32_t c = c0 + 32 * cb + i;
+            if (c < C) {
+              const uint32_t ham = epop + cpop[c] - 2u * v[i];
+              const unsigned long long k = (static_cast<unsigned long long>(ham) << 32) | c;
+              key = k < key ? k : key;
+              if (pops) pops[row * C + c] = ham;
+              if (dist) dist[row * C + c] = static_cast<double>(ham) / static_cast<double>(D);
+            }
           }
         }
       }
+      if (eok) atomicMin(best + row, key);
     }
-    (void)lane;
-    if (rok && half == 0) atomicMin(best + row, key);
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();  // TMEM is read before the next tile's first MMA overwrites it
+    __syncthreads();  // TMEM and s_rowpop are read before the next tile overwrites them
     asm volatile("tcgen05.fence::after_thread_sync;");
   }
   __syncthreads();
@@ -789,20 +807,20 @@ void predict_hamming_device(hv_context* ctx, cudaStream_t st, const uint32_t* cv
     class_popcount_kernel<<<grid_for(C, 8), 256, 0, st>>>(cv, static_cast<uint32_t>(C), static_cast<uint32_t>(W),
                                                           cpop.ptr);
     launched("class_popcount_kernel");
-    ck(cudaFuncSetAttribute(predict_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(tc::kSmemBytes)),
+    // 16-byte row loads when every row (and class) starts 16-byte aligned
+    const bool vec = W % 4 == 0 && (reinterpret_cast<uintptr_t>(enc) & 15u) == 0 &&
+                     (reinterpret_cast<uintptr_t>(cv) & 15u) == 0;
+    auto kern = vec ? predict_tc_kernel<true> : predict_tc_kernel<false>;
+    ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tc::kSmemBytes)),
        "cudaFuncSetAttribute");
-    ck(cudaFuncSetAttribute(predict_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
-       "cudaFuncSetAttribute");
+    ck(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "cudaFuncSetAttribute");
     const uint64_t items = ((rows + tc::kM - 1) / tc::kM) * ((C + tc::kN - 1) / tc::kN);
     int per_sm = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, predict_tc_kernel, tc::kThreads, tc::kSmemBytes),
-       "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tc::kThreads, tc::kSmemBytes), "occupancy");
     const unsigned g = static_cast<unsigned>(
         std::max<uint64_t>(1, std::min<uint64_t>(items, static_cast<uint64_t>(ctx->sm_count) * std::max(per_sm, 1))));
-    predict_tc_kernel<<<g, tc::kThreads, tc::kSmemBytes, st>>>(cv, static_cast<uint32_t>(C), static_cast<uint32_t>(D),
-                                                              static_cast<uint32_t>(W), enc, rows, cpop.ptr, best.ptr,
-                                                              dist, pops);
+    kern<<<g, tc::kThreads, tc::kSmemBytes, st>>>(cv, static_cast<uint32_t>(C), static_cast<uint32_t>(D),
+                                                 static_cast<uint32_t>(W), enc, rows, cpop.ptr, best.ptr, dist, pops);
     launched("predict_tc_kernel");
     if (labels) {
       best_to_labels_kernel<<<sgrid(ctx, rows, 256), 256, 0, st>>>(best.ptr, rows, labels);

@@ -35,8 +35,6 @@ struct MmaSmem {
 };
 constexpr size_t kMmaSmemBytes = sizeof(MmaSmem);
 
-// 4 bits -> 4 bytes of 0/1: bit i of the nibble lands in byte i
-__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
 __device__ __forceinline__ void mma_s8_16832(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                              uint32_t b0, uint32_t b1) {
@@ -46,11 +44,14 @@ __device__ __forceinline__ void mma_s8_16832(int (&c)[4], uint32_t a0, uint32_t 
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// one 32-bit word -> its 32 bytes (bit j -> byte j)
+// one 32-bit word -> 32 bytes of 0/1 in a strided K order (byte 4j + b holds
+// bit 8b + j); rows and classes use the same order, which the dot product
+// does not see
+__device__ __forceinline__ uint32_t spread_lane8(uint32_t x, uint32_t j) { return (x >> j) & 0x01010101u; }
 __device__ __forceinline__ void spread_word(uint32_t x, uint8_t* dst) {
   uint4* d = reinterpret_cast<uint4*>(dst);
-  d[0] = make_uint4(spread4(x & 0xFu), spread4((x >> 4) & 0xFu), spread4((x >> 8) & 0xFu), spread4((x >> 12) & 0xFu));
-  d[1] = make_uint4(spread4((x >> 16) & 0xFu), spread4((x >> 20) & 0xFu), spread4((x >> 24) & 0xFu), spread4(x >> 28));
+  d[0] = make_uint4(spread_lane8(x, 0), spread_lane8(x, 1), spread_lane8(x, 2), spread_lane8(x, 3));
+  d[1] = make_uint4(spread_lane8(x, 4), spread_lane8(x, 5), spread_lane8(x, 6), spread_lane8(x, 7));
 }
 
 // <row, class> for rows [row0, row0 + 128) x classes [c0, c0 + 128) over words

@@ -4,10 +4,10 @@
 //   popc(q ^ c) = |q| + |c| - 2 <q, c>
 //
 // CTA tile = 128 rows x 128 classes; the K dimension is the hypervector's bits,
-// 256 per chunk (8 words). 256 threads: thread t stages half of row t%128 and
-// of class t%128 — the packed words of the next chunk are loaded into
+// 256 per chunk (8 words). 256 threads: threads 2i and 2i+1 stage the two
+// halves of row i and of class i — the packed words of the next chunk are loaded into
 // registers while the current chunk's MMAs run, then every bit is spread to a
-// byte (0/1) and stored in the UMMA K-major no-swizzle layout (8-row x 16-byte core
+// byte (0/1, in a strided K order shared by both operands) and stored in the UMMA K-major no-swizzle layout (8-row x 16-byte core
 // matrices: LBO = 128 B along K, SBO = 1024 B along M/N). One elected thread
 // issues 4 tcgen05.mma (M=128, N=128, K=32 bytes each) per chunk and commits
 // them to the stage's mbarrier; the other stage is being refilled meanwhile.
@@ -24,7 +24,7 @@ constexpr int kM = 128, kN = 128;   // UMMA shape (rows x classes)
 constexpr int kKBytes = 256;        // K bytes (= bits) per chunk: 8 words
 constexpr int kStages = 2;
 constexpr int kThreads = 256;  // 2 staging threads per row/class; warps 0-3 read TMEM
-constexpr uint32_t kTileBytes = kM * kKBytes;  // 16 KB per operand and stage
+constexpr uint32_t kTileBytes = kM * kKBytes;  // 32 KB per operand and stage
 
 struct __align__(1024) Smem {
   uint8_t a[kStages][kTileBytes];
@@ -69,18 +69,27 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
       : "memory");
 }
 
-// 4 bits -> 4 bytes of 0/1: bit i of the nibble lands in byte i
-__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+// The dot product is invariant under any permutation of K applied to both
+// operands, so a 32-bit word is spread "strided": byte 4j + b of the word's
+// 32-byte K slice holds bit 8b + j, i.e. spread byte word j = (x >> j) &
+// 0x01010101 — 15 ALU ops per word instead of ~32 for bit k -> byte k. Rows and
+// classes are staged by the same function, so every (row, class) pair is
+// summed over the same bits.
+__device__ __forceinline__ uint32_t spread_lane(uint32_t x, uint32_t j) { return (x >> j) & 0x01010101u; }
 
-// one 32-bit word of row r -> bytes k = 32*kw .. 32*kw+31 of the chunk, in the
-// core-matrix layout: byte k of row r at (r/8)*kSbo + (k/16)*128 + (r%8)*16 + k%16
+// one 32-bit word of row r -> K bytes 32*kw .. 32*kw+31 of the chunk, in the
+// core-matrix layout: K byte k of row r at (r/8)*kSbo + (k/16)*128 + (r%8)*16 + k%16
 constexpr uint32_t kSbo = (kKBytes / 16) * 128;  // bytes between 8-row groups
-__device__ __forceinline__ void stage_word(uint8_t* tile, uint32_t r, uint32_t kw, uint32_t x) {
-  uint8_t* base = tile + (r >> 3) * kSbo + (r & 7u) * 16;
-  uint4* lo = reinterpret_cast<uint4*>(base + (2 * kw) * 128);
-  uint4* hi = reinterpret_cast<uint4*>(base + (2 * kw + 1) * 128);
-  *lo = make_uint4(spread4(x & 0xFu), spread4((x >> 4) & 0xFu), spread4((x >> 8) & 0xFu), spread4((x >> 12) & 0xFu));
-  *hi = make_uint4(spread4((x >> 16) & 0xFu), spread4((x >> 20) & 0xFu), spread4((x >> 24) & 0xFu), spread4(x >> 28));
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+// tile = shared-window address of the operand tile (the extern array is
+// re-aligned through a generic pointer, so plain C++ stores would compile to
+// generic ST instead of STS)
+__device__ __forceinline__ void stage_word(uint32_t tile, uint32_t r, uint32_t kw, uint32_t x) {
+  const uint32_t base = tile + (r >> 3) * kSbo + (r & 7u) * 16 + 2 * kw * 128;
+  sts128(base, spread_lane(x, 0), spread_lane(x, 1), spread_lane(x, 2), spread_lane(x, 3));
+  sts128(base + 128, spread_lane(x, 4), spread_lane(x, 5), spread_lane(x, 6), spread_lane(x, 7));
 }
 
 }  // namespace tc
