@@ -181,6 +181,10 @@ bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
 
 // Online training, Hamming metric: every batch in one persistent cooperative
 // kernel (hv_online.cu); acc/weight/counts/cv hold the bootstrap state.
+// tcgen05 many-class scan (hv_predict_tc.cu): fills best[] (argmin keys, pre-set
+// to ~0) and the optional dist / pops; false when enc is not 16-byte aligned.
+bool predict_tc_launch(hv_context* ctx, cudaStream_t st, const uint32_t* cv, size_t C, size_t D, const uint32_t* enc,
+                       size_t rows, const uint32_t* cpop, unsigned long long* best, double* dist, uint32_t* pops);
 void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* enc, size_t rows, size_t D,
                              const int32_t* labels, size_t C, size_t bsz, double gamma, const uint32_t* tie,
                              double* acc, double* weight, uint64_t* counts, uint32_t* cv);

@@ -293,179 +293,6 @@ __global__ void __launch_bounds__(kMmaThreads) predict_imma_kernel(const uint32_
   }
 }
 
-// tcgen05 variant (hv_scan_tc.cuh): 128 rows x 128 classes per tile, the dot
-// products accumulated in TMEM by single-thread-issued UMMAs. Lanes l and l+16
-// of a warp load the two 16-byte halves of one row's (class's) 32-byte chunk
-// sector, so a warp's load touches 16 sectors instead of 32 (VEC: one 16-byte
-// load per thread when rows are 16-byte aligned, W % 4 == 0), and each
-// quarter-warp's 16-byte shared stores hit 8 distinct rows (conflict-free).
-template <bool VEC>
-__global__ void __launch_bounds__(tc::kThreads, 1) predict_tc_kernel(const uint32_t* __restrict__ cv, uint32_t C,
-                                                                     uint32_t D, uint32_t W,
-                                                                     const uint32_t* __restrict__ enc, uint64_t rows,
-                                                                     const uint32_t* __restrict__ cpop,
-                                                                     unsigned long long* __restrict__ best,
-                                                                     double* __restrict__ dist,
-                                                                     uint32_t* __restrict__ pops) {
-  extern __shared__ uint8_t tc_raw[];
-  tc::Smem& s = *reinterpret_cast<tc::Smem*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t tid = threadIdx.x, warp = tid >> 5;
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&s.tmem)),
-                 "n"(tc::kN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    for (int st = 0; st < tc::kStages; ++st) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_u32(&s.mbar[st])));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = s.tmem;
-  const uint32_t nct = (C + tc::kN - 1) / tc::kN;
-  const uint64_t nrt = (rows + tc::kM - 1) / tc::kM;
-  const uint32_t nchunks = (W + tc::kKBytes / 32 - 1) / (tc::kKBytes / 32);
-  // per-stage mbarrier phase and "MMAs outstanding" as register bit masks
-  // (indexed arrays would live in local memory)
-  uint32_t phase_bits = 0, pending_bits = 0;
-  uint32_t g = 0;  // global chunk counter (stage = g & 1)
-  constexpr uint32_t kWords = tc::kKBytes / 32;  // words per chunk
-  constexpr uint32_t kSplit = tc::kThreads / tc::kM, kPer = kWords / kSplit;
-  static_assert(kSplit == 2 && kPer == 4, "two staging threads per row, 16 bytes each");
-  const uint32_t sr = (warp << 4) | (tid & 15u), part = (tid >> 4) & 1u;  // staging: row/class sr, words 4*part..+3
-  const uint32_t er = tid;                         // epilogue (tid < 128): TMEM lane = row er
-  __shared__ uint32_t s_rowpop[tc::kM];
-  if (tid < tc::kM) s_rowpop[tid] = 0;
-  __syncthreads();
-  for (uint64_t it = blockIdx.x; it < nrt * nct; it += gridDim.x) {
-    const uint32_t c0 = static_cast<uint32_t>(it % nct) * tc::kN;
-    const uint64_t row0 = (it / nct) * tc::kM;
-    const bool rok = row0 + sr < rows, cok = c0 + sr < C;
-    const uint32_t* rsrc = enc + (rok ? row0 + sr : 0) * W + kPer * part;
-    const uint32_t* csrc = cv + static_cast<uint64_t>(cok ? c0 + sr : 0) * W + kPer * part;
-    uint32_t rowpop = 0;
-    // packed words prefetched two chunks ahead (DRAM latency exceeds one chunk's staging + MMAs)
-    uint32_t nx[2][kPer], ny[2][kPer];
-    auto load = [&](uint32_t kc, uint32_t slot) {
-      const uint32_t w = kc * kWords;
-      if (VEC) {  // W % 4 == 0: the whole 16-byte half is in range or out of range
-        const bool in = w + kPer * part < W;
-        const uint4 x = (rok && in) ? __ldg(reinterpret_cast<const uint4*>(rsrc + w)) : make_uint4(0, 0, 0, 0);
-        const uint4 y = (cok && in) ? __ldg(reinterpret_cast<const uint4*>(csrc + w)) : make_uint4(0, 0, 0, 0);
-        nx[slot][0] = x.x, nx[slot][1] = x.y, nx[slot][2] = x.z, nx[slot][3] = x.w;
-        ny[slot][0] = y.x, ny[slot][1] = y.y, ny[slot][2] = y.z, ny[slot][3] = y.w;
-      } else {
-#pragma unroll
-        for (uint32_t i = 0; i < kPer; ++i) {
-          const bool in = w + kPer * part + i < W;
-          nx[slot][i] = (rok && in) ? __ldg(rsrc + w + i) : 0u;
-          ny[slot][i] = (cok && in) ? __ldg(csrc + w + i) : 0u;
-        }
-      }
-    };
-    load(0, 0);
-    if (nchunks > 1) load(1, 1);
-    for (uint32_t kc = 0; kc < nchunks; ++kc, ++g) {
-      const uint32_t st = g & 1u;
-      uint32_t cx[kPer], cy[kPer];
-      if (kc & 1u) {
-#pragma unroll
-        for (uint32_t i = 0; i < kPer; ++i) {
-          cx[i] = nx[1][i];
-          cy[i] = ny[1][i];
-        }
-        if (kc + 2 < nchunks) load(kc + 2, 1);
-      } else {
-#pragma unroll
-        for (uint32_t i = 0; i < kPer; ++i) {
-          cx[i] = nx[0][i];
-          cy[i] = ny[0][i];
-        }
-        if (kc + 2 < nchunks) load(kc + 2, 0);
-      }
-      if ((pending_bits >> st) & 1u) {  // the MMAs that last read this stage are done
-        tc::mbar_wait(tc::smem_u32(&s.mbar[st]), (phase_bits >> st) & 1u);
-        phase_bits ^= 1u << st;
-        pending_bits &= ~(1u << st);
-      }
-#pragma unroll
-      for (uint32_t i = 0; i < kPer; ++i) {
-        rowpop += __popc(cx[i]);
-        tc::stage_word(tc::smem_u32(s.a[st]), sr, kPer * part + i, cx[i]);
-        tc::stage_word(tc::smem_u32(s.b[st]), sr, kPer * part + i, cy[i]);
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> tensor core reads
-      __syncthreads();
-      if (tid == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t a0 = tc::smem_u32(s.a[st]), b0 = tc::smem_u32(s.b[st]);
-#pragma unroll
-        for (uint32_t j = 0; j < kWords; ++j) {
-          tc::mma_i8(tmem, tc::make_desc(a0 + 256 * j, 128, tc::kSbo), tc::make_desc(b0 + 256 * j, 128, tc::kSbo),
-                     (kc | j) != 0 ? 1u : 0u);
-        }
-        tc::commit(tc::smem_u32(&s.mbar[st]));
-      }
-      pending_bits |= 1u << st;
-    }
-    // |row|: the two staging threads of a row are lanes l and l+16
-    rowpop += __shfl_xor_sync(0xFFFFFFFFu, rowpop, 16);
-    if (part == 0) s_rowpop[sr] = rowpop;
-    for (uint32_t st = 0; st < tc::kStages; ++st) {  // every MMA of the tile has landed in TMEM
-      if ((pending_bits >> st) & 1u) {
-        tc::mbar_wait(tc::smem_u32(&s.mbar[st]), (phase_bits >> st) & 1u);
-        phase_bits ^= 1u << st;
-        pending_bits &= ~(1u << st);
-      }
-    }
-    __syncthreads();  // s_rowpop
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    // epilogue: warp w < 4 owns TMEM lanes (rows) 32w..32w+31; thread = row
-    if (tid < tc::kM) {
-      const uint64_t row = row0 + er;
-      const bool eok = row < rows;
-      const uint32_t epop = s_rowpop[er];
-      unsigned long long key = ~0ull;
-#pragma unroll 1
-      for (uint32_t cb = 0; cb < tc::kN / 32; ++cb) {
-        uint32_t v[32];
-        const uint32_t taddr = tmem + ((32u * warp) << 16) + 32u * cb;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (eok) {
-#pragma unroll
-          for (uint32_t i = 0; i < 32; ++i) {
-            const uint32_t c = c0 + 32 * cb + i;
-            if (c < C) {
-              const uint32_t ham = epop + cpop[c] - 2u * v[i];
-              const unsigned long long k = (static_cast<unsigned long long>(ham) << 32) | c;
-              key = k < key ? k : key;
-              if (pops) pops[row * C + c] = ham;
-              if (dist) dist[row * C + c] = static_cast<double>(ham) / static_cast<double>(D);
-            }
-          }
-        }
-      }
-      if (eok) atomicMin(best + row, key);
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();  // TMEM and s_rowpop are read before the next tile overwrites them
-    asm volatile("tcgen05.fence::after_thread_sync;");
-  }
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(tc::kN));
-}
-
 __global__ void best_to_labels_kernel(const unsigned long long* __restrict__ best, uint64_t rows,
                                       int32_t* __restrict__ labels) {
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows; r += (uint64_t)gridDim.x * blockDim.x) {
@@ -807,21 +634,17 @@ void predict_hamming_device(hv_context* ctx, cudaStream_t st, const uint32_t* cv
     class_popcount_kernel<<<grid_for(C, 8), 256, 0, st>>>(cv, static_cast<uint32_t>(C), static_cast<uint32_t>(W),
                                                           cpop.ptr);
     launched("class_popcount_kernel");
-    // 16-byte row loads when every row (and class) starts 16-byte aligned
-    const bool vec = W % 4 == 0 && (reinterpret_cast<uintptr_t>(enc) & 15u) == 0 &&
-                     (reinterpret_cast<uintptr_t>(cv) & 15u) == 0;
-    auto kern = vec ? predict_tc_kernel<true> : predict_tc_kernel<false>;
-    ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tc::kSmemBytes)),
-       "cudaFuncSetAttribute");
-    ck(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "cudaFuncSetAttribute");
-    const uint64_t items = ((rows + tc::kM - 1) / tc::kM) * ((C + tc::kN - 1) / tc::kN);
-    int per_sm = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tc::kThreads, tc::kSmemBytes), "occupancy");
-    const unsigned g = static_cast<unsigned>(
-        std::max<uint64_t>(1, std::min<uint64_t>(items, static_cast<uint64_t>(ctx->sm_count) * std::max(per_sm, 1))));
-    kern<<<g, tc::kThreads, tc::kSmemBytes, st>>>(cv, static_cast<uint32_t>(C), static_cast<uint32_t>(D),
-                                                 static_cast<uint32_t>(W), enc, rows, cpop.ptr, best.ptr, dist, pops);
-    launched("predict_tc_kernel");
+    if (!predict_tc_launch(ctx, st, cv, C, D, enc, rows, cpop.ptr, best.ptr, dist, pops)) {
+      ck(cudaFuncSetAttribute(predict_imma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(kMmaSmemBytes)),
+         "cudaFuncSetAttribute");
+      const uint64_t items = ((rows + kMmaRows - 1) / kMmaRows) * ((C + kMmaCls - 1) / kMmaCls);
+      const unsigned g = static_cast<unsigned>(std::min<uint64_t>(items, ctx->sm_count * 2ull));
+      predict_imma_kernel<<<g, kMmaThreads, kMmaSmemBytes, st>>>(cv, static_cast<uint32_t>(C),
+                                                                 static_cast<uint32_t>(D), static_cast<uint32_t>(W),
+                                                                 enc, rows, cpop.ptr, best.ptr, dist, pops);
+      launched("predict_imma_kernel");
+    }
     if (labels) {
       best_to_labels_kernel<<<sgrid(ctx, rows, 256), 256, 0, st>>>(best.ptr, rows, labels);
       launched("best_to_labels_kernel");

@@ -1,0 +1,349 @@
+// hv_predict_tc.cu — the many-class Hamming scan (model.cpp:69-79, 96-104,
+// 303-320) on the 5th-generation tensor cores, rows in TMEM.
+//
+//   popc(q ^ c) = |q| + |c| - 2 <q, c>
+//
+// <q, c> is a 0/1 GEMM, rows x D times D x classes, computed with
+// tcgen05.mma kind::i8 (u8 operands holding 0/1, exact s32 accumulation).
+// A CTA owns a PAIR of 128-row tiles against one class tile of N <= 128
+// classes, two accumulators in TMEM (2 x 128 columns). The K dimension is the
+// hypervector's bits, 256 per chunk (8 packed words).
+//
+//   * classes (B operand): spread once per call by tc_arrange_classes_kernel
+//     into the exact shared-memory image the UMMA descriptor reads (K-major,
+//     no swizzle, 8 x 16-byte core matrices), one 32 KB image per (class tile,
+//     chunk); the CTA fetches it with one cp.async.bulk per chunk (async proxy,
+//     completion through the stage's mbarrier transaction count);
+//   * rows (A operand): 4 loader warps keep kRing chunks of packed rows in
+//     flight with 16-byte cp.async into a shared ring; 8 spreader warps (one
+//     thread per row) turn a row's 8 words into 64 byte-columns and write them
+//     straight into TMEM with tcgen05.st — the MMA reads A from TMEM, so no
+//     generic-proxy shared store (and no per-chunk proxy fence, whose MEMBAR
+//     dominated the shared-memory-staged kernel) sits on the critical path;
+//   * one elected thread issues 2 x 8 UMMAs per chunk and commits them to the
+//     stage's mbarrier, which frees both the TMEM A stage and the B stage;
+//   * the epilogue reads the s32 dot products out of TMEM (tcgen05.ld 32x32b,
+//     thread = row) and folds |q| + |c| - 2<q,c> into the (distance, class)
+//     argmin key exactly like the other scans.
+//
+// The bit -> byte spread is "strided" (byte 4j + b of a word's 32-byte K slice
+// holds bit 8b + j); rows and classes use the same order, which the dot
+// product does not see.
+#include <cstdint>
+#include <cstdlib>
+
+#include "hv_internal.cuh"
+#include "hv_scan_tc.cuh"
+
+namespace hvb {
+namespace {
+
+constexpr uint32_t kWords = tc::kKBytes / 32;  // packed words per chunk (8)
+constexpr uint32_t kRows = 2 * tc::kM;        // rows per CTA work item (two accumulators)
+constexpr int kRing = 8;                       // raw row chunks in flight
+constexpr int kSpread = 256, kLoad = 128, kThreads = kSpread + kLoad + 32;  // + 1 class-image warp
+constexpr uint32_t kWin = 12;                  // words per raw row slot: 8 + alignment window
+constexpr uint32_t kImg = tc::kN * tc::kKBytes;  // class image bytes per (tile, chunk)
+// TMEM columns: accumulators [0, 128) and [128, 256); A stages at 256 + 64 * (2 * stage + tile)
+constexpr uint32_t kTmemCols = 512, kAcol = 256, kAcols = tc::kKBytes / 4;
+
+struct __align__(1024) Smem {
+  uint8_t b[tc::kStages][kImg];
+  uint32_t raw[kRing][kRows][kWin];
+  unsigned long long mma_done[tc::kStages], b_full[tc::kStages];
+  unsigned long long raw_full[kRing], raw_empty[kRing];
+  uint32_t tmem;
+};
+constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
+
+__device__ __forceinline__ uint32_t spread(uint32_t x, uint32_t j) { return (x >> j) & 0x01010101u; }
+
+__device__ __forceinline__ void mma_i8_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+// 32 columns of this warp's 32 TMEM lanes from v[0..31] (thread = lane)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]),
+      "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),
+      "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
+// classes -> UMMA B images: img[(ct * nchunks + kc)] holds classes ct*128 ..
+// +127, K bytes of chunk kc, in the core-matrix layout of tc::stage_word.
+__global__ void tc_arrange_classes_kernel(const uint32_t* __restrict__ cv, uint32_t C, uint32_t W, uint32_t nct,
+                                          uint32_t nchunks, uint8_t* __restrict__ img) {
+  const uint64_t total = static_cast<uint64_t>(nct) * nchunks * tc::kN * kWords;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t kw = static_cast<uint32_t>(i % kWords);
+    const uint32_t c = static_cast<uint32_t>((i / kWords) % tc::kN);
+    const uint64_t tk = i / (kWords * tc::kN);  // ct * nchunks + kc
+    const uint32_t kc = static_cast<uint32_t>(tk % nchunks), ct = static_cast<uint32_t>(tk / nchunks);
+    const uint32_t cls = ct * tc::kN + c, w = kc * kWords + kw;
+    const uint32_t x = (cls < C && w < W) ? cv[static_cast<uint64_t>(cls) * W + w] : 0u;
+    uint4* dst = reinterpret_cast<uint4*>(img + tk * kImg + (c >> 3) * tc::kSbo + (c & 7u) * 16 + 2 * kw * 128);
+    dst[0] = make_uint4(spread(x, 0), spread(x, 1), spread(x, 2), spread(x, 3));
+    dst[8] = make_uint4(spread(x, 4), spread(x, 5), spread(x, 6), spread(x, 7));  // +128 bytes
+  }
+}
+
+// ALIGNED: every row starts 16-byte aligned (W % 4 == 0); otherwise each raw
+// slot holds the 16-byte-aligned 48-byte window around the row's chunk and
+// the spreader picks its 8 words at the row's word offset.
+template <bool ALIGNED>
+__global__ void __launch_bounds__(kThreads, 1)
+    predict_tc_kernel(const uint8_t* __restrict__ img, uint32_t C, uint32_t N, uint32_t D, uint32_t W,
+                      const uint32_t* __restrict__ enc, uint64_t rows, const uint32_t* __restrict__ cpop,
+                      unsigned long long* __restrict__ best, double* __restrict__ dist, uint32_t* __restrict__ pops) {
+  extern __shared__ uint8_t tc_raw[];
+  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&s.tmem)),
+                 "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int st = 0; st < tc::kStages; ++st) {
+      tc::mbar_init(tc::smem_u32(&s.mma_done[st]), 1);
+      tc::mbar_init(tc::smem_u32(&s.b_full[st]), 1);
+    }
+    for (int r = 0; r < kRing; ++r) {
+      tc::mbar_init(tc::smem_u32(&s.raw_full[r]), kLoad);
+      tc::mbar_init(tc::smem_u32(&s.raw_empty[r]), kSpread / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = s.tmem;
+  const uint32_t nct = (C + tc::kN - 1) / tc::kN;
+  const uint64_t npairs = (rows + kRows - 1) / kRows;
+  const uint32_t nchunks = (W + kWords - 1) / kWords;
+  const uint64_t items = npairs * nct;
+  if (warp == (kSpread + kLoad) / 32) {
+    // ---- class images: one cp.async.bulk per chunk into B stage gch & 1, once its last MMAs are done
+    if (lane == 0) {
+      uint32_t gch = 0, mma_phase = 0, pending = 0;
+      for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const uint8_t* bimg = img + static_cast<uint64_t>(it % nct) * nchunks * kImg;
+        for (uint32_t kc = 0; kc < nchunks; ++kc, ++gch) {
+          const uint32_t st = gch & 1u;
+          if ((pending >> st) & 1u) {
+            tc::mbar_wait(tc::smem_u32(&s.mma_done[st]), (mma_phase >> st) & 1u);
+            mma_phase ^= 1u << st;
+          }
+          pending |= 1u << st;
+          bulk_g2s(tc::smem_u32(s.b[st]), bimg + static_cast<uint64_t>(kc) * kImg, N * tc::kKBytes,
+                   tc::smem_u32(&s.b_full[st]));
+        }
+      }
+    }
+  } else if (warp >= kSpread / 32) {
+    // ---- row loaders: thread t copies rows t and t + 128 of the pair
+    const uint32_t t = tid - kSpread;
+    uint32_t gch = 0;
+    for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      const uint64_t row0 = (it / nct) * kRows;
+      const uint32_t* src[2];
+      bool ok[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint64_t row = row0 + t + h * tc::kM;
+        ok[h] = row < rows;
+        src[h] = enc + (ok[h] ? row : 0) * W;
+      }
+      for (uint32_t kc = 0; kc < nchunks; ++kc, ++gch) {
+        const uint32_t r = gch % kRing, ph = (gch / kRing) & 1u;
+        tc::mbar_wait(tc::smem_u32(&s.raw_empty[r]), ph ^ 1u);
+        const uint32_t w = kc * kWords;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t dst = tc::smem_u32(&s.raw[r][t + h * tc::kM][0]);
+          if (ALIGNED) {
+#pragma unroll
+            for (uint32_t q = 0; q < 2; ++q) {
+              const bool in = ok[h] && w + 4 * q < W;
+              tc::cp_async16(dst + 16 * q, src[h] + (in ? w + 4 * q : 0), in ? 16u : 0u);
+            }
+          } else {
+            // 48-byte window from the 16-byte boundary at or below word w of the row,
+            // clamped to the row's end (bytes past it are zero-filled, never read)
+            const uintptr_t a = reinterpret_cast<uintptr_t>(src[h] + w);
+            const uintptr_t a16 = a & ~uintptr_t(15), end = reinterpret_cast<uintptr_t>(src[h] + W);
+#pragma unroll
+            for (uint32_t q = 0; q < 3; ++q) {
+              const uintptr_t p = a16 + 16 * q;
+              const uint32_t n = (!ok[h] || w >= W || p >= end) ? 0u : (end - p >= 16 ? 16u : static_cast<uint32_t>(end - p));
+              tc::cp_async16(dst + 16 * q, n ? reinterpret_cast<const void*>(p) : src[h], n);
+            }
+          }
+        }
+        tc::cp_async_arrive(tc::smem_u32(&s.raw_full[r]));
+      }
+    }
+  } else {
+    // ---- spreaders: warp w owns TMEM lanes 32(w%4).. of tile w/4; thread = row
+    const uint32_t tile = warp >> 2, lrow = ((warp & 3u) << 5) | lane, prow = tile * tc::kM + lrow;
+    const uint32_t lane_base = (warp & 3u) << 21;  // (32 * (w % 4)) << 16
+    const uint32_t idesc = (2u << 4) | ((N >> 3) << 17) | ((static_cast<uint32_t>(tc::kM) >> 4) << 24);
+    uint32_t mma_phase = 0, pending = 0, b_phase = 0;
+    uint32_t gch = 0;
+    for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
+      const uint32_t c0 = static_cast<uint32_t>(it % nct) * tc::kN;
+      const uint64_t row0 = (it / nct) * kRows;
+      const uint64_t row = row0 + prow;
+      uint32_t mis = 0;
+      if (!ALIGNED) mis = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(enc + (row < rows ? row : 0) * W) >> 2) & 3u);
+      uint32_t rowpop = 0;
+      for (uint32_t kc = 0; kc < nchunks; ++kc, ++gch) {
+        const uint32_t r = gch % kRing, ph = (gch / kRing) & 1u, st = gch & 1u;
+        tc::mbar_wait(tc::smem_u32(&s.raw_full[r]), ph);
+        uint32_t x[kWords];
+        const uint32_t base = tc::smem_u32(&s.raw[r][prow][0]);
+        if (ALIGNED) {
+          const uint4 u = tc::lds128(base), v = tc::lds128(base + 16);
+          x[0] = u.x, x[1] = u.y, x[2] = u.z, x[3] = u.w, x[4] = v.x, x[5] = v.y, x[6] = v.z, x[7] = v.w;
+        } else {
+          const uint4 u = tc::lds128(base), v = tc::lds128(base + 16), z = tc::lds128(base + 32);
+          const uint32_t win[12] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w, z.x, z.y, z.z, z.w};
+#pragma unroll
+          for (uint32_t i = 0; i < kWords; ++i) {
+            x[i] = mis == 0 ? win[i] : mis == 1 ? win[i + 1] : mis == 2 ? win[i + 2] : win[i + 3];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s.raw_empty[r]));  // release orders the reads above
+#pragma unroll
+        for (uint32_t i = 0; i < kWords; ++i) rowpop += __popc(x[i]);
+        if ((pending >> st) & 1u) {  // the MMAs that last read this A stage are done
+          tc::mbar_wait(tc::smem_u32(&s.mma_done[st]), (mma_phase >> st) & 1u);
+          mma_phase ^= 1u << st;
+        }
+        pending |= 1u << st;
+        const uint32_t acol = kAcol + kAcols * (2 * st + tile);
+#pragma unroll
+        for (uint32_t hw = 0; hw < 2; ++hw) {  // words 4hw..4hw+3 -> columns 32hw..32hw+31
+          uint32_t v[32];
+#pragma unroll
+          for (uint32_t i = 0; i < 4; ++i)
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) v[8 * i + j] = spread(x[4 * hw + i], j);
+          tmem_st32(tmem + lane_base + acol + 32 * hw, v);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        asm volatile("bar.sync 1, %0;" ::"n"(kSpread) : "memory");
+        if (tid == 0) {
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          tc::mbar_wait(tc::smem_u32(&s.b_full[st]), (b_phase >> st) & 1u);
+          b_phase ^= 1u << st;
+          const uint32_t b0 = tc::smem_u32(s.b[st]);
+#pragma unroll
+          for (uint32_t j = 0; j < kWords; ++j) {  // K = 32 bytes per UMMA: 8 A columns, 256 B of image
+            const uint64_t bd = tc::make_desc(b0 + 256 * j, 128, tc::kSbo);
+            const uint32_t acc = (kc | j) != 0 ? 1u : 0u;
+            mma_i8_ts(tmem, tmem + kAcol + kAcols * (2 * st + 0) + 8 * j, bd, idesc, acc);
+            mma_i8_ts(tmem + tc::kN, tmem + kAcol + kAcols * (2 * st + 1) + 8 * j, bd, idesc, acc);
+          }
+          tc::commit(tc::smem_u32(&s.mma_done[st]));
+        }
+      }
+      // every MMA of the pair has landed in TMEM
+      for (uint32_t st = 0; st < tc::kStages; ++st) {
+        if ((pending >> st) & 1u) {
+          tc::mbar_wait(tc::smem_u32(&s.mma_done[st]), (mma_phase >> st) & 1u);
+          mma_phase ^= 1u << st;
+        }
+      }
+      pending = 0;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      // epilogue: thread = row of its tile; accumulator columns 128 * tile ..
+      const bool eok = row < rows;
+      unsigned long long key = ~0ull;
+#pragma unroll 1
+      for (uint32_t cb = 0; cb < tc::kN / 32; ++cb) {
+        if (32 * cb >= N) break;  // warp-uniform
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_base + tc::kN * tile + 32 * cb, v);
+        if (eok) {
+#pragma unroll
+          for (uint32_t i = 0; i < 32; ++i) {
+            const uint32_t c = c0 + 32 * cb + i;
+            if (c < C) {
+              const uint32_t ham = rowpop + cpop[c] - 2u * v[i];
+              const unsigned long long k = (static_cast<unsigned long long>(ham) << 32) | c;
+              key = k < key ? k : key;
+              if (pops) pops[row * C + c] = ham;
+              if (dist) dist[row * C + c] = static_cast<double>(ham) / static_cast<double>(D);
+            }
+          }
+        }
+      }
+      if (eok) atomicMin(best + row, key);
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      asm volatile("bar.sync 1, %0;" ::"n"(kSpread) : "memory");  // accumulators read before the next pair
+      asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
+}
+
+}  // namespace
+
+bool predict_tc_launch(hv_context* ctx, cudaStream_t st, const uint32_t* cv, size_t C, size_t D, const uint32_t* enc,
+                       size_t rows, const uint32_t* cpop, unsigned long long* best, double* dist, uint32_t* pops) {
+  const size_t W = words_per_row(D);
+  if ((reinterpret_cast<uintptr_t>(enc) & 15u) != 0) return false;  // the 16-byte copy windows need it
+  const uint32_t nct = static_cast<uint32_t>((C + tc::kN - 1) / tc::kN);
+  const uint32_t nchunks = static_cast<uint32_t>((W + kWords - 1) / kWords);
+  // N: classes per UMMA, a multiple of 16 covering one class tile
+  const uint32_t N = C >= tc::kN ? tc::kN : static_cast<uint32_t>((C + 15) / 16 * 16);
+  DevBuf<uint8_t> img(static_cast<size_t>(nct) * nchunks * kImg, st);
+  const uint64_t work = static_cast<uint64_t>(nct) * nchunks * tc::kN * kWords;
+  tc_arrange_classes_kernel<<<grid_for(work, 256, ctx->sm_count * 8), 256, 0, st>>>(
+      cv, static_cast<uint32_t>(C), static_cast<uint32_t>(W), nct, nchunks, img.ptr);
+  launched("tc_arrange_classes_kernel");
+  const bool aligned = W % 4 == 0;
+  auto kern = aligned ? predict_tc_kernel<true> : predict_tc_kernel<false>;
+  ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)),
+     "cudaFuncSetAttribute");
+  const uint64_t items = ((rows + kRows - 1) / kRows) * nct;
+  const unsigned g = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(items, ctx->sm_count)));
+  kern<<<g, kThreads, kSmemBytes, st>>>(img.ptr, static_cast<uint32_t>(C), N, static_cast<uint32_t>(D),
+                                        static_cast<uint32_t>(W), enc, rows, cpop, best, dist, pops);
+  launched("predict_tc_kernel");
+  return true;
+}
+
+}  // namespace hvb
