@@ -20,8 +20,11 @@
 //     straight into TMEM with tcgen05.st — the MMA reads A from TMEM, so no
 //     generic-proxy shared store (and no per-chunk proxy fence, whose MEMBAR
 //     dominated the shared-memory-staged kernel) sits on the critical path;
-//   * one elected thread issues 2 x 8 UMMAs per chunk and commits them to the
-//     stage's mbarrier, which frees both the TMEM A stage and the B stage;
+//   * a dedicated MMA warp (one thread) waits for the stage's rows (an
+//     mbarrier the 8 spreader warps arrive on after tcgen05.st) and class
+//     image, issues 2 x 8 UMMAs and commits them to the stage's mbarrier,
+//     which frees both the TMEM A stage and the B stage — no CTA-wide barrier
+//     in the steady state;
 //   * the epilogue reads the s32 dot products out of TMEM (tcgen05.ld 32x32b,
 //     thread = row) and folds |q| + |c| - 2<q,c> into the (distance, class)
 //     argmin key exactly like the other scans.
@@ -41,7 +44,8 @@ namespace {
 constexpr uint32_t kWords = tc::kKBytes / 32;  // packed words per chunk (8)
 constexpr uint32_t kRows = 2 * tc::kM;        // rows per CTA work item (two accumulators)
 constexpr int kRing = 8;                       // raw row chunks in flight
-constexpr int kSpread = 256, kLoad = 128, kThreads = kSpread + kLoad + 32;  // + 1 class-image warp
+constexpr int kSpread = 256, kLoad = 128, kThreads = kSpread + kLoad + 64;  // + class-image warp + MMA warp
+constexpr uint32_t kImgWarp = (kSpread + kLoad) / 32, kMmaWarp = kImgWarp + 1;
 constexpr uint32_t kWin = 12;                  // words per raw row slot: 8 + alignment window
 constexpr uint32_t kImg = tc::kN * tc::kKBytes;  // class image bytes per (tile, chunk)
 // TMEM columns: accumulators [0, 128) and [128, 256); A stages at 256 + 64 * (2 * stage + tile)
@@ -50,7 +54,7 @@ constexpr uint32_t kTmemCols = 512, kAcol = 256, kAcols = tc::kKBytes / 4;
 struct __align__(1024) Smem {
   uint8_t b[tc::kStages][kImg];
   uint32_t raw[kRing][kRows][kWin];
-  unsigned long long mma_done[tc::kStages], b_full[tc::kStages];
+  unsigned long long mma_done[tc::kStages], b_full[tc::kStages], a_full[tc::kStages], acc_empty;
   unsigned long long raw_full[kRing], raw_empty[kRing];
   uint32_t tmem;
 };
@@ -135,7 +139,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int st = 0; st < tc::kStages; ++st) {
       tc::mbar_init(tc::smem_u32(&s.mma_done[st]), 1);
       tc::mbar_init(tc::smem_u32(&s.b_full[st]), 1);
+      tc::mbar_init(tc::smem_u32(&s.a_full[st]), kSpread / 32);
     }
+    tc::mbar_init(tc::smem_u32(&s.acc_empty), kSpread / 32);
     for (int r = 0; r < kRing; ++r) {
       tc::mbar_init(tc::smem_u32(&s.raw_full[r]), kLoad);
       tc::mbar_init(tc::smem_u32(&s.raw_empty[r]), kSpread / 32);
@@ -150,7 +156,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint64_t npairs = (rows + kRows - 1) / kRows;
   const uint32_t nchunks = (W + kWords - 1) / kWords;
   const uint64_t items = npairs * nct;
-  if (warp == (kSpread + kLoad) / 32) {
+  if (warp == kMmaWarp) {
+    // ---- MMA issue: one thread; per chunk 2 x 8 UMMAs (A = the stage's TMEM rows, B = its class image)
+    if (lane == 0) {
+      const uint32_t idesc = (2u << 4) | ((N >> 3) << 17) | ((static_cast<uint32_t>(tc::kM) >> 4) << 24);
+      uint32_t gch = 0, a_phase = 0, b_phase = 0, pair = 0;
+      for (uint64_t it = blockIdx.x; it < items; it += gridDim.x, ++pair) {
+        if (pair > 0) {  // the previous pair's epilogue has read the accumulators
+          tc::mbar_wait(tc::smem_u32(&s.acc_empty), (pair - 1) & 1u);
+        }
+        for (uint32_t kc = 0; kc < nchunks; ++kc, ++gch) {
+          const uint32_t st = gch & 1u;
+          tc::mbar_wait(tc::smem_u32(&s.a_full[st]), (a_phase >> st) & 1u);
+          a_phase ^= 1u << st;
+          tc::mbar_wait(tc::smem_u32(&s.b_full[st]), (b_phase >> st) & 1u);
+          b_phase ^= 1u << st;
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t b0 = tc::smem_u32(s.b[st]);
+#pragma unroll
+          for (uint32_t j = 0; j < kWords; ++j) {  // K = 32 bytes per UMMA: 8 A columns, 256 B of image
+            const uint64_t bd = tc::make_desc(b0 + 256 * j, 128, tc::kSbo);
+            const uint32_t acc = (kc | j) != 0 ? 1u : 0u;
+            mma_i8_ts(tmem, tmem + kAcol + kAcols * (2 * st + 0) + 8 * j, bd, idesc, acc);
+            mma_i8_ts(tmem + tc::kN, tmem + kAcol + kAcols * (2 * st + 1) + 8 * j, bd, idesc, acc);
+          }
+          tc::commit(tc::smem_u32(&s.mma_done[st]));
+        }
+      }
+    }
+  } else if (warp == kImgWarp) {
     // ---- class images: one cp.async.bulk per chunk into B stage gch & 1, once its last MMAs are done
     if (lane == 0) {
       uint32_t gch = 0, mma_phase = 0, pending = 0;
@@ -215,8 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- spreaders: warp w owns TMEM lanes 32(w%4).. of tile w/4; thread = row
     const uint32_t tile = warp >> 2, lrow = ((warp & 3u) << 5) | lane, prow = tile * tc::kM + lrow;
     const uint32_t lane_base = (warp & 3u) << 21;  // (32 * (w % 4)) << 16
-    const uint32_t idesc = (2u << 4) | ((N >> 3) << 17) | ((static_cast<uint32_t>(tc::kM) >> 4) << 24);
-    uint32_t mma_phase = 0, pending = 0, b_phase = 0;
+    uint32_t mma_phase = 0, pending = 0;
     uint32_t gch = 0;
     for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
       const uint32_t c0 = static_cast<uint32_t>(it % nct) * tc::kN;
@@ -262,21 +295,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;");
-        asm volatile("bar.sync 1, %0;" ::"n"(kSpread) : "memory");
-        if (tid == 0) {
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          tc::mbar_wait(tc::smem_u32(&s.b_full[st]), (b_phase >> st) & 1u);
-          b_phase ^= 1u << st;
-          const uint32_t b0 = tc::smem_u32(s.b[st]);
-#pragma unroll
-          for (uint32_t j = 0; j < kWords; ++j) {  // K = 32 bytes per UMMA: 8 A columns, 256 B of image
-            const uint64_t bd = tc::make_desc(b0 + 256 * j, 128, tc::kSbo);
-            const uint32_t acc = (kc | j) != 0 ? 1u : 0u;
-            mma_i8_ts(tmem, tmem + kAcol + kAcols * (2 * st + 0) + 8 * j, bd, idesc, acc);
-            mma_i8_ts(tmem + tc::kN, tmem + kAcol + kAcols * (2 * st + 1) + 8 * j, bd, idesc, acc);
-          }
-          tc::commit(tc::smem_u32(&s.mma_done[st]));
-        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s.a_full[st]));
       }
       // every MMA of the pair has landed in TMEM
       for (uint32_t st = 0; st < tc::kStages; ++st) {
@@ -311,8 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (eok) atomicMin(best + row, key);
       asm volatile("tcgen05.fence::before_thread_sync;");
-      asm volatile("bar.sync 1, %0;" ::"n"(kSpread) : "memory");  // accumulators read before the next pair
-      asm volatile("tcgen05.fence::after_thread_sync;");
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s.acc_empty));  // accumulators free for the next pair
     }
   }
   __syncthreads();

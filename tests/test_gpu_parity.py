@@ -417,6 +417,35 @@ def test_device_classical_and_predict_vs_oracle():
     np.testing.assert_array_equal(pred.cpu().numpy(), ol)
 
 
+@pytest.mark.parametrize("D", [10000, 4096, 1000])
+@pytest.mark.parametrize("skip", [0, 1, 3])
+def test_device_predict_many_classes_offset_rows(D, skip):
+    """Device many-class scan on a row view starting `skip` rows in: the
+    tcgen05 path for 16-byte-aligned row data (aligned rows, or the 48-byte
+    window copies when W % 4 != 0), the mma.sync path otherwise — labels and
+    popcounts bit-exact vs the oracle."""
+    from paper_2206_04746_b200 import device as dv
+    C, rows = 70, 600
+    cbk = dv.DeviceCodebook.make(64, 16, D, seed=5)
+    eng = dv.Engine(cbk, C)
+    bins8, labels = eng.synth(0, rows, 0, 11)
+    enc = eng.encode(bins8)
+    cv, _, _ = eng.train_classical(enc, labels)
+    view = enc[skip:]
+    pops = torch.empty((rows - skip, C), dtype=torch.int32, device=enc.device)
+    pred = eng.predict(cv, view, popcounts=pops)
+    eng.dc.check()
+    encn = view.cpu().numpy().view(np.uint32)
+    cvn = cv.cpu().numpy().view(np.uint32)
+    eb, cb = O.unpack_rows(encn, D), O.unpack_rows(cvn, D)
+    ref = (eb[:, None, :] != cb[None, :, :]).sum(-1)
+    np.testing.assert_array_equal(pops.cpu().numpy(), ref)
+    m = O.NaiveModel(C, D, cbk.model_tiebreak.cpu().numpy().view(np.uint32))
+    m.cv[:] = cb
+    ol, _ = m.predict(encn)
+    np.testing.assert_array_equal(pred.cpu().numpy(), ol)
+
+
 def test_device_online_delta_mode_emulated_ranks():
     """Data-parallel delta mode emulated with 2 ranks on one
     GPU: each rank's per-class deltas for its slice of a batch are summed (the
