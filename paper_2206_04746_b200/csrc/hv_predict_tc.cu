@@ -4,34 +4,38 @@
 //   popc(q ^ c) = |q| + |c| - 2 <q, c>
 //
 // <q, c> is a 0/1 GEMM, rows x D times D x classes, computed with
-// tcgen05.mma kind::i8 (u8 operands holding 0/1, exact s32 accumulation).
+// tcgen05.mma kind::f8f6f4: every bit becomes the e4m3 byte 0x08 (= 2^-6) or
+// 0, so each product is 2^-12 or 0 and the f32 accumulator holds
+// <q, c> * 2^-12 exactly (integers below 2^24 times a power of two). kind::i8
+// with 0/1 bytes measured 1.5-2.6x slower per instruction on this B200.
 // A CTA owns a PAIR of 128-row tiles against one class tile of N <= 128
 // classes, two accumulators in TMEM (2 x 128 columns). The K dimension is the
-// hypervector's bits, 256 per chunk (8 packed words).
+// hypervector's bits, 128 per MMA stage (4 packed words).
 //
 //   * classes (B operand): spread once per call by tc_arrange_classes_kernel
 //     into the exact shared-memory image the UMMA descriptor reads (K-major,
-//     no swizzle, 8 x 16-byte core matrices), one 32 KB image per (class tile,
-//     chunk); the CTA fetches it with one cp.async.bulk per chunk (async proxy,
+//     no swizzle, 8 x 16-byte core matrices), one 16 KB image per (class tile,
+//     4-word stage); the CTA fetches it with one cp.async.bulk per chunk (async proxy,
 //     completion through the stage's mbarrier transaction count);
-//   * rows (A operand): 4 loader warps keep kRing chunks of packed rows in
-//     flight with 16-byte cp.async into a shared ring; 8 spreader warps (one
-//     thread per row) turn a row's 8 words into 64 byte-columns and write them
+//   * rows (A operand): 4 loader warps keep kRing 32-word chunks of packed rows
+//     in flight with 16-byte cp.async into a shared ring (8 lanes per row, so
+//     a warp's copy touches 4 lines); 8 spreader warps (one thread per row)
+//     turn 4 words at a time into 32 byte-columns and write them
 //     straight into TMEM with tcgen05.st — the MMA reads A from TMEM, so no
 //     generic-proxy shared store (and no per-chunk proxy fence, whose MEMBAR
 //     dominated the shared-memory-staged kernel) sits on the critical path;
 //   * a dedicated MMA warp (one thread) waits for the stage's rows (an
 //     mbarrier the 8 spreader warps arrive on after tcgen05.st) and class
-//     image, issues 2 x 8 UMMAs and commits them to the stage's mbarrier,
+//     image, issues 2 x 4 UMMAs (K = 128 bits) and commits them to the stage's mbarrier,
 //     which frees both the TMEM A stage and the B stage — no CTA-wide barrier
 //     in the steady state;
-//   * the epilogue reads the s32 dot products out of TMEM (tcgen05.ld 32x32b,
+//   * the epilogue reads the f32 dot products out of TMEM (tcgen05.ld 32x32b,
 //     thread = row) and folds |q| + |c| - 2<q,c> into the (distance, class)
 //     argmin key exactly like the other scans.
 //
 // The bit -> byte spread is "strided" (byte 4j + b of a word's 32-byte K slice
 // holds bit 8b + j); rows and classes use the same order, which the dot
-// product does not see.
+// product does not see. MMA stages are half chunks (128 K bytes, 4 stages).
 #include <cstdint>
 #include <cstdlib>
 
@@ -41,31 +45,44 @@
 namespace hvb {
 namespace {
 
-constexpr uint32_t kWords = tc::kKBytes / 32;  // packed words per chunk (8)
+// Raw row chunks are 32 words (one 128-byte line of an aligned row): 8
+// loader lanes cover a row, so a warp's cp.async touches 4 lines instead of 32.
+constexpr uint32_t kWords = 32;
+// MMA stages are 4 words (128 K bytes); 4 stages in flight keep the tensor
+// pipe fed while the spreaders refill the oldest one
+constexpr uint32_t kSubWords = 4, kSubBytes = 32 * kSubWords, kSubSbo = (kSubBytes / 16) * 128;
+constexpr uint32_t kStages = 4;
 constexpr uint32_t kRows = 2 * tc::kM;        // rows per CTA work item (two accumulators)
-constexpr int kRing = 8;                       // raw row chunks in flight
+constexpr int kRing = 4;                       // raw row chunks in flight
 constexpr int kSpread = 256, kLoad = 128, kThreads = kSpread + kLoad + 64;  // + class-image warp + MMA warp
 constexpr uint32_t kImgWarp = (kSpread + kLoad) / 32, kMmaWarp = kImgWarp + 1;
-constexpr uint32_t kWin = 12;                  // words per raw row slot: 8 + alignment window
-constexpr uint32_t kImg = tc::kN * tc::kKBytes;  // class image bytes per (tile, chunk)
-// TMEM columns: accumulators [0, 128) and [128, 256); A stages at 256 + 64 * (2 * stage + tile)
-constexpr uint32_t kTmemCols = 512, kAcol = 256, kAcols = tc::kKBytes / 4;
+// words per raw row slot: 32 + the 16-byte alignment window of unaligned rows;
+// the 144-byte stride also makes 8 consecutive rows' 16-byte reads conflict-free
+constexpr uint32_t kWin = kWords + 4;
+constexpr uint32_t kImg = tc::kN * kSubBytes;  // class image bytes per (class tile, half chunk)
+// TMEM columns: accumulators [0, 128) and [128, 256); A stages at 256 + 32 * (2 * stage + tile)
+constexpr uint32_t kTmemCols = 512, kAcol = 256, kAcols = kSubBytes / 4;
 
 struct __align__(1024) Smem {
-  uint8_t b[tc::kStages][kImg];
+  uint8_t b[kStages][kImg];
   uint32_t raw[kRing][kRows][kWin];
-  unsigned long long mma_done[tc::kStages], b_full[tc::kStages], a_full[tc::kStages], acc_empty;
+  unsigned long long mma_done[kStages], b_full[kStages], a_full[kStages], acc_empty;
   unsigned long long raw_full[kRing], raw_empty[kRing];
   uint32_t tmem;
 };
 constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
 
-__device__ __forceinline__ uint32_t spread(uint32_t x, uint32_t j) { return (x >> j) & 0x01010101u; }
+// bit -> e4m3 byte: 0x08 (= 2^-6) or 0; byte b of spread word j holds bit 8b + j
+template <uint32_t J>
+__device__ __forceinline__ uint32_t spread(uint32_t x) {
+  return (J <= 3 ? (x << (3 - J)) : (x >> (J - 3))) & 0x08080808u;
+}
 
-__device__ __forceinline__ void mma_i8_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+// kind::f8f6f4, A e4m3 from TMEM, B e4m3 from shared memory, D f32 in TMEM
+__device__ __forceinline__ void mma_f8_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
       "r"(a), "l"(bdesc), "r"(idesc), "r"(acc));
 }
 
@@ -100,28 +117,29 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                : "memory");
 }
 
-// classes -> UMMA B images: img[(ct * nchunks + kc)] holds classes ct*128 ..
-// +127, K bytes of chunk kc, in the core-matrix layout of tc::stage_word.
+// classes -> UMMA B images: img[ct * nsub + q] holds classes ct*128 .. +127,
+// the K bytes of half chunk q (words 4q .. 4q+3), K-major no-swizzle core
+// matrices: K byte k of class c at (c/8)*kSubSbo + (k/16)*128 + (c%8)*16 + k%16.
 __global__ void tc_arrange_classes_kernel(const uint32_t* __restrict__ cv, uint32_t C, uint32_t W, uint32_t nct,
-                                          uint32_t nchunks, uint8_t* __restrict__ img) {
-  const uint64_t total = static_cast<uint64_t>(nct) * nchunks * tc::kN * kWords;
+                                          uint32_t nsub, uint8_t* __restrict__ img) {
+  const uint64_t total = static_cast<uint64_t>(nct) * nsub * tc::kN * kSubWords;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t kw = static_cast<uint32_t>(i % kWords);
-    const uint32_t c = static_cast<uint32_t>((i / kWords) % tc::kN);
-    const uint64_t tk = i / (kWords * tc::kN);  // ct * nchunks + kc
-    const uint32_t kc = static_cast<uint32_t>(tk % nchunks), ct = static_cast<uint32_t>(tk / nchunks);
-    const uint32_t cls = ct * tc::kN + c, w = kc * kWords + kw;
+    const uint32_t kw = static_cast<uint32_t>(i % kSubWords);
+    const uint32_t c = static_cast<uint32_t>((i / kSubWords) % tc::kN);
+    const uint64_t tk = i / (kSubWords * tc::kN);  // ct * nsub + q
+    const uint32_t q = static_cast<uint32_t>(tk % nsub), ct = static_cast<uint32_t>(tk / nsub);
+    const uint32_t cls = ct * tc::kN + c, w = q * kSubWords + kw;
     const uint32_t x = (cls < C && w < W) ? cv[static_cast<uint64_t>(cls) * W + w] : 0u;
-    uint4* dst = reinterpret_cast<uint4*>(img + tk * kImg + (c >> 3) * tc::kSbo + (c & 7u) * 16 + 2 * kw * 128);
-    dst[0] = make_uint4(spread(x, 0), spread(x, 1), spread(x, 2), spread(x, 3));
-    dst[8] = make_uint4(spread(x, 4), spread(x, 5), spread(x, 6), spread(x, 7));  // +128 bytes
+    uint4* dst = reinterpret_cast<uint4*>(img + tk * kImg + (c >> 3) * kSubSbo + (c & 7u) * 16 + 2 * kw * 128);
+    dst[0] = make_uint4(spread<0>(x), spread<1>(x), spread<2>(x), spread<3>(x));
+    dst[8] = make_uint4(spread<4>(x), spread<5>(x), spread<6>(x), spread<7>(x));  // +128 bytes
   }
 }
 
 // ALIGNED: every row starts 16-byte aligned (W % 4 == 0); otherwise each raw
-// slot holds the 16-byte-aligned 48-byte window around the row's chunk and
-// the spreader picks its 8 words at the row's word offset.
+// slot holds the 16-byte-aligned 144-byte window around the row's chunk and
+// the spreader picks its words at the row's word offset.
 template <bool ALIGNED>
 __global__ void __launch_bounds__(kThreads, 1)
     predict_tc_kernel(const uint8_t* __restrict__ img, uint32_t C, uint32_t N, uint32_t D, uint32_t W,
@@ -136,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int st = 0; st < tc::kStages; ++st) {
+    for (uint32_t st = 0; st < kStages; ++st) {
       tc::mbar_init(tc::smem_u32(&s.mma_done[st]), 1);
       tc::mbar_init(tc::smem_u32(&s.b_full[st]), 1);
       tc::mbar_init(tc::smem_u32(&s.a_full[st]), kSpread / 32);
@@ -154,19 +172,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = s.tmem;
   const uint32_t nct = (C + tc::kN - 1) / tc::kN;
   const uint64_t npairs = (rows + kRows - 1) / kRows;
-  const uint32_t nchunks = (W + kWords - 1) / kWords;
+  const uint32_t nchunks = (W + kWords - 1) / kWords, nsub = (W + kSubWords - 1) / kSubWords;
   const uint64_t items = npairs * nct;
   if (warp == kMmaWarp) {
-    // ---- MMA issue: one thread; per chunk 2 x 8 UMMAs (A = the stage's TMEM rows, B = its class image)
+    // ---- MMA issue: one thread; per stage 2 x 4 UMMAs (A = the stage's TMEM rows, B = its class image)
     if (lane == 0) {
-      const uint32_t idesc = (2u << 4) | ((N >> 3) << 17) | ((static_cast<uint32_t>(tc::kM) >> 4) << 24);
+      // D f32, A and B e4m3, both K-major, N, M = 128
+      const uint32_t idesc = (1u << 4) | ((N >> 3) << 17) | ((static_cast<uint32_t>(tc::kM) >> 4) << 24);
       uint32_t gch = 0, a_phase = 0, b_phase = 0, pair = 0;
       for (uint64_t it = blockIdx.x; it < items; it += gridDim.x, ++pair) {
         if (pair > 0) {  // the previous pair's epilogue has read the accumulators
           tc::mbar_wait(tc::smem_u32(&s.acc_empty), (pair - 1) & 1u);
         }
-        for (uint32_t kc = 0; kc < nchunks; ++kc, ++gch) {
-          const uint32_t st = gch & 1u;
+        for (uint32_t q = 0; q < nsub; ++q, ++gch) {
+          const uint32_t st = gch % kStages;
           tc::mbar_wait(tc::smem_u32(&s.a_full[st]), (a_phase >> st) & 1u);
           a_phase ^= 1u << st;
           tc::mbar_wait(tc::smem_u32(&s.b_full[st]), (b_phase >> st) & 1u);
@@ -174,11 +193,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t b0 = tc::smem_u32(s.b[st]);
 #pragma unroll
-          for (uint32_t j = 0; j < kWords; ++j) {  // K = 32 bytes per UMMA: 8 A columns, 256 B of image
-            const uint64_t bd = tc::make_desc(b0 + 256 * j, 128, tc::kSbo);
-            const uint32_t acc = (kc | j) != 0 ? 1u : 0u;
-            mma_i8_ts(tmem, tmem + kAcol + kAcols * (2 * st + 0) + 8 * j, bd, idesc, acc);
-            mma_i8_ts(tmem + tc::kN, tmem + kAcol + kAcols * (2 * st + 1) + 8 * j, bd, idesc, acc);
+          for (uint32_t j = 0; j < kSubWords; ++j) {  // K = 32 bytes per UMMA: 8 A columns, 256 B of image
+            const uint64_t bd = tc::make_desc(b0 + 256 * j, 128, kSubSbo);
+            const uint32_t acc = (q | j) != 0 ? 1u : 0u;
+            mma_f8_ts(tmem, tmem + kAcol + kAcols * (2 * st + 0) + 8 * j, bd, idesc, acc);
+            mma_f8_ts(tmem + tc::kN, tmem + kAcol + kAcols * (2 * st + 1) + 8 * j, bd, idesc, acc);
           }
           tc::commit(tc::smem_u32(&s.mma_done[st]));
         }
@@ -189,56 +208,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       uint32_t gch = 0, mma_phase = 0, pending = 0;
       for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const uint8_t* bimg = img + static_cast<uint64_t>(it % nct) * nchunks * kImg;
-        for (uint32_t kc = 0; kc < nchunks; ++kc, ++gch) {
-          const uint32_t st = gch & 1u;
+        const uint8_t* bimg = img + static_cast<uint64_t>(it % nct) * nsub * kImg;
+        for (uint32_t q = 0; q < nsub; ++q, ++gch) {
+          const uint32_t st = gch % kStages;
           if ((pending >> st) & 1u) {
             tc::mbar_wait(tc::smem_u32(&s.mma_done[st]), (mma_phase >> st) & 1u);
             mma_phase ^= 1u << st;
           }
           pending |= 1u << st;
-          bulk_g2s(tc::smem_u32(s.b[st]), bimg + static_cast<uint64_t>(kc) * kImg, N * tc::kKBytes,
+          bulk_g2s(tc::smem_u32(s.b[st]), bimg + static_cast<uint64_t>(q) * kImg, N * kSubBytes,
                    tc::smem_u32(&s.b_full[st]));
         }
       }
     }
   } else if (warp >= kSpread / 32) {
-    // ---- row loaders: thread t copies rows t and t + 128 of the pair
-    const uint32_t t = tid - kSpread;
+    // ---- row loaders: lane group t >> 3 takes rows (t >> 3) + 16 i, lane t & 7 the row's 16-byte piece
+    const uint32_t t = tid - kSpread, pc = t & 7u, rg = t >> 3;
     uint32_t gch = 0;
     for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
       const uint64_t row0 = (it / nct) * kRows;
-      const uint32_t* src[2];
-      bool ok[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint64_t row = row0 + t + h * tc::kM;
-        ok[h] = row < rows;
-        src[h] = enc + (ok[h] ? row : 0) * W;
-      }
       for (uint32_t kc = 0; kc < nchunks; ++kc, ++gch) {
         const uint32_t r = gch % kRing, ph = (gch / kRing) & 1u;
         tc::mbar_wait(tc::smem_u32(&s.raw_empty[r]), ph ^ 1u);
         const uint32_t w = kc * kWords;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t dst = tc::smem_u32(&s.raw[r][t + h * tc::kM][0]);
+#pragma unroll 4
+        for (uint32_t i = 0; i < kRows / 16; ++i) {
+          const uint32_t pr = rg + 16 * i;
+          const uint64_t row = row0 + pr;
+          const bool ok = row < rows;
+          const uint32_t* src = enc + (ok ? row : 0) * W;
+          const uint32_t dst = tc::smem_u32(&s.raw[r][pr][0]);
           if (ALIGNED) {
+            const bool in = ok && w + 4 * pc < W;
+            tc::cp_async16(dst + 16 * pc, src + (in ? w + 4 * pc : 0), in ? 16u : 0u);
+          } else {
+            // 144-byte window from the 16-byte boundary at or below word w of the row,
+            // clamped to the row's end (bytes past it are zero-filled, never read)
+            const uintptr_t a16 = reinterpret_cast<uintptr_t>(src + w) & ~uintptr_t(15);
+            const uintptr_t end = reinterpret_cast<uintptr_t>(src + W);
 #pragma unroll
             for (uint32_t q = 0; q < 2; ++q) {
-              const bool in = ok[h] && w + 4 * q < W;
-              tc::cp_async16(dst + 16 * q, src[h] + (in ? w + 4 * q : 0), in ? 16u : 0u);
-            }
-          } else {
-            // 48-byte window from the 16-byte boundary at or below word w of the row,
-            // clamped to the row's end (bytes past it are zero-filled, never read)
-            const uintptr_t a = reinterpret_cast<uintptr_t>(src[h] + w);
-            const uintptr_t a16 = a & ~uintptr_t(15), end = reinterpret_cast<uintptr_t>(src[h] + W);
-#pragma unroll
-            for (uint32_t q = 0; q < 3; ++q) {
-              const uintptr_t p = a16 + 16 * q;
-              const uint32_t n = (!ok[h] || w >= W || p >= end) ? 0u : (end - p >= 16 ? 16u : static_cast<uint32_t>(end - p));
-              tc::cp_async16(dst + 16 * q, n ? reinterpret_cast<const void*>(p) : src[h], n);
+              const uint32_t piece = pc + 8 * q;
+              if (piece < kWin / 4) {
+                const uintptr_t p = a16 + 16 * piece;
+                const uint32_t n =
+                    (!ok || p >= end) ? 0u : (end - p >= 16 ? 16u : static_cast<uint32_t>(end - p));
+                tc::cp_async16(dst + 16 * piece, n ? reinterpret_cast<const void*>(p) : src, n);
+              }
             }
           }
         }
@@ -250,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tile = warp >> 2, lrow = ((warp & 3u) << 5) | lane, prow = tile * tc::kM + lrow;
     const uint32_t lane_base = (warp & 3u) << 21;  // (32 * (w % 4)) << 16
     uint32_t mma_phase = 0, pending = 0;
-    uint32_t gch = 0;
+    uint32_t gch = 0, gsub = 0;
     for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
       const uint32_t c0 = static_cast<uint32_t>(it % nct) * tc::kN;
       const uint64_t row0 = (it / nct) * kRows;
@@ -259,47 +275,52 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!ALIGNED) mis = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(enc + (row < rows ? row : 0) * W) >> 2) & 3u);
       uint32_t rowpop = 0;
       for (uint32_t kc = 0; kc < nchunks; ++kc, ++gch) {
-        const uint32_t r = gch % kRing, ph = (gch / kRing) & 1u, st = gch & 1u;
+        const uint32_t r = gch % kRing, ph = (gch / kRing) & 1u;
         tc::mbar_wait(tc::smem_u32(&s.raw_full[r]), ph);
-        uint32_t x[kWords];
         const uint32_t base = tc::smem_u32(&s.raw[r][prow][0]);
-        if (ALIGNED) {
-          const uint4 u = tc::lds128(base), v = tc::lds128(base + 16);
-          x[0] = u.x, x[1] = u.y, x[2] = u.z, x[3] = u.w, x[4] = v.x, x[5] = v.y, x[6] = v.z, x[7] = v.w;
-        } else {
-          const uint4 u = tc::lds128(base), v = tc::lds128(base + 16), z = tc::lds128(base + 32);
-          const uint32_t win[12] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w, z.x, z.y, z.z, z.w};
+        const uint32_t qend = min(kWords / kSubWords, nsub - kc * (kWords / kSubWords));
+#pragma unroll 1
+        for (uint32_t q = 0; q < qend; ++q, ++gsub) {  // words 4q..4q+3 of the chunk -> stage gsub % kStages
+          uint32_t x[4];
+          if (ALIGNED) {
+            const uint4 u = tc::lds128(base + 16 * q);
+            x[0] = u.x, x[1] = u.y, x[2] = u.z, x[3] = u.w;
+          } else {
+            const uint4 u = tc::lds128(base + 16 * q), v = tc::lds128(base + 16 * q + 16);
+            const uint32_t win[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
 #pragma unroll
-          for (uint32_t i = 0; i < kWords; ++i) {
-            x[i] = mis == 0 ? win[i] : mis == 1 ? win[i + 1] : mis == 2 ? win[i + 2] : win[i + 3];
+            for (uint32_t i = 0; i < 4; ++i) {
+              x[i] = mis == 0 ? win[i] : mis == 1 ? win[i + 1] : mis == 2 ? win[i + 2] : win[i + 3];
+            }
           }
-        }
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s.raw_empty[r]));  // release orders the reads above
-#pragma unroll
-        for (uint32_t i = 0; i < kWords; ++i) rowpop += __popc(x[i]);
-        if ((pending >> st) & 1u) {  // the MMAs that last read this A stage are done
-          tc::mbar_wait(tc::smem_u32(&s.mma_done[st]), (mma_phase >> st) & 1u);
-          mma_phase ^= 1u << st;
-        }
-        pending |= 1u << st;
-        const uint32_t acol = kAcol + kAcols * (2 * st + tile);
-#pragma unroll
-        for (uint32_t hw = 0; hw < 2; ++hw) {  // words 4hw..4hw+3 -> columns 32hw..32hw+31
+          if (q + 1 == qend) {
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s.raw_empty[r]));  // release orders the reads above
+          }
+          rowpop += __popc(x[0]) + __popc(x[1]) + __popc(x[2]) + __popc(x[3]);
+          const uint32_t st = gsub % kStages;
+          if ((pending >> st) & 1u) {  // the MMAs that last read this A stage are done
+            tc::mbar_wait(tc::smem_u32(&s.mma_done[st]), (mma_phase >> st) & 1u);
+            mma_phase ^= 1u << st;
+          }
+          pending |= 1u << st;
           uint32_t v[32];
 #pragma unroll
-          for (uint32_t i = 0; i < 4; ++i)
-#pragma unroll
-            for (uint32_t j = 0; j < 8; ++j) v[8 * i + j] = spread(x[4 * hw + i], j);
-          tmem_st32(tmem + lane_base + acol + 32 * hw, v);
+          for (uint32_t i = 0; i < 4; ++i) {
+            const uint32_t xi = x[i];
+            v[8 * i + 0] = spread<0>(xi), v[8 * i + 1] = spread<1>(xi), v[8 * i + 2] = spread<2>(xi);
+            v[8 * i + 3] = spread<3>(xi), v[8 * i + 4] = spread<4>(xi), v[8 * i + 5] = spread<5>(xi);
+            v[8 * i + 6] = spread<6>(xi), v[8 * i + 7] = spread<7>(xi);
+          }
+          tmem_st32(tmem + lane_base + kAcol + kAcols * (2 * st + tile), v);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s.a_full[st]));
         }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s.a_full[st]));
       }
       // every MMA of the pair has landed in TMEM
-      for (uint32_t st = 0; st < tc::kStages; ++st) {
+      for (uint32_t st = 0; st < kStages; ++st) {
         if ((pending >> st) & 1u) {
           tc::mbar_wait(tc::smem_u32(&s.mma_done[st]), (mma_phase >> st) & 1u);
           mma_phase ^= 1u << st;
@@ -320,7 +341,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (uint32_t i = 0; i < 32; ++i) {
             const uint32_t c = c0 + 32 * cb + i;
             if (c < C) {
-              const uint32_t ham = rowpop + cpop[c] - 2u * v[i];
+              // <q, c> * 2^-12, exact in f32 (D < 2^24)
+              const uint32_t dot = static_cast<uint32_t>(__uint_as_float(v[i]) * 4096.0f);
+              const uint32_t ham = rowpop + cpop[c] - 2u * dot;
               const unsigned long long k = (static_cast<unsigned long long>(ham) << 32) | c;
               key = k < key ? k : key;
               if (pops) pops[row * C + c] = ham;
@@ -345,14 +368,15 @@ bool predict_tc_launch(hv_context* ctx, cudaStream_t st, const uint32_t* cv, siz
                        size_t rows, const uint32_t* cpop, unsigned long long* best, double* dist, uint32_t* pops) {
   const size_t W = words_per_row(D);
   if ((reinterpret_cast<uintptr_t>(enc) & 15u) != 0) return false;  // the 16-byte copy windows need it
+  if (D >= (size_t(1) << 24)) return false;                          // f32-exact dot products
   const uint32_t nct = static_cast<uint32_t>((C + tc::kN - 1) / tc::kN);
-  const uint32_t nchunks = static_cast<uint32_t>((W + kWords - 1) / kWords);
+  const uint32_t nsub = static_cast<uint32_t>((W + kSubWords - 1) / kSubWords);
   // N: classes per UMMA, a multiple of 16 covering one class tile
   const uint32_t N = C >= tc::kN ? tc::kN : static_cast<uint32_t>((C + 15) / 16 * 16);
-  DevBuf<uint8_t> img(static_cast<size_t>(nct) * nchunks * kImg, st);
-  const uint64_t work = static_cast<uint64_t>(nct) * nchunks * tc::kN * kWords;
+  DevBuf<uint8_t> img(static_cast<size_t>(nct) * nsub * kImg, st);
+  const uint64_t work = static_cast<uint64_t>(nct) * nsub * tc::kN * kSubWords;
   tc_arrange_classes_kernel<<<grid_for(work, 256, ctx->sm_count * 8), 256, 0, st>>>(
-      cv, static_cast<uint32_t>(C), static_cast<uint32_t>(W), nct, nchunks, img.ptr);
+      cv, static_cast<uint32_t>(C), static_cast<uint32_t>(W), nct, nsub, img.ptr);
   launched("tc_arrange_classes_kernel");
   const bool aligned = W % 4 == 0;
   auto kern = aligned ? predict_tc_kernel<true> : predict_tc_kernel<false>;

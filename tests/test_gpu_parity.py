@@ -446,6 +446,33 @@ def test_device_predict_many_classes_offset_rows(D, skip):
     np.testing.assert_array_equal(pred.cpu().numpy(), ol)
 
 
+@pytest.mark.parametrize("D", [65536, 4096 + 64])
+def test_device_predict_many_classes_extreme_counts(D):
+    """Dot products up to D (all-ones rows against all-ones classes) and 0
+    stay exact through the tensor-core scan's f32 accumulators."""
+    from paper_2206_04746_b200 import device as dv
+    C, rows, W = 64, 300, D // 32
+    cbk = dv.DeviceCodebook.make(8, 16, D, seed=5)
+    eng = dv.Engine(cbk, C)
+    rng = np.random.default_rng(D)
+    encn = rng.integers(0, 2**32, (rows, W), dtype=np.uint64).astype(np.uint32)
+    encn[::3] = 0xFFFFFFFF
+    encn[1::7] = 0
+    cvn = rng.integers(0, 2**32, (C, W), dtype=np.uint64).astype(np.uint32)
+    cvn[::2] = 0xFFFFFFFF
+    cvn[5] = 0
+    enc = torch.from_numpy(encn.view(np.int32)).cuda()
+    cv = torch.from_numpy(cvn.view(np.int32)).cuda()
+    pops = torch.empty((rows, C), dtype=torch.int32, device="cuda")
+    pred = eng.predict(cv, enc, popcounts=pops)
+    eng.dc.check()
+    eb, cb = O.unpack_rows(encn, D), O.unpack_rows(cvn, D)
+    ref = (eb[:, None, :] != cb[None, :, :]).sum(-1)
+    np.testing.assert_array_equal(pops.cpu().numpy(), ref)
+    key = ref.astype(np.int64) * C + np.arange(C)[None, :]
+    np.testing.assert_array_equal(pred.cpu().numpy(), key.argmin(1))
+
+
 def test_device_online_delta_mode_emulated_ranks():
     """Data-parallel delta mode emulated with 2 ranks on one
     GPU: each rank's per-class deltas for its slice of a batch are summed (the
