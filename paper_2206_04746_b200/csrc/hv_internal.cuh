@@ -185,6 +185,13 @@ bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
 // to ~0) and the optional dist / pops; false when enc is not 16-byte aligned.
 bool predict_tc_launch(hv_context* ctx, cudaStream_t st, const uint32_t* cv, size_t C, size_t D, const uint32_t* enc,
                        size_t rows, const uint32_t* cpop, unsigned long long* best, double* dist, uint32_t* pops);
+// rows x C Hamming popcounts on the tensor cores, split over K to fill the GPU
+// (online scoring): ADDS into pops, which must be zero; img:
+// tc_image_bytes(C, D) bytes, cpop: C words of scratch; requires tc_usable(enc, D)
+size_t tc_image_bytes(size_t C, size_t D);
+bool tc_usable(const uint32_t* enc, size_t D);
+void popc_tc_split(hv_context* ctx, cudaStream_t st, const uint32_t* cv, size_t C, size_t D, const uint32_t* enc,
+                   size_t rows, uint32_t* cpop, uint32_t* pops, uint8_t* img);
 void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* enc, size_t rows, size_t D,
                              const int32_t* labels, size_t C, size_t bsz, double gamma, const uint32_t* tie,
                              double* acc, double* weight, uint64_t* counts, uint32_t* cv);

@@ -91,6 +91,8 @@ struct OnlineParams {
   uint32_t ksplit;             // tiled scoring: word range split into this many items per tile
   uint32_t* pscr;              // bsz x C partial popcounts (ksplit > 1), zero between batches
   uint32_t* arrive;            // per (row tile, class block) arrival counters (ksplit > 1)
+  uint32_t* pre;               // optional: bsz x C popcounts of the (single) batch, precomputed;
+                               // zeroed as read, and best[0, bsz) is reset after the batch
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -151,9 +153,22 @@ __device__ void score_tiled(const OnlineParams& p, unsigned long long* best_out,
     const uint32_t kbeg = static_cast<uint32_t>((static_cast<uint64_t>(p.W) * kx / ks) & ~3ull);
     const uint32_t kend = kx + 1 == ks ? p.W : static_cast<uint32_t>((static_cast<uint64_t>(p.W) * (kx + 1) / ks) & ~3ull);
     uint32_t a[kScanRowsPerWarp];
-    scan_tile<kOThreads>(p.enc, b0 + t0, nr, p.W, p.cv, p.C, cb * kScanCls, s, a, kbeg, kend);
     const uint32_t c = cb * kScanCls + lane;
     const bool compute = warp < kScanRows / kScanRowsPerWarp;
+    if (p.pre) {  // tensor-core popcounts of this batch (uniform per launch)
+#pragma unroll
+      for (int k = 0; k < kScanRowsPerWarp; ++k) {
+        const uint32_t r = warp * kScanRowsPerWarp + k;
+        a[k] = 0u;
+        if (compute && r < nr && c < p.C) {
+          uint32_t* slot = p.pre + (t0 + r) * p.C + c;
+          a[k] = *slot;
+          *slot = 0u;  // the next batch's split-K partials add into zeros
+        }
+      }
+    } else {
+      scan_tile<kOThreads>(p.enc, b0 + t0, nr, p.W, p.cv, p.C, cb * kScanCls, s, a, kbeg, kend);
+    }
     if (ks > 1) {
       if (compute && c < p.C) {
 #pragma unroll
@@ -491,7 +506,8 @@ __global__ void __launch_bounds__(kOThreads, 2) online_persistent_kernel(OnlineP
       replay_lists<COLS>(p, s, b0);
     }
     if (lane_class) {
-      unsigned long long* nxt = p.best + (par ^ 1u) * p.bsz;
+      // one batch per launch with precomputed popcounts: reset this batch's own keys
+      unsigned long long* nxt = p.pre ? bestv : p.best + (par ^ 1u) * p.bsz;
       const uint64_t gt = static_cast<uint64_t>(blockIdx.x) * kOThreads + threadIdx.x;
       for (uint64_t r = gt; r < p.bsz; r += static_cast<uint64_t>(gridDim.x) * kOThreads) nxt[r] = ~0ull;
     }
@@ -553,7 +569,7 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   const uint64_t want = std::max<uint64_t>(items, score_ctas);
   OnlineParams p{enc,     labels,   rows,     static_cast<uint32_t>(D), static_cast<uint32_t>(W),
                  static_cast<uint32_t>(C), n, gamma, tie, acc, wts.ptr, counts, cv, best.ptr, truep.ptr, lidx.ptr,
-                 lval.ptr, llen.ptr, nullptr, lane_class ? 1u : 0u, 1u, nullptr, nullptr};
+                 lval.ptr, llen.ptr, nullptr, lane_class ? 1u : 0u, 1u, nullptr, nullptr, nullptr};
   // HVB200_ONLINE_PROFILE=1: print the time per phase (CTA 0's view, barrier waits included)
   const char* pe = getenv("HVB200_ONLINE_PROFILE");
   DevBuf<unsigned long long> prof(pe && pe[0] == '1' ? 3 : 0, st);
@@ -574,7 +590,12 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   } else {
     grid_est = cooperative_grid<false, 1>(ctx, want);
   }
-  if (lane_class) {
+  // many classes: score each batch on the tensor cores (hv_predict_tc.cu) and
+  // run the persistent kernel once per batch on the precomputed popcounts
+  const char* te = getenv("HVB200_ONLINE_TC");
+  const bool tc_mode = !merged && lane_class && C >= 64 && (te == nullptr || te[0] != '0') && tc_usable(enc, D) &&
+                       (n * W) % 4 == 0;
+  if (lane_class && !tc_mode) {
     const uint64_t tiles = ((n + kScanRows - 1) / kScanRows) * ((C + kScanCls - 1) / kScanCls);
     // ~3 items per CTA keeps the tail of the score phase short
     const uint64_t ks = std::min<uint64_t>((3 * grid_est + tiles - 1) / tiles, std::max<size_t>(1, W / kScanK));
@@ -592,7 +613,22 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
     ck(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kOThreads), args, 0, st),
        "online_persistent_kernel");
   };
-  if (merged) {
+  if (tc_mode) {
+    DevBuf<uint32_t> pre(n * C, st), cpop(C, st);
+    DevBuf<uint8_t> img(tc_image_bytes(C, D), st);
+    pre.zero();
+    p.pre = pre.ptr;
+    const auto kern = cols8 ? online_persistent_kernel<false, 8>
+                            : cols4 ? online_persistent_kernel<false, 4> : online_persistent_kernel<false, 1>;
+    for (size_t b0 = 0; b0 < rows; b0 += n) {
+      const size_t nn = std::min(n, rows - b0);
+      popc_tc_split(ctx, st, cv, C, D, enc + b0 * W, nn, cpop.ptr, pre.ptr, img.ptr);
+      p.enc = enc + b0 * W;
+      p.labels = labels + b0;
+      p.rows = nn;
+      launch(kern, grid_est);  // parity 0 only: best[0, n) was reset by the previous launch
+    }
+  } else if (merged) {
     launch(online_persistent_kernel<true, 1>, cooperative_grid<true, 1>(ctx, want));
   } else if (cols8) {
     launch(online_persistent_kernel<false, 8>, cooperative_grid<false, 8>(ctx, want));

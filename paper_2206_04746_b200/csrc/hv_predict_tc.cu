@@ -53,7 +53,10 @@ constexpr uint32_t kWords = 32;
 constexpr uint32_t kSubWords = 4, kSubBytes = 32 * kSubWords, kSubSbo = (kSubBytes / 16) * 128;
 constexpr uint32_t kStages = 4;
 constexpr uint32_t kRows = 2 * tc::kM;        // rows per CTA work item (two accumulators)
-constexpr int kRing = 4;                       // raw row chunks in flight
+// raw row chunks in flight: 4 for the full scan, 3 for the split-K popcount
+// variant, whose epilogue transpose needs the shared memory
+template <bool PARTIAL>
+constexpr int kRingOf = PARTIAL ? 3 : 4;
 constexpr int kSpread = 256, kLoad = 128, kThreads = kSpread + kLoad + 64;  // + class-image warp + MMA warp
 constexpr uint32_t kImgWarp = (kSpread + kLoad) / 32, kMmaWarp = kImgWarp + 1;
 // words per raw row slot: 32 + the 16-byte alignment window of unaligned rows;
@@ -63,14 +66,18 @@ constexpr uint32_t kImg = tc::kN * kSubBytes;  // class image bytes per (class t
 // TMEM columns: accumulators [0, 128) and [128, 256); A stages at 256 + 32 * (2 * stage + tile)
 constexpr uint32_t kTmemCols = 512, kAcol = 256, kAcols = kSubBytes / 4;
 
+template <bool PARTIAL>
 struct __align__(1024) Smem {
+  static constexpr int kRing = kRingOf<PARTIAL>;
   uint8_t b[kStages][kImg];
   uint32_t raw[kRing][kRows][kWin];
-  unsigned long long mma_done[kStages], b_full[kStages], a_full[kStages], acc_empty;
+  uint32_t xpose[PARTIAL ? kSpread / 32 : 1][32][33];  // split-K epilogue: (row, class) -> (class, row) per warp
+  unsigned long long mma_done[kStages], a_full[kStages], b_full[kStages], acc_empty;
   unsigned long long raw_full[kRing], raw_empty[kRing];
   uint32_t tmem;
 };
-constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
+template <bool PARTIAL>
+constexpr size_t kSmemBytes = sizeof(Smem<PARTIAL>) + 1024;
 
 // bit -> e4m3 byte: 0x08 (= 2^-6) or 0; byte b of spread word j holds bit 8b + j
 template <uint32_t J>
@@ -120,8 +127,18 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 // classes -> UMMA B images: img[ct * nsub + q] holds classes ct*128 .. +127,
 // the K bytes of half chunk q (words 4q .. 4q+3), K-major no-swizzle core
 // matrices: K byte k of class c at (c/8)*kSubSbo + (k/16)*128 + (c%8)*16 + k%16.
+// cpop (optional): the first blocks also write each class's popcount (warp per class).
 __global__ void tc_arrange_classes_kernel(const uint32_t* __restrict__ cv, uint32_t C, uint32_t W, uint32_t nct,
-                                          uint32_t nsub, uint8_t* __restrict__ img) {
+                                          uint32_t nsub, uint8_t* __restrict__ img, uint32_t* __restrict__ cpop) {
+  if (cpop != nullptr) {
+    const uint32_t c = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31u;
+    if (c < C) {
+      uint32_t a = 0;
+      for (uint32_t w = lane; w < W; w += 32) a += __popc(cv[static_cast<uint64_t>(c) * W + w]);
+      a = __reduce_add_sync(0xFFFFFFFFu, a);
+      if (lane == 0) cpop[c] = a;
+    }
+  }
   const uint64_t total = static_cast<uint64_t>(nct) * nsub * tc::kN * kSubWords;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -137,16 +154,39 @@ __global__ void tc_arrange_classes_kernel(const uint32_t* __restrict__ cv, uint3
   }
 }
 
+// One CTA work item: a pair of row tiles x one class tile x one K range (a
+// split of the 32-word chunks; ks = 1 covers the whole hypervector).
+struct Item {
+  uint32_t ct, k0, k1, q0, q1;
+  uint64_t row0;
+};
+__device__ __forceinline__ Item item_of(uint64_t it, uint32_t nct, uint32_t ks, uint32_t nchunks, uint32_t nsub) {
+  Item m;
+  const uint32_t kx = static_cast<uint32_t>(it % ks);
+  const uint64_t rest = it / ks;
+  m.ct = static_cast<uint32_t>(rest % nct);
+  m.row0 = (rest / nct) * kRows;
+  m.k0 = static_cast<uint32_t>(static_cast<uint64_t>(nchunks) * kx / ks);
+  m.k1 = static_cast<uint32_t>(static_cast<uint64_t>(nchunks) * (kx + 1) / ks);
+  m.q0 = m.k0 * (kWords / kSubWords);
+  m.q1 = min(m.k1 * (kWords / kSubWords), nsub);
+  return m;
+}
+
 // ALIGNED: every row starts 16-byte aligned (W % 4 == 0); otherwise each raw
 // slot holds the 16-byte-aligned 144-byte window around the row's chunk and
 // the spreader picks its words at the row's word offset.
-template <bool ALIGNED>
+template <bool ALIGNED, bool PARTIAL>
 __global__ void __launch_bounds__(kThreads, 1)
     predict_tc_kernel(const uint8_t* __restrict__ img, uint32_t C, uint32_t N, uint32_t D, uint32_t W,
                       const uint32_t* __restrict__ enc, uint64_t rows, const uint32_t* __restrict__ cpop,
-                      unsigned long long* __restrict__ best, double* __restrict__ dist, uint32_t* __restrict__ pops) {
+                      unsigned long long* __restrict__ best, double* __restrict__ dist, uint32_t* __restrict__ pops,
+                      uint32_t ks) {
   extern __shared__ uint8_t tc_raw[];
-  Smem& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
+  using SmemT = Smem<PARTIAL>;
+  constexpr int kRing = SmemT::kRing;
+  SmemT& s = *reinterpret_cast<SmemT*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
+  if (!PARTIAL) ks = 1;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&s.tmem)),
@@ -173,7 +213,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t nct = (C + tc::kN - 1) / tc::kN;
   const uint64_t npairs = (rows + kRows - 1) / kRows;
   const uint32_t nchunks = (W + kWords - 1) / kWords, nsub = (W + kSubWords - 1) / kSubWords;
-  const uint64_t items = npairs * nct;
+  // best == nullptr: popcounts only, split-K over ks items per tile; each item
+  // ADDS its partial |q| - 2<q, c> (+ |c| for the first split) into pops
+  // (mod 2^32, zeroed by the caller)
+  const uint64_t items = npairs * nct * ks;
   if (warp == kMmaWarp) {
     // ---- MMA issue: one thread; per stage 2 x 4 UMMAs (A = the stage's TMEM rows, B = its class image)
     if (lane == 0) {
@@ -181,10 +224,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc = (1u << 4) | ((N >> 3) << 17) | ((static_cast<uint32_t>(tc::kM) >> 4) << 24);
       uint32_t gch = 0, a_phase = 0, b_phase = 0, pair = 0;
       for (uint64_t it = blockIdx.x; it < items; it += gridDim.x, ++pair) {
+        const Item m = item_of(it, nct, ks, nchunks, nsub);
         if (pair > 0) {  // the previous pair's epilogue has read the accumulators
           tc::mbar_wait(tc::smem_u32(&s.acc_empty), (pair - 1) & 1u);
         }
-        for (uint32_t q = 0; q < nsub; ++q, ++gch) {
+        for (uint32_t q = m.q0; q < m.q1; ++q, ++gch) {
           const uint32_t st = gch % kStages;
           tc::mbar_wait(tc::smem_u32(&s.a_full[st]), (a_phase >> st) & 1u);
           a_phase ^= 1u << st;
@@ -195,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (uint32_t j = 0; j < kSubWords; ++j) {  // K = 32 bytes per UMMA: 8 A columns, 256 B of image
             const uint64_t bd = tc::make_desc(b0 + 256 * j, 128, kSubSbo);
-            const uint32_t acc = (q | j) != 0 ? 1u : 0u;
+            const uint32_t acc = (q != m.q0 || j != 0) ? 1u : 0u;
             mma_f8_ts(tmem, tmem + kAcol + kAcols * (2 * st + 0) + 8 * j, bd, idesc, acc);
             mma_f8_ts(tmem + tc::kN, tmem + kAcol + kAcols * (2 * st + 1) + 8 * j, bd, idesc, acc);
           }
@@ -208,8 +252,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       uint32_t gch = 0, mma_phase = 0, pending = 0;
       for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const uint8_t* bimg = img + static_cast<uint64_t>(it % nct) * nsub * kImg;
-        for (uint32_t q = 0; q < nsub; ++q, ++gch) {
+        const Item m = item_of(it, nct, ks, nchunks, nsub);
+        const uint8_t* bimg = img + static_cast<uint64_t>(m.ct) * nsub * kImg;
+        for (uint32_t q = m.q0; q < m.q1; ++q, ++gch) {
           const uint32_t st = gch % kStages;
           if ((pending >> st) & 1u) {
             tc::mbar_wait(tc::smem_u32(&s.mma_done[st]), (mma_phase >> st) & 1u);
@@ -226,8 +271,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t t = tid - kSpread, pc = t & 7u, rg = t >> 3;
     uint32_t gch = 0;
     for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
-      const uint64_t row0 = (it / nct) * kRows;
-      for (uint32_t kc = 0; kc < nchunks; ++kc, ++gch) {
+      const Item m = item_of(it, nct, ks, nchunks, nsub);
+      const uint64_t row0 = m.row0;
+      for (uint32_t kc = m.k0; kc < m.k1; ++kc, ++gch) {
         const uint32_t r = gch % kRing, ph = (gch / kRing) & 1u;
         tc::mbar_wait(tc::smem_u32(&s.raw_empty[r]), ph ^ 1u);
         const uint32_t w = kc * kWords;
@@ -268,13 +314,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t mma_phase = 0, pending = 0;
     uint32_t gch = 0, gsub = 0;
     for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
-      const uint32_t c0 = static_cast<uint32_t>(it % nct) * tc::kN;
-      const uint64_t row0 = (it / nct) * kRows;
+      const Item m = item_of(it, nct, ks, nchunks, nsub);
+      const uint32_t c0 = m.ct * tc::kN;
+      const uint64_t row0 = m.row0;
       const uint64_t row = row0 + prow;
       uint32_t mis = 0;
       if (!ALIGNED) mis = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(enc + (row < rows ? row : 0) * W) >> 2) & 3u);
       uint32_t rowpop = 0;
-      for (uint32_t kc = 0; kc < nchunks; ++kc, ++gch) {
+      for (uint32_t kc = m.k0; kc < m.k1; ++kc, ++gch) {
         const uint32_t r = gch % kRing, ph = (gch / kRing) & 1u;
         tc::mbar_wait(tc::smem_u32(&s.raw_full[r]), ph);
         const uint32_t base = tc::smem_u32(&s.raw[r][prow][0]);
@@ -336,7 +383,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (32 * cb >= N) break;  // warp-uniform
         uint32_t v[32];
         tmem_ld32(tmem + lane_base + tc::kN * tile + 32 * cb, v);
-        if (eok) {
+        if (PARTIAL) {
+          // partial (split-K) popcounts |q|_k - 2<q, c>_k (+ |c| once), mod 2^32,
+          // transposed through shared memory so each warp-wide atomic covers 32
+          // consecutive classes of one row
+          uint32_t(&xp)[32][33] = s.xpose[warp];
+#pragma unroll
+          for (uint32_t i = 0; i < 32; ++i) {
+            const uint32_t c = c0 + 32 * cb + i;
+            const uint32_t dot = static_cast<uint32_t>(__uint_as_float(v[i]) * 4096.0f);
+            xp[lane][i] = rowpop - 2u * dot + ((m.k0 == 0 && c < C) ? cpop[c] : 0u);
+          }
+          __syncwarp();
+          const uint32_t c = c0 + 32 * cb + lane;
+          const uint64_t wrow0 = row0 + tile * tc::kM + ((warp & 3u) << 5);
+#pragma unroll 4
+          for (uint32_t j = 0; j < 32; ++j) {
+            if (c < C && wrow0 + j < rows) atomicAdd(pops + (wrow0 + j) * C + c, xp[j][lane]);
+          }
+          __syncwarp();
+        } else if (eok) {
 #pragma unroll
           for (uint32_t i = 0; i < 32; ++i) {
             const uint32_t c = c0 + 32 * cb + i;
@@ -352,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (eok) atomicMin(best + row, key);
+      if (eok && !PARTIAL) atomicMin(best + row, key);
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s.acc_empty));  // accumulators free for the next pair
@@ -364,30 +430,67 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-bool predict_tc_launch(hv_context* ctx, cudaStream_t st, const uint32_t* cv, size_t C, size_t D, const uint32_t* enc,
-                       size_t rows, const uint32_t* cpop, unsigned long long* best, double* dist, uint32_t* pops) {
+namespace {
+// arrange the class images into img (nct * nsub * kImg bytes) and run the scan
+// cpop_out: compute the class popcounts into it (cpop then points there)
+void tc_scan(hv_context* ctx, cudaStream_t st, const uint32_t* cv, size_t C, size_t D, const uint32_t* enc,
+             size_t rows, const uint32_t* cpop, unsigned long long* best, double* dist, uint32_t* pops, uint8_t* img,
+             uint32_t ks, uint32_t* cpop_out = nullptr) {
   const size_t W = words_per_row(D);
-  if ((reinterpret_cast<uintptr_t>(enc) & 15u) != 0) return false;  // the 16-byte copy windows need it
-  if (D >= (size_t(1) << 24)) return false;                          // f32-exact dot products
   const uint32_t nct = static_cast<uint32_t>((C + tc::kN - 1) / tc::kN);
   const uint32_t nsub = static_cast<uint32_t>((W + kSubWords - 1) / kSubWords);
   // N: classes per UMMA, a multiple of 16 covering one class tile
   const uint32_t N = C >= tc::kN ? tc::kN : static_cast<uint32_t>((C + 15) / 16 * 16);
-  DevBuf<uint8_t> img(static_cast<size_t>(nct) * nsub * kImg, st);
   const uint64_t work = static_cast<uint64_t>(nct) * nsub * tc::kN * kSubWords;
-  tc_arrange_classes_kernel<<<grid_for(work, 256, ctx->sm_count * 8), 256, 0, st>>>(
-      cv, static_cast<uint32_t>(C), static_cast<uint32_t>(W), nct, nsub, img.ptr);
+  const unsigned ag = std::max(grid_for(work, 256, ctx->sm_count * 8), static_cast<unsigned>((C + 7) / 8));
+  tc_arrange_classes_kernel<<<ag, 256, 0, st>>>(cv, static_cast<uint32_t>(C), static_cast<uint32_t>(W), nct, nsub,
+                                                 img, cpop_out);
   launched("tc_arrange_classes_kernel");
+  if (cpop_out) cpop = cpop_out;
   const bool aligned = W % 4 == 0;
-  auto kern = aligned ? predict_tc_kernel<true> : predict_tc_kernel<false>;
-  ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)),
-     "cudaFuncSetAttribute");
-  const uint64_t items = ((rows + kRows - 1) / kRows) * nct;
+  const bool partial = best == nullptr;
+  auto kern = partial ? (aligned ? predict_tc_kernel<true, true> : predict_tc_kernel<false, true>)
+                      : (aligned ? predict_tc_kernel<true, false> : predict_tc_kernel<false, false>);
+  const size_t smem = partial ? kSmemBytes<true> : kSmemBytes<false>;
+  static bool attr_set[4] = {false, false, false, false};  // per process; the attribute is per function
+  if (!attr_set[2 * partial + aligned]) {
+    ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+       "cudaFuncSetAttribute");
+    attr_set[2 * partial + aligned] = true;
+  }
+  const uint64_t items = ((rows + kRows - 1) / kRows) * nct * ks;
   const unsigned g = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(items, ctx->sm_count)));
-  kern<<<g, kThreads, kSmemBytes, st>>>(img.ptr, static_cast<uint32_t>(C), N, static_cast<uint32_t>(D),
-                                        static_cast<uint32_t>(W), enc, rows, cpop, best, dist, pops);
+  kern<<<g, kThreads, smem, st>>>(img, static_cast<uint32_t>(C), N, static_cast<uint32_t>(D),
+                                        static_cast<uint32_t>(W), enc, rows, cpop, best, dist, pops, ks);
   launched("predict_tc_kernel");
+}
+}  // namespace
+
+size_t tc_image_bytes(size_t C, size_t D) {
+  const size_t W = words_per_row(D);
+  return ((C + tc::kN - 1) / tc::kN) * ((W + kSubWords - 1) / kSubWords) * kImg;
+}
+
+bool tc_usable(const uint32_t* enc, size_t D) {
+  return (reinterpret_cast<uintptr_t>(enc) & 15u) == 0 && D < (size_t(1) << 24);
+}
+
+bool predict_tc_launch(hv_context* ctx, cudaStream_t st, const uint32_t* cv, size_t C, size_t D, const uint32_t* enc,
+                       size_t rows, const uint32_t* cpop, unsigned long long* best, double* dist, uint32_t* pops) {
+  if (!tc_usable(enc, D)) return false;  // 16-byte copy windows; f32-exact dot products
+  DevBuf<uint8_t> img(tc_image_bytes(C, D), st);
+  tc_scan(ctx, st, cv, C, D, enc, rows, cpop, best, dist, pops, img.ptr, 1);
   return true;
+}
+
+void popc_tc_split(hv_context* ctx, cudaStream_t st, const uint32_t* cv, size_t C, size_t D, const uint32_t* enc,
+                   size_t rows, uint32_t* cpop, uint32_t* pops, uint8_t* img) {
+  const size_t W = words_per_row(D);
+  const uint64_t base = ((rows + kRows - 1) / kRows) * ((C + tc::kN - 1) / tc::kN);
+  const uint64_t nchunks = (W + kWords - 1) / kWords;
+  const uint32_t ks = static_cast<uint32_t>(
+      std::max<uint64_t>(1, std::min<uint64_t>(nchunks, (ctx->sm_count + base - 1) / base)));
+  tc_scan(ctx, st, cv, C, D, enc, rows, nullptr, nullptr, nullptr, pops, img, ks, cpop);
 }
 
 }  // namespace hvb

@@ -349,7 +349,8 @@ def test_online_random_vs_oracle_bitexact(bsz):
 @pytest.mark.parametrize("C,D,n,bsz", [(2, 1000, 900, 300), (1, 333, 600, 64), (3, 1000, 700, 256), (8, 333, 600, 64),
                                        (26, 2048, 800, 100), (32, 777, 500, 128), (100, 4096, 600, 512),
                                        (40, 64, 300, 1), (3, 70, 257, 256), (6, 10000, 2100, 1024), (6, 2000, 300, 32),
-                                       (100, 1500, 400, 7)])
+                                       (100, 1500, 400, 7), (64, 10000, 700, 256), (130, 3000, 500, 128),
+                                       (100, 4096, 600, 100)])
 def test_online_modes_vs_oracle_bitexact(C, D, n, bsz):
     """Every path of the persistent online trainer against the oracle:
     MERGED (C <= 2), LISTS with warp-per-row scoring (2 < C < 32) and with
@@ -471,6 +472,25 @@ def test_device_predict_many_classes_extreme_counts(D):
     np.testing.assert_array_equal(pops.cpu().numpy(), ref)
     key = ref.astype(np.int64) * C + np.arange(C)[None, :]
     np.testing.assert_array_equal(pred.cpu().numpy(), key.argmin(1))
+
+
+@pytest.mark.parametrize("C,D,rows,bsz", [(100, 32768, 3000, 1024), (64, 10000, 2600, 512)])
+def test_online_tensor_core_scoring_matches_popc_scoring(C, D, rows, bsz, monkeypatch):
+    """Many-class online training scores each batch on the tensor cores
+    (split-K tcgen05 popcounts feeding the persistent trainer); it must give
+    the same fp64 accumulators, weights and class vectors as the POPC-scored
+    persistent kernel (HVB200_ONLINE_TC=0)."""
+    from paper_2206_04746_b200 import device as dv
+    cbk = dv.DeviceCodebook.make(64, 16, D, seed=3)
+    eng = dv.Engine(cbk, C)
+    bins8, labels = eng.synth(0, rows, 0, 5)
+    enc = eng.encode(bins8)
+    tc = eng.train_online(enc, labels, bsz)
+    monkeypatch.setenv("HVB200_ONLINE_TC", "0")
+    ref = eng.train_online(enc, labels, bsz)
+    eng.dc.check()
+    for a, b in zip(tc, ref):
+        assert torch.equal(a, b)
 
 
 def test_device_online_delta_mode_emulated_ranks():
