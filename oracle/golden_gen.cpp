@@ -20,6 +20,7 @@
 #include "hypervec/bitmat.hpp"
 #include "hypervec/data.hpp"
 #include "hypervec/encoding.hpp"
+#include "hypervec/eval.hpp"
 #include "hypervec/kernels.hpp"
 #include "hypervec/model.hpp"
 #include "hypervec/rng.hpp"
@@ -333,6 +334,54 @@ void gen_synth() {
   c.put("y", ds.y);
 }
 
+// eval.cpp:12-116 on sequences shaped like concatenated fold predictions:
+// seizure-like runs, glitches, multi-class labels, edge lengths and windows.
+void gen_eval() {
+  Rng rng(777);
+  const std::vector<std::size_t> lengths = {0, 1, 2, 3, 7, 64, 1000, 4099};
+  const std::vector<std::size_t> windows = {1, 3, 5, 9, 31, 101};
+  int k = 0;
+  for (std::size_t n : lengths) {
+    for (int variant = 0; variant < 3; ++variant) {
+      Case c("eval_" + std::to_string(k++));
+      std::vector<int> truth(n), pred(n);
+      // truth: runs of positives (variant 0/1) or 5-class labels (variant 2)
+      int cur = 0;
+      for (std::size_t i = 0; i < n; ++i) {
+        if (variant == 2) {
+          truth[i] = static_cast<int>(rng.uniform_below(5));
+        } else {
+          if (rng.uniform_below(variant == 0 ? 40 : 6) == 0) cur ^= 1;
+          truth[i] = cur;
+        }
+        const bool flip = rng.uniform_below(variant == 1 ? 3 : 10) == 0;
+        pred[i] = variant == 2 ? (flip ? static_cast<int>(rng.uniform_below(5)) : truth[i])
+                               : (flip ? 1 - truth[i] : truth[i]);
+      }
+      c.put("pred", pred);
+      c.put("truth", truth);
+      const int positive = variant == 2 ? 2 : 1;
+      c.set("positive", positive);
+      std::vector<double> ratios = {std::numeric_limits<double>::quiet_NaN(), std::numeric_limits<double>::quiet_NaN(),
+                                    std::numeric_limits<double>::quiet_NaN(), std::numeric_limits<double>::quiet_NaN()};
+      if (n > 0) {
+        const EvalReport r = sample_metrics(pred, truth, positive);
+        c.put("counts", std::vector<std::uint64_t>{r.tp, r.fp, r.tn, r.fn});
+        ratios[0] = r.accuracy;
+        if (r.tpr) ratios[1] = *r.tpr;
+        if (r.ppv) ratios[2] = *r.ppv;
+        if (r.f1) ratios[3] = *r.f1;
+        c.put("ratios", ratios);
+      }
+      const EpisodeCounts e = episode_metrics(pred, truth, positive);
+      c.put("episodes", std::vector<std::uint64_t>{e.detected, e.total, e.false_positive});
+      if (variant != 2) {
+        for (std::size_t w : windows) c.put("smooth_" + std::to_string(w), smooth_labels(pred, w));
+      }
+    }
+  }
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -352,6 +401,7 @@ int main(int argc, char** argv) {
   gen_pipeline("isolet", 160, 617, 26, 2000, 13, {32}, 1.0);
   gen_online_update();
   gen_synth();
+  gen_eval();
   std::cout << "golden vectors written to " << g_root << "\n";
   return 0;
 }

@@ -552,3 +552,90 @@ void hvo_synth(uint64_t row0, size_t rows, size_t features, size_t classes, size
     }
   }
 }
+
+/* ======================================================================= */
+/* Evaluation (eval.cpp:12-116)                                            */
+/* ======================================================================= */
+
+/* eval.cpp:12-37: centred majority over `window` in-bounds samples, the
+ * window shifted inward at the edges, ties -> 1. Validation (window odd and
+ * >= 1, labels 0/1) happens before the empty / window-1 early return. */
+int hvo_smooth_labels(const int32_t* labels, size_t n, size_t window, int32_t* out, uint64_t* bad) {
+  if (window == 0 || window % 2 == 0) {
+    *bad = window;
+    return HVO_INVALID_ARGUMENT;
+  }
+  for (size_t i = 0; i < n; ++i) {
+    if (labels[i] != 0 && labels[i] != 1) {
+      *bad = i;
+      return HVO_INVALID_ARGUMENT;
+    }
+  }
+  if (n == 0) return HVO_OK;
+  if (window == 1) {
+    memcpy(out, labels, n * sizeof(int32_t));
+    return HVO_OK;
+  }
+  const size_t len = window < n ? window : n;
+  const size_t half = (window - 1) / 2;
+  size_t* prefix = (size_t*)calloc(n + 1, sizeof(size_t));
+  for (size_t i = 0; i < n; ++i) prefix[i + 1] = prefix[i] + (size_t)labels[i];
+  for (size_t i = 0; i < n; ++i) {
+    size_t start = i > half ? i - half : 0;
+    if (start > n - len) start = n - len;
+    const size_t ones = prefix[start + len] - prefix[start];
+    out[i] = 2 * ones >= len ? 1 : 0;
+  }
+  free(prefix);
+  return HVO_OK;
+}
+
+/* eval.cpp:39-77: confusion against one positive class; accuracy over exact
+ * matches; a ratio with a zero denominator stays absent (NaN here). */
+int hvo_sample_metrics(const int32_t* pred, size_t n_pred, const int32_t* truth, size_t n_truth,
+                       int positive_class, uint64_t* counts, double* ratios) {
+  if (n_pred != n_truth || n_pred == 0) return HVO_INVALID_ARGUMENT;
+  uint64_t tp = 0, fp = 0, tn = 0, fn = 0, exact = 0;
+  for (size_t i = 0; i < n_pred; ++i) {
+    if (pred[i] == truth[i]) ++exact;
+    const int p = pred[i] == positive_class, t = truth[i] == positive_class;
+    if (p && t) ++tp;
+    else if (p) ++fp;
+    else if (t) ++fn;
+    else ++tn;
+  }
+  counts[0] = tp; counts[1] = fp; counts[2] = tn; counts[3] = fn; counts[4] = exact;
+  ratios[0] = (double)exact / (double)n_pred;
+  ratios[1] = tp + fn > 0 ? (double)tp / (double)(tp + fn) : NAN;
+  ratios[2] = tp + fp > 0 ? (double)tp / (double)(tp + fp) : NAN;
+  ratios[3] = NAN;
+  if (!isnan(ratios[1]) && !isnan(ratios[2]) && ratios[1] + ratios[2] > 0.0) {
+    ratios[3] = 2.0 * ratios[2] * ratios[1] / (ratios[2] + ratios[1]);
+  }
+  return HVO_OK;
+}
+
+/* eval.cpp:79-116: truth episodes (maximal positive-truth runs) detected iff a
+ * sample in the run is predicted positive; false-positive episodes are
+ * maximal positive-prediction runs with no positive truth inside. */
+int hvo_episode_metrics(const int32_t* pred, size_t n_pred, const int32_t* truth, size_t n_truth,
+                        int positive_class, uint64_t* out) {
+  if (n_pred != n_truth) return HVO_INVALID_ARGUMENT;
+  const size_t n = n_pred;
+  uint64_t detected = 0, total = 0, fpe = 0;
+  for (size_t i = 0; i < n;) {
+    if (truth[i] != positive_class) { ++i; continue; }
+    int hit = 0;
+    while (i < n && truth[i] == positive_class) { hit = hit || pred[i] == positive_class; ++i; }
+    ++total;
+    if (hit) ++detected;
+  }
+  for (size_t i = 0; i < n;) {
+    if (pred[i] != positive_class) { ++i; continue; }
+    int overlaps = 0;
+    while (i < n && pred[i] == positive_class) { overlaps = overlaps || truth[i] == positive_class; ++i; }
+    if (!overlaps) ++fpe;
+  }
+  out[0] = detected; out[1] = total; out[2] = fpe;
+  return HVO_OK;
+}

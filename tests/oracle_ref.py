@@ -69,6 +69,47 @@ def _declare(L):
 
 
 # ---------------------------------------------------------------- packing --
+def _declare_eval(L):
+    sz, vp = C.c_size_t, C.c_void_p
+    L.hvo_smooth_labels.argtypes = [vp, sz, sz, vp, vp]
+    L.hvo_sample_metrics.argtypes = [vp, sz, vp, sz, C.c_int, vp, vp]
+    L.hvo_episode_metrics.argtypes = [vp, sz, vp, sz, C.c_int, vp]
+
+
+def smooth_labels(labels, window):
+    """eval.cpp:12-37 via hvo_smooth_labels; ValueError like the reference's invalid_argument."""
+    L = lib()
+    _declare_eval(L)
+    a = np.ascontiguousarray(labels, np.int32)
+    out = np.zeros(len(a), np.int32)
+    bad = np.zeros(1, np.uint64)
+    if L.hvo_smooth_labels(_p(a), len(a), window, _p(out), _p(bad)) != 0:
+        raise ValueError(f"smooth_labels: bad input at {int(bad[0])}")
+    return out
+
+
+def sample_metrics(pred, truth, positive):
+    """eval.cpp:39-77 -> (counts[tp, fp, tn, fn, exact], ratios[acc, tpr, ppv, f1]; NaN = absent)."""
+    L = lib()
+    _declare_eval(L)
+    p, t = np.ascontiguousarray(pred, np.int32), np.ascontiguousarray(truth, np.int32)
+    counts, ratios = np.zeros(5, np.uint64), np.zeros(4, np.float64)
+    if L.hvo_sample_metrics(_p(p), len(p), _p(t), len(t), positive, _p(counts), _p(ratios)) != 0:
+        raise ValueError("sample_metrics: bad input")
+    return counts, ratios
+
+
+def episode_metrics(pred, truth, positive):
+    """eval.cpp:79-116 -> [detected, total, false_positive]."""
+    L = lib()
+    _declare_eval(L)
+    p, t = np.ascontiguousarray(pred, np.int32), np.ascontiguousarray(truth, np.int32)
+    out = np.zeros(3, np.uint64)
+    if L.hvo_episode_metrics(_p(p), len(p), _p(t), len(t), positive, _p(out)) != 0:
+        raise ValueError("episode_metrics: bad input")
+    return out
+
+
 def words_per_row(dim: int) -> int:
     return (dim + 31) // 32
 

@@ -151,3 +151,33 @@ def test_synth_generator_matches_reference_make_synth():
             got[i, f] = centre + jitter * (2.0 * unit[i * feats + f] - 1.0) * 0.5 * width
     np.testing.assert_array_equal(y, np.arange(rows) % classes)
     np.testing.assert_array_equal(got, X)
+
+
+@pytest.mark.parametrize("name", cases("eval_"))
+def test_eval_smoothing_and_metrics(name):
+    """eval.cpp:12-116 — smoothing, sample and episode metrics on the reference's outputs."""
+    c = Case(name)
+    pred, truth, pos = c["pred"], c["truth"], c.int("positive")
+    for w in (1, 3, 5, 9, 31, 101):
+        if c.has(f"smooth_{w}"):
+            np.testing.assert_array_equal(O.smooth_labels(pred, w), c[f"smooth_{w}"])
+    np.testing.assert_array_equal(O.episode_metrics(pred, truth, pos), c["episodes"])
+    if len(pred):
+        counts, ratios = O.sample_metrics(pred, truth, pos)
+        np.testing.assert_array_equal(counts[:4], c["counts"])
+        np.testing.assert_array_equal(ratios.view(np.uint64), c["ratios"].view(np.uint64))  # bit-exact, NaN = absent
+
+
+def test_eval_oracle_rejects_like_reference():
+    with pytest.raises(ValueError):
+        O.smooth_labels([0, 1], 2)
+    with pytest.raises(ValueError):
+        O.smooth_labels([0, 1], 0)
+    with pytest.raises(ValueError):
+        O.smooth_labels([0, 2], 3)
+    with pytest.raises(ValueError):
+        O.sample_metrics([], [], 1)
+    with pytest.raises(ValueError):
+        O.sample_metrics([1, 0], [1], 1)
+    # test_eval.cpp:24-32 known answers
+    np.testing.assert_array_equal(O.smooth_labels([0, 1, 0, 1, 1, 1, 0], 3), [0, 0, 1, 1, 1, 1, 1])
