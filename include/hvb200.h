@@ -204,6 +204,54 @@ hv_status hv_dataset_fold(hv_context* ctx, const hv_dataset* ds, const uint64_t*
                           hv_metric metric, double gamma, const uint32_t* model_tiebreak, int online,
                           size_t batch_size, int32_t* labels_out, double* min_out, double* max_out);
 
+/* ---- evaluation of concatenated predictions (eval.hpp:16-74) -------------
+ * EvalReport (eval.hpp:26-37): confusion counts against one positive class,
+ * accuracy over exact matches, and ratios that are ABSENT (has_* = 0, value
+ * NaN) when their denominator is zero, plus episode counts (eval.hpp:13-17). */
+typedef struct hv_eval_report {
+  uint64_t tp, fp, tn, fn;
+  double accuracy, tpr, ppv, f1;
+  int has_tpr, has_ppv, has_f1;
+  uint64_t episodes_detected, episodes_total, episodes_false_positive;
+} hv_eval_report;
+/* eval.hpp:44 smooth_labels (eval.cpp:12-37): centred majority over `window`
+ * in-bounds samples, ties -> 1; INVALID_ARGUMENT for an even/zero window or a
+ * non-binary label (first index, reference messages). Host arrays. */
+hv_status hv_smooth_labels(hv_context* ctx, const int32_t* labels, size_t n, size_t window, int32_t* out);
+/* eval.hpp:48 sample_metrics (eval.cpp:39-77); episode fields left zero. */
+hv_status hv_sample_metrics(hv_context* ctx, const int32_t* pred, size_t n_pred, const int32_t* truth,
+                            size_t n_truth, int positive_class, hv_eval_report* report);
+/* eval.hpp:52 episode_metrics (eval.cpp:79-116). */
+hv_status hv_episode_metrics(hv_context* ctx, const int32_t* pred, size_t n_pred, const int32_t* truth,
+                             size_t n_truth, int positive_class, uint64_t* detected, uint64_t* total,
+                             uint64_t* false_positive);
+/* Device-pointer forms (async on the context stream; smoothing synchronises
+ * once to validate): confusion5 = tp, fp, tn, fn, exact; episodes3 =
+ * detected, total, false_positive (device uint64, either nullable). */
+hv_status hv_dev_smooth_labels(hv_context* ctx, const int32_t* labels, size_t n, size_t window, int32_t* out);
+hv_status hv_dev_eval_counts(hv_context* ctx, const int32_t* pred, const int32_t* truth, size_t n,
+                             int positive_class, uint64_t* confusion5, uint64_t* episodes3);
+
+/* ---- HBM-resident experiment (run_experiment, experiment.cpp:280-345) ----
+ * Folds of one resident dataset scatter their test predictions into a
+ * device array (predicted[row], -1 = untested; a later fold overwrites);
+ * finish concatenates the tested rows in original order, smooths binary runs
+ * (class_count == 2 && smooth_window > 1, experiment.cpp:331-336), and scores
+ * them (sample + episode metrics) without the predictions leaving HBM.
+ * Outputs (host, nullable, capacity = dataset rows): tested row indices,
+ * truth, raw prediction and final (smoothed) label per tested row. */
+typedef struct hv_experiment hv_experiment;
+hv_status hv_experiment_create(hv_context* ctx, const hv_dataset* ds, hv_experiment** out);
+void hv_experiment_destroy(hv_experiment* ex);
+hv_status hv_experiment_fold(hv_context* ctx, hv_experiment* ex, const uint64_t* train_idx, size_t n_train,
+                             const uint64_t* test_idx, size_t n_test, size_t bins, const uint32_t* id_vectors,
+                             const uint32_t* value_vectors, size_t dim, hv_binding binding,
+                             const uint32_t* encode_tiebreak, size_t class_count, hv_metric metric, double gamma,
+                             const uint32_t* model_tiebreak, int online, size_t batch_size);
+hv_status hv_experiment_finish(hv_context* ctx, hv_experiment* ex, size_t class_count, size_t smooth_window,
+                               int positive_class, hv_eval_report* report, uint64_t* n_tested,
+                               uint64_t* tested_rows, int32_t* truth, int32_t* predicted, int32_t* final_labels);
+
 /* model.hpp:67-70 hamming_distance_words (host-side helper, no device) */
 double hv_hamming_distance_words(const uint32_t* a, const uint32_t* b, size_t dim);
 

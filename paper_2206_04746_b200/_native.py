@@ -62,6 +62,16 @@ class Model(C.Structure):
                 ("sample_counts", C.c_void_p), ("class_vectors", C.c_void_p), ("tiebreak", C.c_void_p)]
 
 
+class EvalReportC(C.Structure):
+    """struct hv_eval_report (eval.hpp:13-37)."""
+
+    _fields_ = [("tp", C.c_uint64), ("fp", C.c_uint64), ("tn", C.c_uint64), ("fn", C.c_uint64),
+                ("accuracy", C.c_double), ("tpr", C.c_double), ("ppv", C.c_double), ("f1", C.c_double),
+                ("has_tpr", C.c_int), ("has_ppv", C.c_int), ("has_f1", C.c_int),
+                ("episodes_detected", C.c_uint64), ("episodes_total", C.c_uint64),
+                ("episodes_false_positive", C.c_uint64)]
+
+
 sz, u64, u32, i32, vp, dbl, ci = C.c_size_t, C.c_uint64, C.c_uint32, C.c_int32, C.c_void_p, C.c_double, C.c_int
 ST = C.c_int  # hv_status
 
@@ -127,6 +137,15 @@ SIGNATURES = {
     "hv_dataset_create": (ST, [vp, vp, sz, sz, vp, C.POINTER(vp)]),
     "hv_dataset_destroy": (None, [vp]),
     "hv_dataset_fold": (ST, [vp, vp, vp, sz, vp, sz, sz, vp, vp, sz, ci, vp, sz, ci, dbl, vp, ci, sz, vp, vp, vp]),
+    "hv_smooth_labels": (ST, [vp, vp, sz, sz, vp]),
+    "hv_sample_metrics": (ST, [vp, vp, sz, vp, sz, ci, vp]),
+    "hv_episode_metrics": (ST, [vp, vp, sz, vp, sz, ci, vp, vp, vp]),
+    "hv_dev_smooth_labels": (ST, [vp, vp, sz, sz, vp]),
+    "hv_dev_eval_counts": (ST, [vp, vp, vp, sz, ci, vp, vp]),
+    "hv_experiment_create": (ST, [vp, vp, C.POINTER(vp)]),
+    "hv_experiment_destroy": (None, [vp]),
+    "hv_experiment_fold": (ST, [vp, vp, vp, sz, vp, sz, sz, vp, vp, sz, ci, vp, sz, ci, dbl, vp, ci, sz]),
+    "hv_experiment_finish": (ST, [vp, vp, sz, sz, ci, vp, vp, vp, vp, vp, vp]),
     "hv_fold_encode_train": (ST, [vp, vp, sz, vp, vp, sz, sz, vp, vp, sz, sz, vp, sz, C.POINTER(vp)]),
     "hv_fold_counts": (ST, [vp, C.POINTER(vp), C.POINTER(vp)]),
     "hv_fold_predict": (ST, [vp, vp, vp, vp]),

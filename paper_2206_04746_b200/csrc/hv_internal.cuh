@@ -197,6 +197,22 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
                              double* acc, double* weight, uint64_t* counts, uint32_t* cv);
 
 // Host-side codebook helpers shared by several entry points (hv_host.cpp).
+// hv_eval.cu — eval.cpp:12-116 on device labels
+void smooth_labels_device(hv_context* ctx, cudaStream_t st, const int32_t* labels, size_t n, size_t window,
+                          int32_t* out);
+void confusion_device(hv_context* ctx, cudaStream_t st, const int32_t* pred, const int32_t* truth, size_t n,
+                      int positive, unsigned long long* out5);
+void episodes_device(hv_context* ctx, cudaStream_t st, const int32_t* pred, const int32_t* truth, size_t n,
+                     int positive, unsigned long long* out3);
+void fill_report(const unsigned long long c5[5], const unsigned long long e3[3], size_t n, hv_eval_report* r);
+void scatter_labels_device(hv_context* ctx, cudaStream_t st, const uint64_t* idx, size_t n, const int32_t* lab,
+                           int32_t* predicted);
+template <class T>
+struct DevBuf;
+size_t compact_tested_device(hv_context* ctx, cudaStream_t st, const int32_t* predicted, const int32_t* y,
+                             size_t rows, DevBuf<uint64_t>& tested, DevBuf<int32_t>& pred_seq,
+                             DevBuf<int32_t>& truth_seq);
+
 void generate_random_words(size_t count, size_t dim, uint64_t seed, uint32_t* out);
 uint64_t derive_seed(uint64_t seed, uint64_t tag);
 

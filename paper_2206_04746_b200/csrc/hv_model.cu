@@ -1350,14 +1350,20 @@ hv_status hv_dataset_create(hv_context* ctx, const double* X, size_t rows, size_
 
 void hv_dataset_destroy(hv_dataset* ds) { delete ds; }
 
-hv_status hv_dataset_fold(hv_context* ctx, const hv_dataset* ds, const uint64_t* train_idx, size_t n_train,
-                          const uint64_t* test_idx, size_t n_test, size_t bins, const uint32_t* id_vectors,
-                          const uint32_t* value_vectors, size_t dim, hv_binding binding,
-                          const uint32_t* encode_tiebreak, size_t class_count, hv_metric metric, double gamma,
-                          const uint32_t* model_tiebreak, int online, size_t batch_size, int32_t* labels_out,
-                          double* min_out, double* max_out) {
-  return guarded([&] {
-    require(ctx);
+}  // extern "C"
+
+namespace hvb {
+namespace {
+// run_fold_packed (experiment.cpp:148-178) on a resident dataset; the test
+// labels go to the host (labels_out) and/or are scattered on device into
+// predicted[test row] (run_experiment's concatenation, experiment.cpp:305-310).
+void dataset_fold_impl(hv_context* ctx, const hv_dataset* ds, const uint64_t* train_idx, size_t n_train,
+                       const uint64_t* test_idx, size_t n_test, size_t bins, const uint32_t* id_vectors,
+                       const uint32_t* value_vectors, size_t dim, hv_binding binding, const uint32_t* encode_tiebreak,
+                       size_t class_count, hv_metric metric, double gamma, const uint32_t* model_tiebreak, int online,
+                       size_t batch_size, int32_t* labels_out, int32_t* predicted_dev, double* min_out,
+                       double* max_out) {
+  {
     if (!ds) invalid("dataset_fold: null dataset");
     // reference order: fit_discretizer, discretize, encode, train, predict
     if (n_train == 0) invalid("fit_discretizer: empty training matrix");
@@ -1420,7 +1426,10 @@ hv_status hv_dataset_fold(hv_context* ctx, const hv_dataset* ds, const uint64_t*
         argmax_kernel<<<sgrid(ctx, n_test, 128), 128, 0, st>>>(sc.ptr, n_test, static_cast<uint32_t>(C), lab.ptr);
         launched("argmax_kernel");
       }
-      ck(cudaMemcpyAsync(labels_out, lab.ptr, n_test * sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H labels");
+      if (labels_out) {
+        ck(cudaMemcpyAsync(labels_out, lab.ptr, n_test * sizeof(int32_t), cudaMemcpyDeviceToHost, st), "D2H labels");
+      }
+      if (predicted_dev) scatter_labels_device(ctx, st, idx.ptr + n_train, n_test, lab.ptr, predicted_dev);
     }
     if (min_out) mn.download(min_out);
     if (max_out) mx.download(max_out);
@@ -1442,6 +1451,95 @@ hv_status hv_dataset_fold(hv_context* ctx, const hv_dataset* ds, const uint64_t*
       }
       fail(HV_ERR_DOMAIN, "cosine_similarity: zero query vector");
     }
+  }
+}
+}  // namespace
+}  // namespace hvb
+
+struct hv_experiment {
+  const hv_dataset* ds = nullptr;
+  hvb::DevBuf<int32_t> predicted;  // rows, -1 = untested
+};
+
+extern "C" {
+
+hv_status hv_dataset_fold(hv_context* ctx, const hv_dataset* ds, const uint64_t* train_idx, size_t n_train,
+                          const uint64_t* test_idx, size_t n_test, size_t bins, const uint32_t* id_vectors,
+                          const uint32_t* value_vectors, size_t dim, hv_binding binding,
+                          const uint32_t* encode_tiebreak, size_t class_count, hv_metric metric, double gamma,
+                          const uint32_t* model_tiebreak, int online, size_t batch_size, int32_t* labels_out,
+                          double* min_out, double* max_out) {
+  return guarded([&] {
+    require(ctx);
+    if (n_test && !labels_out) invalid("dataset_fold: null labels_out");
+    dataset_fold_impl(ctx, ds, train_idx, n_train, test_idx, n_test, bins, id_vectors, value_vectors, dim, binding,
+                      encode_tiebreak, class_count, metric, gamma, model_tiebreak, online, batch_size, labels_out,
+                      nullptr, min_out, max_out);
+  });
+}
+
+hv_status hv_experiment_create(hv_context* ctx, const hv_dataset* ds, hv_experiment** out) {
+  return guarded([&] {
+    require(ctx);
+    if (!ds || !out) invalid("experiment_create: null dataset or output");
+    auto ex = std::make_unique<hv_experiment>();
+    ex->ds = ds;
+    ex->predicted = DevBuf<int32_t>(std::max<size_t>(ds->rows, 1), ctx->stream);
+    ck(cudaMemsetAsync(ex->predicted.ptr, 0xFF, ex->predicted.bytes(), ctx->stream), "memset");
+    sync(ctx);
+    *out = ex.release();
+  });
+}
+
+void hv_experiment_destroy(hv_experiment* ex) { delete ex; }
+
+hv_status hv_experiment_fold(hv_context* ctx, hv_experiment* ex, const uint64_t* train_idx, size_t n_train,
+                             const uint64_t* test_idx, size_t n_test, size_t bins, const uint32_t* id_vectors,
+                             const uint32_t* value_vectors, size_t dim, hv_binding binding,
+                             const uint32_t* encode_tiebreak, size_t class_count, hv_metric metric, double gamma,
+                             const uint32_t* model_tiebreak, int online, size_t batch_size) {
+  return guarded([&] {
+    require(ctx);
+    if (!ex) invalid("experiment_fold: null experiment");
+    dataset_fold_impl(ctx, ex->ds, train_idx, n_train, test_idx, n_test, bins, id_vectors, value_vectors, dim,
+                      binding, encode_tiebreak, class_count, metric, gamma, model_tiebreak, online, batch_size,
+                      nullptr, ex->predicted.ptr, nullptr, nullptr);
+  });
+}
+
+hv_status hv_experiment_finish(hv_context* ctx, hv_experiment* ex, size_t class_count, size_t smooth_window,
+                               int positive_class, hv_eval_report* report, uint64_t* n_tested,
+                               uint64_t* tested_rows, int32_t* truth, int32_t* predicted, int32_t* final_labels) {
+  return guarded([&] {
+    require(ctx);
+    if (!ex) invalid("experiment_finish: null experiment");
+    cudaStream_t st = ctx->stream;
+    DevBuf<uint64_t> tested;
+    DevBuf<int32_t> pred_seq, truth_seq;
+    const size_t m = compact_tested_device(ctx, st, ex->predicted.ptr, ex->ds->y.ptr, ex->ds->rows, tested, pred_seq,
+                                           truth_seq);
+    if (m == 0) invalid("no test samples produced by split");
+    // experiment.cpp:331-336: smoothing only for binary runs
+    const bool smooth = class_count == 2 && smooth_window > 1;
+    DevBuf<int32_t> fin;
+    const int32_t* final_seq = pred_seq.ptr;
+    if (smooth) {
+      fin = DevBuf<int32_t>(m, st);
+      smooth_labels_device(ctx, st, pred_seq.ptr, m, smooth_window, fin.ptr);
+      final_seq = fin.ptr;
+    }
+    DevBuf<unsigned long long> counts(8, st);
+    confusion_device(ctx, st, final_seq, truth_seq.ptr, m, positive_class, counts.ptr);
+    episodes_device(ctx, st, final_seq, truth_seq.ptr, m, positive_class, counts.ptr + 5);
+    unsigned long long h[8];
+    counts.download(h);
+    if (tested_rows) ck(cudaMemcpyAsync(tested_rows, tested.ptr, m * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    if (truth) ck(cudaMemcpyAsync(truth, truth_seq.ptr, m * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    if (predicted) ck(cudaMemcpyAsync(predicted, pred_seq.ptr, m * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    if (final_labels) ck(cudaMemcpyAsync(final_labels, final_seq, m * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    sync(ctx);
+    if (report) fill_report(h, h + 5, m, report);
+    if (n_tested) *n_tested = m;
   });
 }
 

@@ -414,6 +414,62 @@ def hamming_distance(a: PackedBitMatrix, row_a: int, b: PackedBitMatrix, row_b: 
     return hamming_distance_words(a.words[row_a], b.words[row_b], a.dim)
 
 
+@dataclass
+class EpisodeCounts:  # eval.hpp:13-17
+    detected: int = 0
+    total: int = 0
+    false_positive: int = 0
+
+
+@dataclass
+class EvalReport:
+    """eval.hpp:26-37: absent ratios are None (the reference's std::nullopt)."""
+
+    tp: int = 0
+    fp: int = 0
+    tn: int = 0
+    fn: int = 0
+    accuracy: float = 0.0
+    tpr: float | None = None
+    ppv: float | None = None
+    f1: float | None = None
+    episodes: EpisodeCounts | None = None
+
+    @classmethod
+    def _from_c(cls, r: "N.EvalReportC", episodes: bool) -> "EvalReport":
+        return cls(int(r.tp), int(r.fp), int(r.tn), int(r.fn), r.accuracy, r.tpr if r.has_tpr else None,
+                   r.ppv if r.has_ppv else None, r.f1 if r.has_f1 else None,
+                   EpisodeCounts(int(r.episodes_detected), int(r.episodes_total), int(r.episodes_false_positive))
+                   if episodes else None)
+
+
+def smooth_labels(labels, window: int) -> np.ndarray:
+    """eval.cpp:12-37 on the device (prefix-count scan + windowed majority)."""
+    a = np.ascontiguousarray(labels, np.int32)
+    out = np.zeros(max(a.size, 1), np.int32)
+    N.check(N.lib().hv_smooth_labels(_ctx(), _p(a), a.size, window, _p(out)))
+    return out[:a.size]
+
+
+def sample_metrics(pred, truth, positive_class: int) -> EvalReport:
+    """eval.cpp:39-77: confusion counts on the device, ratios as the reference forms them."""
+    p = np.ascontiguousarray(pred, np.int32)
+    t = np.ascontiguousarray(truth, np.int32)
+    r = N.EvalReportC()
+    N.check(N.lib().hv_sample_metrics(_ctx(), _p(p), p.size, _p(t), t.size, positive_class, C.byref(r)))
+    return EvalReport._from_c(r, episodes=False)
+
+
+def episode_metrics(pred, truth, positive_class: int) -> EpisodeCounts:
+    """eval.cpp:79-116: run-level detection counts (one device scan)."""
+    p = np.ascontiguousarray(pred, np.int32)
+    t = np.ascontiguousarray(truth, np.int32)
+    d, n, f = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    N.check(N.lib().hv_episode_metrics(_ctx(), _p(p), p.size, _p(t), t.size, positive_class, C.byref(d),
+                                       C.byref(n), C.byref(f)))
+    return EpisodeCounts(d.value, n.value, f.value)
+
+
 class Dataset:
     """An HBM-resident feature matrix for repeated folds (run_fold_packed,
     experiment.cpp:148-178, with the discretizer re-fit per fold on device)."""
@@ -446,9 +502,73 @@ class Dataset:
                                         _p(mn), _p(mx)))
         return labels[:te.size], mn, mx
 
+    def experiment(self) -> "Experiment":
+        return Experiment(self)
+
     def close(self):
         if self._h:
             N.lib().hv_dataset_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class ExperimentResult:
+    """experiment.hpp ExperimentResult / PredictionRow columns, as arrays."""
+
+    fold_count: int
+    report: EvalReport
+    rows: np.ndarray       # tested row indices, original order
+    truth: np.ndarray
+    predicted: np.ndarray  # raw fold predictions
+    final: np.ndarray      # after smoothing
+
+
+class Experiment:
+    """run_experiment (experiment.cpp:280-345) over an HBM-resident Dataset:
+    every fold scatters its predictions on device; finish() concatenates the
+    tested rows, smooths binary runs and scores them without a host round trip."""
+
+    def __init__(self, ds: Dataset):
+        self.ds = ds
+        self.folds = 0
+        h = C.c_void_p()
+        N.check(N.lib().hv_experiment_create(_ctx(), ds._h, C.byref(h)))
+        self._h = h
+
+    def fold(self, train_idx, test_idx, codebook: Codebook, encode_tiebreak: PackedBitMatrix, cfg: ModelConfig,
+             trainer: str = "classical", batch_size: int = 1024):
+        tr = np.ascontiguousarray(train_idx, np.uint64)
+        te = np.ascontiguousarray(test_idx, np.uint64)
+        mtb = PackedBitMatrix(1, cfg.dim)
+        N.check(N.lib().hv_generate_random(1, cfg.dim, N.lib().hv_derive_seed(cfg.seed, 3), _p(mtb.words)))
+        N.check(N.lib().hv_experiment_fold(_ctx(), self._h, _p(tr), tr.size, _p(te), te.size,
+                                           codebook.bin_count(), _p(codebook.id_vectors.words),
+                                           _p(codebook.value_vectors.words), cfg.dim, codebook.binding,
+                                           _p(encode_tiebreak.words), cfg.class_count, cfg.metric, cfg.gamma,
+                                           _p(mtb.words), 1 if trainer == "online" else 0, batch_size))
+        self.folds += 1
+
+    def finish(self, class_count: int, smooth_window: int = 1, positive_class: int = 1) -> ExperimentResult:
+        rows = self.ds.rows
+        r = N.EvalReportC()
+        m = C.c_uint64()
+        idx = np.zeros(max(rows, 1), np.uint64)
+        truth, pred, fin = (np.zeros(max(rows, 1), np.int32) for _ in range(3))
+        N.check(N.lib().hv_experiment_finish(_ctx(), self._h, class_count, smooth_window, positive_class,
+                                             C.byref(r), C.byref(m), _p(idx), _p(truth), _p(pred), _p(fin)))
+        k = m.value
+        return ExperimentResult(self.folds, EvalReport._from_c(r, episodes=True), idx[:k], truth[:k], pred[:k],
+                                fin[:k])
+
+    def close(self):
+        if self._h:
+            N.lib().hv_experiment_destroy(self._h)
             self._h = None
 
     def __del__(self):
