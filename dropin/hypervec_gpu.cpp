@@ -2,7 +2,8 @@
 //
 // Compiled against the reference's own headers (-I /root/reference/proj/include)
 // it defines the hypervec:: functions of kernels.hpp, encoding.hpp and
-// model.hpp that carry the hot path, each as a thin adapter over the C ABI of
+// model.hpp that carry the hot path (and the eval.hpp scoring of their
+// predictions), each as a thin adapter over the C ABI of
 // libhvb200 (include/hvb200.h): same signatures, same exceptions and messages.
 // Linking this object ahead of the reference library (whose definitions of the
 // same symbols are weakened, see dropin/Makefile) makes every existing caller —
@@ -18,6 +19,7 @@
 #include "hvb200.h"
 #include "hypervec/bitmat.hpp"
 #include "hypervec/encoding.hpp"
+#include "hypervec/eval.hpp"
 #include "hypervec/kernels.hpp"
 #include "hypervec/model.hpp"
 
@@ -240,6 +242,38 @@ std::vector<Prediction> predict(const HDModel& model, const PackedBitMatrix& enc
     out[i].distances.assign(dist.begin() + static_cast<long>(i * C), dist.begin() + static_cast<long>((i + 1) * C));
   }
   return out;
+}
+
+// ------------------------------------------------------------- eval.hpp ----
+std::vector<int> smooth_labels(std::span<const int> labels, std::size_t window) {
+  std::vector<int> out(labels.size());
+  check(hv_smooth_labels(ctx(), reinterpret_cast<const int32_t*>(labels.data()), labels.size(), window,
+                         reinterpret_cast<int32_t*>(out.data())));
+  return out;
+}
+
+EvalReport sample_metrics(std::span<const int> pred, std::span<const int> truth, int positive_class) {
+  hv_eval_report r{};
+  check(hv_sample_metrics(ctx(), reinterpret_cast<const int32_t*>(pred.data()), pred.size(),
+                          reinterpret_cast<const int32_t*>(truth.data()), truth.size(), positive_class, &r));
+  EvalReport out;
+  out.tp = r.tp;
+  out.fp = r.fp;
+  out.tn = r.tn;
+  out.fn = r.fn;
+  out.accuracy = r.accuracy;
+  if (r.has_tpr) out.tpr = r.tpr;
+  if (r.has_ppv) out.ppv = r.ppv;
+  if (r.has_f1) out.f1 = r.f1;
+  return out;
+}
+
+EpisodeCounts episode_metrics(std::span<const int> pred, std::span<const int> truth, int positive_class) {
+  EpisodeCounts e;
+  check(hv_episode_metrics(ctx(), reinterpret_cast<const int32_t*>(pred.data()), pred.size(),
+                           reinterpret_cast<const int32_t*>(truth.data()), truth.size(), positive_class, &e.detected,
+                           &e.total, &e.false_positive));
+  return e;
 }
 
 }  // namespace hypervec

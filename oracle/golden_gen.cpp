@@ -14,6 +14,7 @@
 #include <fstream>
 #include <iostream>
 #include <map>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -21,6 +22,7 @@
 #include "hypervec/data.hpp"
 #include "hypervec/encoding.hpp"
 #include "hypervec/eval.hpp"
+#include "hypervec/io.hpp"
 #include "hypervec/kernels.hpp"
 #include "hypervec/model.hpp"
 #include "hypervec/rng.hpp"
@@ -382,6 +384,53 @@ void gen_eval() {
   }
 }
 
+std::vector<std::uint8_t> bytes_of(const std::string& s) { return {s.begin(), s.end()}; }
+
+// io.cpp:85-107 (HVPB), encoding.cpp:313-330 (HVCB), model.cpp:322-337 (HVMD)
+// written by the reference for the "odd" pipeline (pipeline_odd inputs) and
+// for models whose gamma exercises the JSON number formatting.
+void gen_containers() {
+  Case c("containers");
+  synth::SynthSpec spec;
+  spec.rows = 157;
+  spec.features = 13;
+  spec.classes = 3;
+  spec.seed = 12;
+  Dataset ds = synth::make_synth(spec);
+  const std::size_t rows = 157, F = 13, C = 3, D = 1000, train_rows = 125;
+  Discretizer disc = fit_discretizer(std::span<const double>(ds.X.data(), train_rows * F), train_rows, F, 16);
+  std::vector<std::uint32_t> bins = discretize_matrix(ds.X, rows, disc);
+  Codebook cb = make_codebook(GenerationStrategy::kRandom, BindingStrategy::kIdLevel, F, 16, D, derive_seed(12, 1));
+  PackedBitMatrix etb = generate_random(1, D, derive_seed(12, 2));
+  PackedBitMatrix enc = encode_batch(bins, rows, cb, etb, 2);
+  PackedBitMatrix train(train_rows, D);
+  for (std::size_t r = 0; r < train_rows; ++r) {
+    auto src = enc.row(r);
+    std::copy(src.begin(), src.end(), train.row(r).begin());
+  }
+  std::vector<int> ytrain(ds.y.begin(), ds.y.begin() + static_cast<long>(train_rows));
+  auto dump = [&](const std::string& key, auto&& writer) {
+    std::ostringstream out(std::ios::binary);
+    writer(out);
+    c.put(key, bytes_of(out.str()));
+  };
+  dump("hvpb_encoded", [&](std::ostream& o) { io::write_packed(o, enc); });
+  dump("hvpb_empty", [&](std::ostream& o) { io::write_packed(o, PackedBitMatrix(0, 37)); });
+  dump("hvcb_random", [&](std::ostream& o) { save_codebook(cb, o); });
+  Codebook cb2 = make_codebook(GenerationStrategy::kSandwich, BindingStrategy::kPermutation, 5, 4, 64, 99);
+  dump("hvcb_sandwich_perm", [&](std::ostream& o) { save_codebook(cb2, o); });
+  ModelConfig cfg{C, D, Metric::kHamming, 0.6, 12};
+  dump("hvmd_classical", [&](std::ostream& o) { save_model(train_classical(train, ytrain, cfg), o); });
+  dump("hvmd_online_b5", [&](std::ostream& o) { save_model(train_online(train, ytrain, 5, cfg), o); });
+  const std::vector<double> gammas = {1.0, 0.1, 1e-05, 123.456, 2.5e-300, 0.30000000000000004, 1e16, 7.0,
+                                      1e15, 1e-4, 123456789012345.6, 0.5, 1e300, 5e-324, 0.0};
+  c.put("gammas", gammas);
+  for (std::size_t g = 0; g < gammas.size(); ++g) {
+    ModelConfig gc{2, 40, g % 2 ? Metric::kCosine : Metric::kHamming, gammas[g], 1000 + g};
+    dump("hvmd_gamma_" + std::to_string(g), [&](std::ostream& o) { save_model(make_empty_model(gc), o); });
+  }
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -402,6 +451,7 @@ int main(int argc, char** argv) {
   gen_online_update();
   gen_synth();
   gen_eval();
+  gen_containers();
   std::cout << "golden vectors written to " << g_root << "\n";
   return 0;
 }

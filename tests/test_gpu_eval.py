@@ -146,3 +146,26 @@ def test_resident_experiment_matches_oracle_protocol(C, trainer, window):
     with pytest.raises(hv.InvalidArgument, match="no test samples produced by split"):
         empty.finish(C, window, 1)
     ds.close()
+
+
+def test_gpu_results_save_byte_identical_to_reference_files():
+    """§8 f4: hypervectors encoded and models trained on the B200, written
+    with the HVPB/HVMD containers, are the reference's files byte for byte."""
+    from paper_2206_04746_b200 import containers as cio
+
+    c, p = Case("containers"), Case("pipeline_odd")
+    F, D, C, tr = 13, 1000, 3, 125
+    cb = hv.make_codebook(0, 0, F, 16, D, hv.derive_seed(12, 1))
+    etb = hv.generate_random(1, D, hv.derive_seed(12, 2))
+    enc = hv.encode_batch(p["bins"], 157, cb, etb)
+    assert cio.write_packed(enc) == bytes(c["hvpb_encoded"].astype(np.uint8))
+    assert cio.save_codebook(cb) == bytes(c["hvcb_random"].astype(np.uint8))
+    train = hv.PackedBitMatrix(tr, D, enc.words[:tr])
+    cfg = hv.ModelConfig(class_count=C, dim=D, metric=0, gamma=0.6, seed=12)
+    y = p["y"][:tr]
+    assert cio.save_model(hv.train_classical(train, y, cfg)) == bytes(c["hvmd_classical"].astype(np.uint8))
+    assert cio.save_model(hv.train_online(train, y, 5, cfg)) == bytes(c["hvmd_online_b5"].astype(np.uint8))
+    # and a reference file loads into a model the GPU predicts with
+    m = cio.load_model(bytes(c["hvmd_classical"].astype(np.uint8)))
+    labels, _ = hv.predict_arrays(m, hv.PackedBitMatrix(157 - tr, D, enc.words[tr:]))
+    np.testing.assert_array_equal(labels, p["classical_pred"])
