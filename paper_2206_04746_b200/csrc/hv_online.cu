@@ -37,6 +37,7 @@
 // Touched classes are re-binarised with the batch's final weight
 // (model.cpp:139-163, 277-279).
 #include <cooperative_groups.h>
+#include <cuda_pipeline.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -522,6 +523,166 @@ __global__ void __launch_bounds__(kOThreads, 2) online_persistent_kernel(OnlineP
   }
 }
 
+// ---------------------------------------------------- small batches ----
+// Small batches (the UCI-HAR batch sweep down to one sample): the persistent
+// kernel's grid barriers (~3 us each, two per batch) dominate there. One
+// thread-block cluster of kClCTAs CTAs runs every batch instead, with one
+// cluster barrier per batch. CTA q owns a slice of the words, i.e. of the
+// accumulator columns and class-vector words, and keeps both slices resident
+// in shared memory for the whole run (written back once at the end):
+//   1. the batch rows' slice is already staged (cp.async, issued during the
+//      previous batch); partial Hamming popcounts of every (row, class) pair
+//      over the slice are added into every CTA's totals through distributed
+//      shared memory (batch-parity double buffer);
+//   2. cluster barrier; every CTA derives the same predictions and add values
+//      (model.cpp:259-276), per-class row lists in sample order, and class
+//      weights / counts in that order;
+//   3. every touched class: each thread replays the list on its elements of
+//      the slice (independent chains, sample order per element) and
+//      re-binarises them with the batch's final weight (model.cpp:139-163).
+// Bit-identical to the reference like every other mode.
+constexpr uint32_t kClCTAs = 8, kClThreads = 1024, kClMaxRows = 64, kClMaxC = 32, kClR = 4;
+constexpr size_t kClDefaultRows = 16;  // measured crossover with the persistent kernel
+
+__global__ void __cluster_dims__(kClCTAs, 1, 1) __launch_bounds__(kClThreads, 1)
+    online_cluster_kernel(OnlineParams p) {
+  cg::cluster_group cluster = cg::this_cluster();
+  // dynamic: accs (C x ws*32 doubles) | xs (2 x nmax x ws words) | cvs (C x ws words)
+  extern __shared__ __align__(16) uint8_t dyn[];
+  __shared__ uint32_t tot[2][kClMaxRows][kClMaxC];
+  __shared__ double vt[kClMaxRows], vp[kClMaxRows], wsm[kClMaxC];
+  __shared__ int32_t ct[kClMaxRows], cp[kClMaxRows];
+  __shared__ uint8_t lrow[kClMaxC][kClMaxRows];
+  __shared__ double lv[kClMaxC][kClMaxRows];
+  __shared__ uint32_t llen[kClMaxC];
+  __shared__ unsigned long long cnt[kClMaxC];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t q = cluster.block_rank();
+  const uint32_t W = p.W, C = p.C, D = p.D;
+  const uint32_t ws = (W + kClCTAs - 1) / kClCTAs;  // words per CTA
+  const uint32_t w0 = min(W, q * ws), w1 = min(W, w0 + ws), nw = w1 - w0;
+  const uint32_t nmax = static_cast<uint32_t>(p.bsz);
+  const uint32_t E = ws * 32u;  // accumulator elements per class in the slice
+  double* accs = reinterpret_cast<double*>(dyn);
+  uint32_t* xsb = reinterpret_cast<uint32_t*>(accs + static_cast<size_t>(C) * E);
+  uint32_t* cvs = xsb + 2 * nmax * ws;
+  for (uint32_t k = tid; k < C * E; k += kClThreads) {
+    const uint32_t c = k / E, e = k % E, j = w0 * 32u + e;
+    accs[k] = (e < nw * 32u && j < D) ? p.acc[static_cast<uint64_t>(c) * D + j] : 0.0;
+  }
+  for (uint32_t k = tid; k < C * nw; k += kClThreads) cvs[(k / nw) * ws + k % nw] = p.cv[(k / nw) * W + w0 + k % nw];
+  for (uint32_t k = tid; k < 2 * kClMaxRows * kClMaxC; k += kClThreads) (&tot[0][0][0])[k] = 0;
+  if (tid < C) {
+    wsm[tid] = p.weight[tid];
+    cnt[tid] = p.counts[tid];
+  }
+  auto stage = [&](uint64_t b, uint32_t buf) {  // rows [b, b + n) of the slice, asynchronously
+    const uint32_t n = static_cast<uint32_t>(min(p.bsz, p.rows - b));
+    uint32_t* xs = xsb + buf * nmax * ws;
+    for (uint32_t k = tid; k < n * nw; k += kClThreads) {
+      __pipeline_memcpy_async(xs + (k / nw) * ws + k % nw, p.enc + (b + k / nw) * W + w0 + k % nw, 4);
+    }
+    __pipeline_commit();
+  };
+  stage(0, 0);
+  cluster.sync();  // every CTA's totals are zero before anyone adds
+  uint32_t par = 0;
+  for (uint64_t b0 = 0; b0 < p.rows; b0 += p.bsz, par ^= 1u) {
+    const uint32_t n = static_cast<uint32_t>(min(p.bsz, p.rows - b0));
+    const uint32_t* xs = xsb + par * nmax * ws;
+    __pipeline_wait_prior(0);
+    __syncthreads();
+    if (b0 + p.bsz < p.rows) stage(b0 + p.bsz, par ^ 1u);  // lands during this batch
+    for (uint32_t pr = warp; pr < n * C; pr += kClThreads / 32) {
+      const uint32_t r = pr / C, c = pr % C;
+      uint32_t a = 0;
+      for (uint32_t w = lane; w < nw; w += 32) a += __popc(xs[r * ws + w] ^ cvs[c * ws + w]);
+      a = __reduce_add_sync(kFull, a);
+      if (lane < kClCTAs && a) atomicAdd(cluster.map_shared_rank(&tot[par][r][c], lane), a);
+    }
+    cluster.sync();
+    if (tid < n) {  // pick_label (strict <, lowest class on ties), score_to_delta
+      const int32_t y = p.labels[b0 + tid];
+      uint32_t best = tot[par][tid][0], bc = 0;
+      for (uint32_t c = 1; c < C; ++c) {
+        if (tot[par][tid][c] < best) {
+          best = tot[par][tid][c];
+          bc = c;
+        }
+      }
+      ct[tid] = y;
+      vt[tid] = delta_of(tot[par][tid][y], D);
+      const bool wrong = static_cast<int32_t>(bc) != y;
+      cp[tid] = wrong ? static_cast<int32_t>(bc) : -1;
+      vp[tid] = wrong ? penalty_of((static_cast<unsigned long long>(best) << 32) | bc, p.gamma, D) : 0.0;
+    }
+    __syncthreads();
+    if (tid < C) {  // class tid: its rows in sample order; weight and count over its true samples
+      uint32_t m = 0;
+      double wsum = wsm[tid];
+      for (uint32_t r = 0; r < n; ++r) {
+        if (ct[r] == static_cast<int32_t>(tid)) {
+          lrow[tid][m] = static_cast<uint8_t>(r);
+          lv[tid][m++] = vt[r];
+          wsum = __dadd_rn(wsum, vt[r]);
+          cnt[tid] += 1;
+        } else if (cp[r] == static_cast<int32_t>(tid)) {
+          lrow[tid][m] = static_cast<uint8_t>(r);
+          lv[tid][m++] = vp[r];
+        }
+      }
+      llen[tid] = m;
+      wsm[tid] = wsum;
+    } else if (tid >= 64) {  // this batch's totals are consumed: zero them for batch b + 2
+      for (uint32_t k = tid - 64; k < n * kClMaxC; k += kClThreads - 64) (&tot[par][0][0])[k] = 0;
+    }
+    __syncthreads();
+    const uint32_t R = (nw * 32u + kClThreads - 1) / kClThreads;
+    for (uint32_t c = 0; c < C; ++c) {
+      const uint32_t m = llen[c];
+      if (m == 0) continue;  // untouched: not re-binarised (uniform)
+      double* ac = accs + static_cast<size_t>(c) * E;
+      double a[kClR];
+#pragma unroll
+      for (uint32_t k = 0; k < kClR; ++k) a[k] = (k < R && k * (kClThreads / 32) + warp < nw) ? ac[k * kClThreads + tid] : 0.0;
+      for (uint32_t e = 0; e < m; ++e) {
+        const uint32_t* x = xs + lrow[c][e] * ws;
+        const double v = lv[c][e];
+#pragma unroll
+        for (uint32_t k = 0; k < kClR; ++k) {
+          const uint32_t w = k * (kClThreads / 32) + warp;  // local word
+          if (k < R && w < nw && ((x[w] >> lane) & 1u)) a[k] = __dadd_rn(a[k], v);
+        }
+      }
+      const double total = wsm[c];
+#pragma unroll
+      for (uint32_t k = 0; k < kClR; ++k) {
+        if (k >= R) break;
+        const uint32_t w = k * (kClThreads / 32) + warp, j = (w0 + w) * 32u + lane;
+        uint32_t bit = 0;
+        if (w < nw && j < D) {
+          ac[k * kClThreads + tid] = a[k];
+          const double twice = 2.0 * a[k];
+          bit = twice > total ? 1u : (twice < total ? 0u : ((p.tie[w0 + w] >> lane) & 1u));
+        }
+        const uint32_t word = __ballot_sync(kFull, bit);
+        if (lane == 0 && w < nw) cvs[c * ws + w] = word;
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t k = tid; k < C * E; k += kClThreads) {
+    const uint32_t c = k / E, e = k % E, j = w0 * 32u + e;
+    if (e < nw * 32u && j < D) p.acc[static_cast<uint64_t>(c) * D + j] = accs[k];
+  }
+  for (uint32_t k = tid; k < C * nw; k += kClThreads) p.cv[(k / nw) * W + w0 + k % nw] = cvs[(k / nw) * ws + k % nw];
+  if (q == 0 && tid < C) {
+    p.weight[tid] = wsm[tid];
+    p.counts[tid] = cnt[tid];
+  }
+  cluster.sync();  // no CTA leaves while a peer may still add into its shared memory
+}
+
 __global__ void weight_copy_kernel(const double* __restrict__ src, double* __restrict__ dst, uint32_t C) {
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c < C) dst[c] = src[c];
@@ -548,6 +709,34 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   if (rows == 0) return;
   const size_t W = words_per_row(D);
   const size_t n = std::min(bsz, rows);
+  // small batches: one cluster, no grid barriers (HVB200_ONLINE_CLUSTER=0 disables, =N sets the row limit)
+  const char* cl_env = getenv("HVB200_ONLINE_CLUSTER");
+  const size_t cl_rows = cl_env ? static_cast<size_t>(atoi(cl_env)) : kClDefaultRows;
+  const size_t ws = (W + kClCTAs - 1) / kClCTAs;
+  const size_t cl_smem = C * ws * 32 * sizeof(double) + (2 * n + C) * ws * sizeof(uint32_t);
+  if (n <= std::min<size_t>(cl_rows, kClMaxRows) && C <= kClMaxC && ws * 32 <= kClR * kClThreads &&
+      cl_smem <= (180u << 10)) {
+    OnlineParams p{};
+    p.enc = enc;
+    p.labels = labels;
+    p.rows = rows;
+    p.D = static_cast<uint32_t>(D);
+    p.W = static_cast<uint32_t>(W);
+    p.C = static_cast<uint32_t>(C);
+    p.bsz = n;
+    p.gamma = gamma;
+    p.tie = tie;
+    p.acc = acc;
+    p.weight = weight;
+    p.counts = counts;
+    p.cv = cv;
+    ck(cudaFuncSetAttribute(online_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(cl_smem)),
+       "cudaFuncSetAttribute");
+    online_cluster_kernel<<<kClCTAs, kClThreads, cl_smem, st>>>(p);
+    launched("online_cluster_kernel");
+    return;
+  }
   // MERGED also for tiny batches: streaming a few rows per item is cheaper
   // than the extra grid barrier of the list phase
   const bool merged = C <= kMergedMaxC || n <= 32;

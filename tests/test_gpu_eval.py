@@ -123,15 +123,18 @@ def test_resident_experiment_matches_oracle_protocol(C, trainer, window):
     predicted = np.full(n, -1, np.int32)
     # tscv-like: expanding train window, next block tested; one block re-tested (last fold wins)
     folds = [(np.arange(0, 300), np.arange(300, 500)), (np.arange(0, 500), np.arange(500, 800)),
-             (np.arange(0, 800), np.arange(800, 1000)), (np.arange(0, 700), np.arange(700, 800))]
+             (np.arange(0, 800), np.arange(800, 1000)), (np.arange(0, 700), np.arange(700, 800)),
+             # rows listed twice in one fold (both copies get the same label, as in the reference loop)
+             (np.arange(0, 350), np.concatenate([np.arange(1100, 1200), np.arange(1150, 1200)[::-1]]))]
     for tr, te in folds:
         ex.fold(tr, te, cb, etb, cfg, trainer, 64)
-        predicted[te] = _oracle_fold(X, y, tr, te, cb, etb, mtb, C, B, D, trainer, 0, 1.0, 64)
+        for r, lab in zip(te, _oracle_fold(X, y, tr, te, cb, etb, mtb, C, B, D, trainer, 0, 1.0, 64)):
+            predicted[r] = lab  # experiment.cpp:307-309 order
     res = ex.finish(C, window, 1)
     tested = np.nonzero(predicted >= 0)[0]
     pred_seq, truth_seq = predicted[tested], y[tested]
     final = O.smooth_labels(pred_seq, window) if (C == 2 and window > 1) else pred_seq
-    assert res.fold_count == 4
+    assert res.fold_count == 5
     np.testing.assert_array_equal(res.rows, tested)
     np.testing.assert_array_equal(res.truth, truth_seq)
     np.testing.assert_array_equal(res.predicted, pred_seq)

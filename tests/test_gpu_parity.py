@@ -368,6 +368,32 @@ def test_online_modes_vs_oracle_bitexact(C, D, n, bsz):
     np.testing.assert_array_equal(on.class_vectors.words, oo.class_vectors)
 
 
+@pytest.mark.parametrize("C,D,n,bsz", [(1, 100, 50, 1), (2, 10000, 300, 1), (6, 10000, 400, 5), (6, 1000, 257, 16),
+                                        (26, 2048, 200, 7), (32, 333, 130, 64), (3, 31, 90, 4), (13, 8192, 100, 33),
+                                        (6, 20000, 120, 2)])
+def test_online_cluster_path_vs_oracle_bitexact(C, D, n, bsz, monkeypatch):
+    """The small-batch cluster trainer (one 8-CTA cluster, word slices resident
+    in shared memory, DSMEM popcount reduction), forced for batches up to 64
+    rows: accumulators, weights, counts and class vectors bit-exact vs the
+    oracle — including slices narrower than a CTA's threads and D % 32 != 0.
+    Shapes whose slices do not fit shared memory fall back to the persistent
+    kernel and must agree just the same."""
+    monkeypatch.setenv("HVB200_ONLINE_CLUSTER", "64")
+    rng = np.random.default_rng(C * 77 + bsz + D)
+    centers = rng.integers(0, 2, (C, D), dtype=np.uint8)
+    y = rng.integers(0, C, n).astype(np.int32)
+    enc = O.pack_rows(centers[y] ^ (rng.random((n, D)) < 0.3).astype(np.uint8))
+    cfg = hv.ModelConfig(class_count=C, dim=D, gamma=0.7, seed=C + D + 1)
+    before = launch_count()
+    on = hv.train_online(P(enc, D), y, bsz, cfg)
+    assert launch_count() > before
+    oo = O.NaiveModel(C, D, on.tiebreak.words, O.HAMMING, 0.7).train_online(enc, y, bsz)
+    np.testing.assert_array_equal(on.accumulators.reshape(C, D), oo.acc)
+    np.testing.assert_array_equal(on.class_weight, oo.weight)
+    np.testing.assert_array_equal(on.sample_counts, oo.counts)
+    np.testing.assert_array_equal(on.class_vectors.words, oo.class_vectors)
+
+
 @pytest.mark.parametrize("popc", ["0", "1", "imma"])
 @pytest.mark.parametrize("C,D,n", [(32, 1000, 257), (33, 64, 100), (100, 4096, 300), (64, 10000, 70), (40, 31, 33),
                                    (129, 500, 40), (200, 96, 77), (64, 33, 300), (100, 1000, 129)])
