@@ -1,3 +1,5 @@
+"""Small-batch online training: persistent cooperative kernel vs the cluster trainer
+(UCI-HAR shape, batch 1..64); prints one JSON line per batch size. GPU only."""
 import os, sys, json, torch
 sys.path.insert(0, os.getcwd())
 from paper_2206_04746_b200 import device as dv
