@@ -45,16 +45,21 @@ def split(rows):
 
 
 def timed(fn, reps=1):
+    """Median of `reps` individually timed calls after two warm-up calls (the
+    first call of a path pays lazy module loading and memory-pool growth)."""
     s = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    fn()  # warm-up
+    fn()
+    fn()
     torch.cuda.synchronize()
-    e0.record(s)
-    for _ in range(reps):
+    times = []
+    for _ in range(max(reps, 1)):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
         out = fn()
-    e1.record(s)
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps, out
+        e1.record(s)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    return sorted(times)[len(times) // 2], out
 
 
 def ref_cpu(F, C, D, rows, trainer, batch, label_kind, target_s=8.0):
@@ -78,7 +83,7 @@ def ref_cpu(F, C, D, rows, trainer, batch, label_kind, target_s=8.0):
             "encode_s": r["encode_s"], "train_s": r["train_s"], "predict_s": r["predict_s"]}
 
 
-def one(tag, F, C, D, rows, trainer, batch, label_kind=0, cpu=True, reps=2):
+def one(tag, F, C, D, rows, trainer, batch, label_kind=0, cpu=True, reps=3):
     W = (D + 31) // 32
     ntr, nte = split(rows)
     cbk = dv.DeviceCodebook.make(F, 16, D, seed=1)
