@@ -210,10 +210,13 @@ void destroy_stager(hv_context* ctx) {
 }
 
 size_t stage_chunk_rows(size_t rows, size_t F) {
-  // ~96 MB of uint8 per slot: a chunk is several encoder waves, three slots
-  // of pinned memory stay ~300 MB
+  // ~32 MB of uint8 per slot (a chunk is still several encoder waves): the
+  // e2e CHB-MIT fold measured 54.8 M dp/s at 32 MB vs 53.7 M at 96 MB and
+  // 48.0 M at 384 MB (shorter head and tail of the pipeline)
   const size_t ldb = bins_pitch(F);
-  return std::max<size_t>(1, std::min<size_t>(std::max<size_t>(rows, 1), (size_t(96) << 20) / ldb));
+  size_t mb = 32;
+  if (const char* e = getenv("HVB200_STAGE_MB")) mb = std::max<size_t>(1, static_cast<size_t>(atoll(e)));  // tuning
+  return std::max<size_t>(1, std::min<size_t>(std::max<size_t>(rows, 1), (mb << 20) / ldb));
 }
 
 uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, size_t F, size_t B, size_t D,
