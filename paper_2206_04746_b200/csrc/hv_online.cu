@@ -367,16 +367,33 @@ __device__ void build_lists(const OnlineParams& p, const unsigned long long* bes
     double wsum = p.weight[c];
     uint64_t ntrue = 0;
     uint32_t len = 0;
+    // the next chunk's label / key / true-class popcount are loaded while this
+    // chunk is compacted (the chunks were latency-bound on these loads)
+    int32_t y_n = -1;
+    unsigned long long b_n = 0;
+    uint32_t t_n = 0;
+    auto fetch = [&](uint32_t ch) {
+      const uint32_t r = ch + tid;
+      y_n = -1;
+      if (tid < kLChunk && r < n) {
+        y_n = p.labels[b0 + r];
+        b_n = bestv[r];
+        t_n = p.truep[r];
+      }
+    };
+    fetch(0);
     for (uint32_t ch = 0; ch < n; ch += kLChunk) {
+      const int32_t y = y_n;
+      const unsigned long long bst = b_n;
+      const uint32_t tp = t_n;
+      if (ch + kLChunk < n) fetch(ch + kLChunk);
       bool is_t = false, is_p = false;
       double v = 0.0;
       const uint32_t r = ch + tid;
       if (tid < kLChunk && r < n) {
-        const int32_t y = p.labels[b0 + r];
-        const unsigned long long bst = bestv[r];
         is_t = y == static_cast<int32_t>(c);
         is_p = !is_t && static_cast<uint32_t>(bst) == c;
-        if (is_t) v = delta_of(p.truep[r], p.D);
+        if (is_t) v = delta_of(tp, p.D);
         if (is_p) v = penalty_of(bst, p.gamma, p.D);
       }
       const bool flag = is_t || is_p;
