@@ -111,8 +111,49 @@ __device__ __forceinline__ double penalty_of(unsigned long long best, double gam
 }
 
 // ---------------------------------------------------------------- score ----
+// short rows (W <= 64) and up to kWarpC classes: the row word is loaded once
+// per step and every class's word of that step is in flight together (one
+// accumulator per class, reduced at the end) instead of one latency-bound
+// pass per class. Measured: MNIST-shaped D = 1024 score phase 5.1 -> 2.9 us
+// per batch; slower for long rows (D = 10000: 11.8 -> 14.6), which keep the
+// per-class passes.
+constexpr uint32_t kWarpC = 16;
+
 __device__ void score_warp_per_row(const OnlineParams& p, unsigned long long* best_out, uint64_t b0, uint32_t n,
                                    uint64_t gwarp, uint64_t gwarps, uint32_t lane) {
+  if (p.C <= kWarpC && p.W <= 64) {
+    for (uint64_t r = gwarp; r < n; r += gwarps) {
+      const uint32_t* q = p.enc + (b0 + r) * p.W;
+      const int32_t y = p.labels[b0 + r];
+      uint32_t a[kWarpC];
+#pragma unroll
+      for (uint32_t c = 0; c < kWarpC; ++c) a[c] = 0;
+      for (uint32_t w = lane; w < p.W; w += 32u) {
+        const uint32_t x = __ldg(q + w);
+#pragma unroll
+        for (uint32_t c = 0; c < kWarpC; ++c) {
+          if (c < p.C) a[c] += __popc(x ^ p.cv[static_cast<uint64_t>(c) * p.W + w]);
+        }
+      }
+      uint32_t best = 0, bestp = kFull, truep = 0;
+#pragma unroll
+      for (uint32_t c = 0; c < kWarpC; ++c) {
+        if (c < p.C) {
+          const uint32_t t = __reduce_add_sync(kFull, a[c]);
+          if (t < bestp) {  // strict: the lowest class wins ties (model.cpp:96-104)
+            bestp = t;
+            best = c;
+          }
+          if (static_cast<int32_t>(c) == y) truep = t;
+        }
+      }
+      if (lane == 0) {
+        best_out[r] = (static_cast<unsigned long long>(bestp) << 32) | best;
+        p.truep[r] = truep;
+      }
+    }
+    return;
+  }
   for (uint64_t r = gwarp; r < n; r += gwarps) {
     const uint32_t* q = p.enc + (b0 + r) * p.W;
     const int32_t y = p.labels[b0 + r];
