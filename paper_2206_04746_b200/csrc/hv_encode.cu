@@ -270,10 +270,11 @@ void encode_device(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, size_
   if (wcount != W || ldo != W) {
     // a column slice: the fused encoder writes it directly; other bindings
     // encode whole rows into scratch and copy the slice out
-    if (binding == HV_BIND_ID_LEVEL && allow_fast &&
+    if ((binding == HV_BIND_ID_LEVEL || binding == HV_BIND_PERMUTATION) && allow_fast &&
         launch_tt(ctx, st, bins8, static_cast<uint32_t>(ldb), rows, static_cast<uint32_t>(F), id, val,
                   static_cast<uint32_t>(B), static_cast<uint32_t>(D), static_cast<uint32_t>(W), tie, out,
-                  static_cast<uint32_t>(w0), static_cast<uint32_t>(wcount), static_cast<uint32_t>(ldo))) {
+                  static_cast<uint32_t>(w0), static_cast<uint32_t>(wcount), static_cast<uint32_t>(ldo),
+                  binding == HV_BIND_PERMUTATION)) {
       return;
     }
     DevBuf<uint32_t> full(rows * W, st);
@@ -294,6 +295,12 @@ void encode_device(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, size_
                             out);
       return;
     case HV_BIND_PERMUTATION:
+      // the table encoder with rotated level vectors as its bound words
+      if (allow_fast && launch_tt(ctx, st, bins8, static_cast<uint32_t>(ldb), rows, static_cast<uint32_t>(F), id, val,
+                                  static_cast<uint32_t>(B), static_cast<uint32_t>(D), static_cast<uint32_t>(W), tie, out,
+                                  0u, static_cast<uint32_t>(W), static_cast<uint32_t>(W), true)) {
+        return;
+      }
       launch_generic<true>(ctx, st, hs_high_planes(F), bins8, static_cast<uint32_t>(ldb), rows,
                            static_cast<uint32_t>(F), id, val, static_cast<uint32_t>(D), static_cast<uint32_t>(W), tie,
                            out);

@@ -57,6 +57,7 @@ struct TT6Params {
   uint32_t block_rows;  // rows per work item
   uint64_t blocks;      // ceil(rows / block_rows)
   unsigned int* counter;
+  uint32_t perm;        // permutation binding: bound word = rotate(V_b, f) (encoding.cpp:273-279)
 };
 
 template <int NW>
@@ -126,16 +127,23 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
     const uint64_t block = item / p.slices;
     const uint32_t wb = slice * NW;  // first local output word of the slice
     if (slice != cur_slice) {
-      // entry (f, b): NW words ID_f[w] ^ V_b[w], w = w0+wb+j; zero for f >= F, b >= B, past the range
+      // entry (f, b): NW bound words (ID_f[w] ^ V_b[w], or rotate(V_b, f)[w]), w = w0+wb+j; zero for f >= F, b >= B, past the range
       for (uint32_t k = threadIdx.x; k < p.F16 * kTBins; k += nthreads) {
         const uint32_t f = k / kTBins, b = k % kTBins;
         uint32_t e[NW];
 #pragma unroll
         for (int j = 0; j < NW; ++j) {
           const uint32_t w = p.w0 + wb + j;
-          e[j] = (wb + j < p.wcount && f < p.F && b < p.B)
-                     ? __ldg(p.id + static_cast<uint64_t>(f) * p.W + w) ^ __ldg(p.val + static_cast<uint64_t>(b) * p.W + w)
-                     : 0u;
+          if (wb + j < p.wcount && f < p.F && b < p.B) {
+            // id-level: ID_f ^ V_b; permutation: word w of V_b rotated by f (bits past D are
+            // masked at the output)
+            e[j] = p.perm ? get_bits_cyclic(p.val + static_cast<uint64_t>(b) * p.W, p.W, p.D,
+                                            (w * 32u + p.D - (f % p.D)) % p.D)
+                          : __ldg(p.id + static_cast<uint64_t>(f) * p.W + w) ^
+                                __ldg(p.val + static_cast<uint64_t>(b) * p.W + w);
+          } else {
+            e[j] = 0u;
+          }
         }
 #pragma unroll
         for (int t = 0; t < NPR; ++t) {
@@ -285,7 +293,7 @@ void launch_tt6_inst(hv_context* ctx, cudaStream_t st, TT6Params p, size_t smem)
 
 bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
                const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
-               uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo, uint32_t* counter) {
+               uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo, uint32_t* counter, bool perm) {
   const uint32_t F16 = (F + 15) / 16 * 16;
   // planes above the six HS levels: counts < 64 * 2^NH; instantiated NH in {3, 4, 6}
   int nh = 0;
@@ -325,7 +333,7 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
   }
   if (const char* br_env = getenv("HVB200_TT_BLOCK_ROWS")) block_rows = static_cast<uint32_t>(atoi(br_env));
   TT6Params p{bins8, ldb, rows, F, F16, D, W, B, id, val, tie, out, w0, wcount, ldo, slices, block_rows,
-              (rows + block_rows - 1) / block_rows, counter};
+              (rows + block_rows - 1) / block_rows, counter, perm ? 1u : 0u};
 #define HV_TT6(NPR, G, MB, N)                                            \
   if (s.npr == NPR && s.g == G && s.minb == MB && nh == N) {             \
     launch_tt6_inst<NPR, G, N, MB>(ctx, st, p, smem);                    \
@@ -345,13 +353,13 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
 
 bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
                const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
-               uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo) {
+               uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo, bool perm) {
   if (B > static_cast<uint32_t>(kTBins) || F == 0 || rows == 0 || wcount == 0) return false;
   if (ldb % kChunk != 0 || (reinterpret_cast<uintptr_t>(bins8) & 15u)) return false;
   // one work counter per launch from the context's ring (concurrent launches on
   // the context's two streams must not share one)
   unsigned int* counter = ctx->d_counters + (ctx->next_counter++ % hv_context::kCounters);
-  return launch_v6(ctx, st, bins8, ldb, rows, F, id, val, B, D, W, tie, out, w0, wcount, ldo, counter);
+  return launch_v6(ctx, st, bins8, ldb, rows, F, id, val, B, D, W, tie, out, w0, wcount, ldo, counter, perm);
 }
 
 }  // namespace hvb

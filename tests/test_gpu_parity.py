@@ -198,13 +198,16 @@ def test_permutation_and_appending_vs_oracle(binding, D):
     np.testing.assert_array_equal(got.words, want)
 
 
-def test_encode_fast_and_generic_kernels_agree_at_scale():
+@pytest.mark.parametrize("binding", [0, 1])
+def test_encode_fast_and_generic_kernels_agree_at_scale(binding):
     """Size-independent property at bench scale: both device encoders give
-    identical words for 200k CHB-MIT-shaped rows; a sample is oracle-checked."""
+    identical words for 200k CHB-MIT-shaped rows, for ID-level and for
+    permutation binding (the table encoder with rotated level vectors); a
+    sample is oracle-checked."""
     from paper_2206_04746_b200 import device as dv
     import os
     F, B, D, C, rows = 342, 16, 10000, 2, 200_000
-    cbk = dv.DeviceCodebook.make(F, B, D, seed=3)
+    cbk = dv.DeviceCodebook.make(F, B, D, seed=3, binding=binding)
     eng = dv.Engine(cbk, C)
     bins8, labels = eng.synth(0, rows, 1, 7)
     fast = eng.encode(bins8)
@@ -220,7 +223,7 @@ def test_encode_fast_and_generic_kernels_agree_at_scale():
     ref_b, _ = O.synth_c(0, rows, F, C, B, 1, 7)
     np.testing.assert_array_equal(b, ref_b[idx])
     want = O.encode_batch(b, cbk.id_vectors.cpu().numpy().view(np.uint32), cbk.value_vectors.cpu().numpy().view(np.uint32),
-                          B, D, O.BIND_ID_LEVEL, cbk.encode_tiebreak.cpu().numpy().view(np.uint32))
+                          B, D, binding, cbk.encode_tiebreak.cpu().numpy().view(np.uint32))
     np.testing.assert_array_equal(fast[idx].cpu().numpy().view(np.uint32), want)
 
 
