@@ -94,7 +94,18 @@ struct OnlineParams {
   uint32_t* arrive;            // per (row tile, class block) arrival counters (ksplit > 1)
   uint32_t* pre;               // optional: bsz x C popcounts of the (single) batch, precomputed;
                                // zeroed as read, and best[0, bsz) is reset after the batch
+  uint32_t* wflag;             // MERGED: per-class epoch flags of the separate weight tasks (nullable)
 };
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* ptr) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_u32(uint32_t* ptr, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -323,6 +334,46 @@ __device__ void replay_merged(const OnlineParams& p, const unsigned long long* b
   const uint32_t tid = threadIdx.x, lane = tid & 31u;
   const uint32_t nwb = (p.W + RTile<COLS>::kWords - 1) / RTile<COLS>::kWords;
   const uint64_t items = static_cast<uint64_t>(p.C) * nwb;
+  // With spare CTAs, the class weights (a dependent chain over every true
+  // sample of the batch) run as separate tasks on CTAs without a replay item
+  // and publish through an epoch flag, instead of a weight warp inside every
+  // item whose chain was on the item's critical path.
+  const bool sep = p.wflag != nullptr && gridDim.x >= items + p.C;
+  const uint32_t epoch = static_cast<uint32_t>(b0 / p.bsz) + 1u;
+  if (sep && blockIdx.x >= items && blockIdx.x < items + p.C) {
+    const uint32_t c = static_cast<uint32_t>(blockIdx.x - items);
+    double wsum = p.weight[par * p.C + c];
+    uint64_t ntrue = 0;
+    auto fill = [&](uint32_t ch, uint32_t buf) {  // threads 32.. : delta of the true samples, else +0.0
+      if (tid >= 32 && tid < 32 + kLChunk) {
+        const uint32_t k = tid - 32, r = ch + k;
+        const bool is_t = r < n && p.labels[b0 + r] == static_cast<int32_t>(c);
+        s.val[buf][k] = is_t ? delta_of(p.truep[r], p.D) : 0.0;
+        s.flag[buf][k] = is_t ? 1 : 0;
+      }
+    };
+    fill(0, 0);
+    __syncthreads();
+    uint32_t buf = 0;
+    for (uint32_t ch = 0; ch < n; ch += kLChunk, buf ^= 1u) {
+      if (ch + kLChunk < n) fill(ch + kLChunk, buf ^ 1u);
+      if (tid == 0) {
+        const uint32_t m = min(static_cast<uint32_t>(kLChunk), n - ch);
+#pragma unroll 8
+        for (uint32_t k = 0; k < m; ++k) {
+          wsum = __dadd_rn(wsum, s.val[buf][k]);  // model.cpp:268, sample order
+          ntrue += s.flag[buf][k];
+        }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      p.weight[(par ^ 1u) * p.C + c] = wsum;
+      p.counts[c] += ntrue;
+      __threadfence();
+      st_release_u32(p.wflag + c, epoch);
+    }
+  }
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const uint32_t c = static_cast<uint32_t>(item / nwb);
     const uint32_t wb = static_cast<uint32_t>(item % nwb);
@@ -379,7 +430,7 @@ __device__ void replay_merged(const OnlineParams& p, const unsigned long long* b
       const uint32_t m = min(static_cast<uint32_t>(RTile<COLS>::kChunk), n - ch);
       if (tid < kOReplay) {
         replay_chunk<COLS>(s.words[buf], s.val[buf], m, a);  // non-listed rows carry +0.0
-      } else if (lane == 0) {
+      } else if (lane == 0 && !sep) {
 #pragma unroll 8
         for (uint32_t k = 0; k < m; ++k) {
           const uint8_t f = s.flag[buf][k];
@@ -390,10 +441,20 @@ __device__ void replay_merged(const OnlineParams& p, const unsigned long long* b
       if (more) store_chunk(buf ^ 1u);  // the other buffer was last read before the previous barrier
       __syncthreads();
     }
-    if (tid == kOReplay) s.weight = wsum;
+    if (tid == kOReplay) {
+      if (sep) {  // the weight task of class c publishes the batch's final weight
+        const unsigned long long t0 = gtimer();
+        while (ld_acquire_u32(p.wflag + c) != epoch) {
+          if (gtimer() - t0 > 2000000000ull) __trap();  // 2 s: a lost task is a bug, never a hang
+        }
+        s.weight = p.weight[(par ^ 1u) * p.C + c];
+      } else {
+        s.weight = wsum;
+      }
+    }
     const int touched = __syncthreads_or(mine);
     if (tid < kOReplay) store_columns<COLS>(p, c, wb, a, s.weight, touched != 0);
-    if (wb == 0 && tid == kOReplay) {
+    if (!sep && wb == 0 && tid == kOReplay) {
       p.weight[(par ^ 1u) * p.C + c] = wsum;
       p.counts[c] += ntrue;
     }
@@ -813,10 +874,14 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   const uint64_t iw = cols8 ? 64 : cols4 ? 32 : 8;  // words per replay item
   const uint64_t items = static_cast<uint64_t>(C) * ((W + iw - 1) / iw);
   const uint64_t score_ctas = (n + kOThreads / 32 - 1) / (kOThreads / 32);
-  const uint64_t want = std::max<uint64_t>(items, score_ctas);
+  // MERGED: one extra CTA per class for the separate weight tasks
+  const uint64_t want = std::max<uint64_t>(items + (merged ? C : 0), score_ctas);
+  DevBuf<uint32_t> wflag(merged ? C : 0, st);
+  if (merged) wflag.zero();
   OnlineParams p{enc,     labels,   rows,     static_cast<uint32_t>(D), static_cast<uint32_t>(W),
                  static_cast<uint32_t>(C), n, gamma, tie, acc, wts.ptr, counts, cv, best.ptr, truep.ptr, lidx.ptr,
-                 lval.ptr, llen.ptr, nullptr, lane_class ? 1u : 0u, 1u, nullptr, nullptr, nullptr};
+                 lval.ptr, llen.ptr, nullptr, lane_class ? 1u : 0u, 1u, nullptr, nullptr, nullptr,
+                 merged ? wflag.ptr : nullptr};
   // HVB200_ONLINE_PROFILE=1: print the time per phase (CTA 0's view, barrier waits included)
   const char* pe = getenv("HVB200_ONLINE_PROFILE");
   DevBuf<unsigned long long> prof(pe && pe[0] == '1' ? 3 : 0, st);
