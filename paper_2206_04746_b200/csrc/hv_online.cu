@@ -327,6 +327,70 @@ struct Smem {
   double weight;
 };
 
+// The class weight of class c over the batch's true samples, in sample order
+// (model.cpp:268), and its sample count: threads 32.. stage the deltas of a
+// 256-row chunk (+0.0 for other rows) while thread 0 runs the dependent chain
+// over the previous one; then the result is published to the replay items
+// through the class's epoch flag (release; the items acquire it).
+// LISTS = true: walk the class's list (built by the list phase) instead of
+// every row of the batch; its true entries carry their delta.
+template <bool LISTS>
+__device__ void class_weight_task(const OnlineParams& p, Smem& s, uint64_t b0, uint32_t n, uint32_t c,
+                                  const double* w_in, double* w_out, uint32_t epoch) {
+  const uint32_t tid = threadIdx.x;
+  double wsum = *w_in;
+  uint64_t ntrue = 0;
+  if (LISTS) n = p.llen[c];
+  auto fill = [&](uint32_t ch, uint32_t buf) {
+    if (tid >= 32 && tid < 32 + kLChunk) {
+      const uint32_t k = tid - 32, e = ch + k;
+      bool is_t = false;
+      double v = 0.0;
+      if (e < n) {
+        if (LISTS) {
+          const uint32_t r = p.lidx[static_cast<uint64_t>(c) * p.bsz + e];
+          is_t = p.labels[b0 + r] == static_cast<int32_t>(c);
+          if (is_t) v = p.lval[static_cast<uint64_t>(c) * p.bsz + e];
+        } else {
+          is_t = p.labels[b0 + e] == static_cast<int32_t>(c);
+          if (is_t) v = delta_of(p.truep[e], p.D);
+        }
+      }
+      s.val[buf][k] = v;
+      s.flag[buf][k] = is_t ? 1 : 0;
+    }
+  };
+  fill(0, 0);
+  __syncthreads();
+  uint32_t buf = 0;
+  for (uint32_t ch = 0; ch < n; ch += kLChunk, buf ^= 1u) {
+    if (ch + kLChunk < n) fill(ch + kLChunk, buf ^ 1u);
+    if (tid == 0) {
+      const uint32_t m = min(static_cast<uint32_t>(kLChunk), n - ch);
+#pragma unroll 8
+      for (uint32_t k = 0; k < m; ++k) {
+        wsum = __dadd_rn(wsum, s.val[buf][k]);
+        ntrue += s.flag[buf][k];
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    *w_out = wsum;
+    p.counts[c] += ntrue;
+    __threadfence();
+    st_release_u32(p.wflag + c, epoch);
+  }
+  __syncthreads();  // s reuse
+}
+
+__device__ __forceinline__ void await_class_weight(const OnlineParams& p, uint32_t c, uint32_t epoch) {
+  const unsigned long long t0 = gtimer();
+  while (ld_acquire_u32(p.wflag + c) != epoch) {
+    if (gtimer() - t0 > 2000000000ull) __trap();  // 2 s: a lost task is a bug, never a hang
+  }
+}
+
 // ------------------------------------------------------- MERGED replay ----
 template <int COLS>
 __device__ void replay_merged(const OnlineParams& p, const unsigned long long* bestv, Smem& s, uint64_t b0, uint32_t n,
@@ -342,37 +406,7 @@ __device__ void replay_merged(const OnlineParams& p, const unsigned long long* b
   const uint32_t epoch = static_cast<uint32_t>(b0 / p.bsz) + 1u;
   if (sep && blockIdx.x >= items && blockIdx.x < items + p.C) {
     const uint32_t c = static_cast<uint32_t>(blockIdx.x - items);
-    double wsum = p.weight[par * p.C + c];
-    uint64_t ntrue = 0;
-    auto fill = [&](uint32_t ch, uint32_t buf) {  // threads 32.. : delta of the true samples, else +0.0
-      if (tid >= 32 && tid < 32 + kLChunk) {
-        const uint32_t k = tid - 32, r = ch + k;
-        const bool is_t = r < n && p.labels[b0 + r] == static_cast<int32_t>(c);
-        s.val[buf][k] = is_t ? delta_of(p.truep[r], p.D) : 0.0;
-        s.flag[buf][k] = is_t ? 1 : 0;
-      }
-    };
-    fill(0, 0);
-    __syncthreads();
-    uint32_t buf = 0;
-    for (uint32_t ch = 0; ch < n; ch += kLChunk, buf ^= 1u) {
-      if (ch + kLChunk < n) fill(ch + kLChunk, buf ^ 1u);
-      if (tid == 0) {
-        const uint32_t m = min(static_cast<uint32_t>(kLChunk), n - ch);
-#pragma unroll 8
-        for (uint32_t k = 0; k < m; ++k) {
-          wsum = __dadd_rn(wsum, s.val[buf][k]);  // model.cpp:268, sample order
-          ntrue += s.flag[buf][k];
-        }
-      }
-      __syncthreads();
-    }
-    if (tid == 0) {
-      p.weight[(par ^ 1u) * p.C + c] = wsum;
-      p.counts[c] += ntrue;
-      __threadfence();
-      st_release_u32(p.wflag + c, epoch);
-    }
+    class_weight_task<false>(p, s, b0, n, c, p.weight + par * p.C + c, p.weight + (par ^ 1u) * p.C + c, epoch);
   }
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const uint32_t c = static_cast<uint32_t>(item / nwb);
@@ -443,10 +477,7 @@ __device__ void replay_merged(const OnlineParams& p, const unsigned long long* b
     }
     if (tid == kOReplay) {
       if (sep) {  // the weight task of class c publishes the batch's final weight
-        const unsigned long long t0 = gtimer();
-        while (ld_acquire_u32(p.wflag + c) != epoch) {
-          if (gtimer() - t0 > 2000000000ull) __trap();  // 2 s: a lost task is a bug, never a hang
-        }
+        await_class_weight(p, c, epoch);
         s.weight = p.weight[(par ^ 1u) * p.C + c];
       } else {
         s.weight = wsum;
@@ -463,7 +494,8 @@ __device__ void replay_merged(const OnlineParams& p, const unsigned long long* b
 }
 
 // -------------------------------------------------------- LISTS phases ----
-__device__ void build_lists(const OnlineParams& p, const unsigned long long* bestv, Smem& s, uint64_t b0, uint32_t n) {
+__device__ void build_lists(const OnlineParams& p, const unsigned long long* bestv, Smem& s, uint64_t b0, uint32_t n,
+                            bool sep) {
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   for (uint32_t c = blockIdx.x; c < p.C; c += gridDim.x) {
     double wsum = p.weight[c];
@@ -516,7 +548,7 @@ __device__ void build_lists(const OnlineParams& p, const unsigned long long* bes
         p.lval[static_cast<uint64_t>(c) * p.bsz + len + pos] = v;
       }
       __syncthreads();
-      if (tid == kOReplay) {  // class weight over the true samples, in sample order
+      if (tid == kOReplay && !sep) {  // class weight over the true samples, in sample order
 #pragma unroll 8
         for (uint32_t k = 0; k < m; ++k) {
           const uint8_t f = s.flag[0][k];
@@ -528,18 +560,25 @@ __device__ void build_lists(const OnlineParams& p, const unsigned long long* bes
       __syncthreads();
     }
     if (tid == kOReplay) {
-      p.weight[c] = wsum;
-      p.counts[c] += ntrue;
+      if (!sep) {
+        p.weight[c] = wsum;
+        p.counts[c] += ntrue;
+      }
       p.llen[c] = len;
     }
   }
 }
 
 template <int COLS>
-__device__ void replay_lists(const OnlineParams& p, Smem& s, uint64_t b0) {
+__device__ void replay_lists(const OnlineParams& p, Smem& s, uint64_t b0, uint32_t n, bool sep) {
   const uint32_t tid = threadIdx.x;
   const uint32_t nwb = (p.W + RTile<COLS>::kWords - 1) / RTile<COLS>::kWords;
   const uint64_t items = static_cast<uint64_t>(p.C) * nwb;
+  const uint32_t epoch = static_cast<uint32_t>(b0 / p.bsz) + 1u;
+  if (sep && blockIdx.x >= items && blockIdx.x < items + p.C) {
+    const uint32_t c = static_cast<uint32_t>(blockIdx.x - items);
+    class_weight_task<true>(p, s, b0, n, c, p.weight + c, p.weight + c, epoch);  // LISTS: weights in place
+  }
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const uint32_t c = static_cast<uint32_t>(item / nwb);
     const uint32_t len = p.llen[c];
@@ -583,7 +622,15 @@ __device__ void replay_lists(const OnlineParams& p, Smem& s, uint64_t b0) {
       if (more) store_chunk(buf ^ 1u);
       __syncthreads();
     }
-    if (tid < kOReplay) store_columns<COLS>(p, c, wb, a, p.weight[c], true);
+    if (sep) {
+      if (tid == kOReplay) {
+        await_class_weight(p, c, epoch);
+        s.weight = p.weight[c];
+      }
+      __syncthreads();
+    }
+    if (tid < kOReplay) store_columns<COLS>(p, c, wb, a, sep ? s.weight : p.weight[c], true);
+    if (sep) __syncthreads();  // s.weight reuse by the next item
   }
 }
 
@@ -620,10 +667,12 @@ __global__ void __launch_bounds__(kOThreads, 2) online_persistent_kernel(OnlineP
     if constexpr (MERGED) {
       replay_merged<COLS>(p, bestv, s, b0, n, par);
     } else {
-      build_lists(p, bestv, s, b0, n);
+      const uint64_t litems = static_cast<uint64_t>(p.C) * ((p.W + RTile<COLS>::kWords - 1) / RTile<COLS>::kWords);
+      const bool sep = p.wflag != nullptr && gridDim.x >= litems + p.C;
+      build_lists(p, bestv, s, b0, n, sep);
       grid.sync();
       if (prof) t2 = gtimer();
-      replay_lists<COLS>(p, s, b0);
+      replay_lists<COLS>(p, s, b0, n, sep);
     }
     if (lane_class) {
       // one batch per launch with precomputed popcounts: reset this batch's own keys
@@ -874,14 +923,15 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   const uint64_t iw = cols8 ? 64 : cols4 ? 32 : 8;  // words per replay item
   const uint64_t items = static_cast<uint64_t>(C) * ((W + iw - 1) / iw);
   const uint64_t score_ctas = (n + kOThreads / 32 - 1) / (kOThreads / 32);
-  // MERGED: one extra CTA per class for the separate weight tasks
-  const uint64_t want = std::max<uint64_t>(items + (merged ? C : 0), score_ctas);
-  DevBuf<uint32_t> wflag(merged ? C : 0, st);
-  if (merged) wflag.zero();
+  // one extra CTA per class for the separate weight tasks
+  const uint64_t want = std::max<uint64_t>(items + C, score_ctas);
+  const char* wt_env = getenv("HVB200_ONLINE_WTASK");  // =0: class weights inside the items / list phase
+  const bool wtask = !(wt_env && wt_env[0] == '0');
+  DevBuf<uint32_t> wflag(wtask ? C : 0, st);
+  if (wtask) wflag.zero();
   OnlineParams p{enc,     labels,   rows,     static_cast<uint32_t>(D), static_cast<uint32_t>(W),
                  static_cast<uint32_t>(C), n, gamma, tie, acc, wts.ptr, counts, cv, best.ptr, truep.ptr, lidx.ptr,
-                 lval.ptr, llen.ptr, nullptr, lane_class ? 1u : 0u, 1u, nullptr, nullptr, nullptr,
-                 merged ? wflag.ptr : nullptr};
+                 lval.ptr, llen.ptr, nullptr, lane_class ? 1u : 0u, 1u, nullptr, nullptr, nullptr, wtask ? wflag.ptr : nullptr};
   // HVB200_ONLINE_PROFILE=1: print the time per phase (CTA 0's view, barrier waits included)
   const char* pe = getenv("HVB200_ONLINE_PROFILE");
   DevBuf<unsigned long long> prof(pe && pe[0] == '1' ? 3 : 0, st);
@@ -926,6 +976,7 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
        "online_persistent_kernel");
   };
   if (tc_mode) {
+    p.wflag = nullptr;  // one launch per batch restarts the epochs: weights stay in the list phase
     DevBuf<uint32_t> pre(n * C, st), cpop(C, st);
     DevBuf<uint8_t> img(tc_image_bytes(C, D), st);
     pre.zero();
