@@ -101,7 +101,7 @@ __device__ __forceinline__ uint32_t majority6(const uint32_t (&pl)[6 + NH], uint
   return gt | ((F & 1u) ? 0u : (eq & tie));
 }
 
-template <int NPR, int G, int NH, int MINB>
+template <int NPR, int G, int NH, int MINB, bool PERM>
 __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
   constexpr int NW = 2 * NPR;
   constexpr uint32_t kFeatBytes = NPR * kTBins * 8;  // one feature's entries (all pairs)
@@ -134,15 +134,15 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
 #pragma unroll
         for (int j = 0; j < NW; ++j) {
           const uint32_t w = p.w0 + wb + j;
-          if (wb + j < p.wcount && f < p.F && b < p.B) {
-            // id-level: ID_f ^ V_b; permutation: word w of V_b rotated by f (bits past D are
-            // masked at the output)
-            e[j] = p.perm ? get_bits_cyclic(p.val + static_cast<uint64_t>(b) * p.W, p.W, p.D,
-                                            (w * 32u + p.D - (f % p.D)) % p.D)
-                          : __ldg(p.id + static_cast<uint64_t>(f) * p.W + w) ^
-                                __ldg(p.val + static_cast<uint64_t>(b) * p.W + w);
+          if constexpr (PERM) {  // word w of V_b rotated by f (bits past D are masked at the output)
+            e[j] = (wb + j < p.wcount && f < p.F && b < p.B)
+                       ? get_bits_cyclic(p.val + static_cast<uint64_t>(b) * p.W, p.W, p.D,
+                                         (w * 32u + p.D - (f % p.D)) % p.D)
+                       : 0u;
           } else {
-            e[j] = 0u;
+            e[j] = (wb + j < p.wcount && f < p.F && b < p.B)
+                       ? __ldg(p.id + static_cast<uint64_t>(f) * p.W + w) ^ __ldg(p.val + static_cast<uint64_t>(b) * p.W + w)
+                       : 0u;
           }
         }
 #pragma unroll
@@ -278,7 +278,9 @@ namespace {
 
 template <int NPR, int G, int NH, int MINB>
 void launch_tt6_inst(hv_context* ctx, cudaStream_t st, TT6Params p, size_t smem) {
-  auto kern = encode_tt6_kernel<NPR, G, NH, MINB>;
+  // separate instantiations: the permutation table build must not perturb the
+  // ID-level kernel's code (it cost 1.5 % there as a runtime branch)
+  auto kern = p.perm ? encode_tt6_kernel<NPR, G, NH, MINB, true> : encode_tt6_kernel<NPR, G, NH, MINB, false>;
   ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
      "cudaFuncSetAttribute");
   int per_sm = 0;
