@@ -46,7 +46,7 @@ struct TT6Params {
   const uint8_t* bins8;
   uint32_t ldb;
   uint64_t rows;
-  uint32_t F, F16, D, W, B;
+  uint32_t F, Fpad, D, W, B;  // Fpad: F rounded up to a multiple of 8 (zero table rows)
   const uint32_t* id;
   const uint32_t* val;
   const uint32_t* tie;
@@ -110,10 +110,10 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   constexpr uint32_t nthreads = G * 32;
-  const uint32_t tbytes = p.F16 * kFeatBytes;  // multiple of 256 (F16 % 16 == 0)
+  const uint32_t tbytes = p.Fpad * kFeatBytes;  // multiple of 256 (Fpad % 8 == 0)
   uint32_t* Sw = reinterpret_cast<uint32_t*>(sm6 + tbytes) + warp * (16 * 32);  // [16 words][32 rows]
   const uint64_t items = static_cast<uint64_t>(p.slices) * p.blocks;
-  const uint32_t nchunks = (p.F16 + kChunk - 1) / kChunk;
+  const uint32_t nchunks = (p.Fpad + kChunk - 1) / kChunk;
   uint32_t cur_slice = 0xFFFFFFFFu;
   const uint32_t lr = lane >> 2, lq = lane & 3u;
 
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
     const uint32_t wb = slice * NW;  // first local output word of the slice
     if (slice != cur_slice) {
       // entry (f, b): NW bound words (ID_f[w] ^ V_b[w], or rotate(V_b, f)[w]), w = w0+wb+j; zero for f >= F, b >= B, past the range
-      for (uint32_t k = threadIdx.x; k < p.F16 * kTBins; k += nthreads) {
+      for (uint32_t k = threadIdx.x; k < p.Fpad * kTBins; k += nthreads) {
         const uint32_t f = k / kTBins, b = k % kTBins;
         uint32_t e[NW];
 #pragma unroll
@@ -214,28 +214,38 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
           ++i;
           return v;
         };
-        const uint32_t nf = min(static_cast<uint32_t>(kChunk), p.F16 - ch * kChunk);  // multiple of 16
+        const uint32_t nf = min(static_cast<uint32_t>(kChunk), p.Fpad - ch * kChunk);  // multiple of 8
         Words<NW> carry;  // weight 64, rippled into hi
         if (nf == kChunk) {
           carry = hs_tree<6, NW>(s, ld);
         } else {
-          // 1..3 blocks of 16: carries of weight 16 half-add into levels 4 and 5
+          // 0..3 blocks of 16 and 0..1 block of 8 (< 64 features): carries of
+          // weight 16 half-add into levels 4 and 5, a block of 8's carry into 3..5
 #pragma unroll
           for (int j = 0; j < NW; ++j) carry.v[j] = 0;
-          auto block16 = [&]() {
-            const Words<NW> c16 = hs_tree<4, NW>(s, ld);
+          auto add16 = [&](const Words<NW>& c16) {
 #pragma unroll
             for (int j = 0; j < NW; ++j) {
               const uint32_t c32 = s[4][j] & c16.v[j];
               s[4][j] ^= c16.v[j];
               const uint32_t c64 = s[5][j] & c32;
               s[5][j] ^= c32;
-              carry.v[j] |= c64;  // at most one weight-64 carry per bit across <= 3 blocks of 16
+              carry.v[j] |= c64;  // at most one weight-64 carry per bit: the chunk adds < 64
             }
           };
-          block16();
-          if (nf > 16) block16();
-          if (nf > 32) block16();
+          if (nf >= 16) add16(hs_tree<4, NW>(s, ld));
+          if (nf >= 32) add16(hs_tree<4, NW>(s, ld));
+          if (nf >= 48) add16(hs_tree<4, NW>(s, ld));
+          if (nf & 8u) {
+            const Words<NW> c8 = hs_tree<3, NW>(s, ld);
+            Words<NW> c16;
+#pragma unroll
+            for (int j = 0; j < NW; ++j) {
+              c16.v[j] = s[3][j] & c8.v[j];
+              s[3][j] ^= c8.v[j];
+            }
+            add16(c16);
+          }
         }
 #pragma unroll
         for (int j = 0; j < NW; ++j) {
@@ -296,13 +306,17 @@ void launch_tt6_inst(hv_context* ctx, cudaStream_t st, TT6Params p, size_t smem)
 bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
                const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
                uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo, uint32_t* counter, bool perm) {
+  // zero-padded feature count: a multiple of 8 (the partial chunk runs blocks of
+  // 16 and 8), unless padding to 16 completes a 64-feature chunk (the full-chunk
+  // tree is cheaper per feature): CHB-MIT 342 -> 344 (was 352), UCI-HAR 561 -> 576
   const uint32_t F16 = (F + 15) / 16 * 16;
+  const uint32_t Fpad = (F16 % kChunk == 0) ? F16 : (F + 7) / 8 * 8;
   // planes above the six HS levels: counts < 64 * 2^NH; instantiated NH in {3, 4, 6}
   int nh = 0;
   while ((64ull << nh) <= F) ++nh;
   nh = nh <= 3 ? 3 : nh <= 4 ? 4 : nh <= 6 ? 6 : -1;
   if (nh < 0) return false;
-  const size_t pair_table = static_cast<size_t>(F16) * kTBins * 8;
+  const size_t pair_table = static_cast<size_t>(Fpad) * kTBins * 8;
   const size_t wstage = 16 * 32 * 4;
   // Shapes (word pairs per lane, warps per CTA, CTAs per SM), preferred first:
   // the most pairs whose tables fit (measured at CHB-MIT: 4 or 3 pairs with 8
@@ -334,7 +348,7 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
     block_rows = static_cast<uint32_t>(std::max<uint64_t>(256, (br + 255) / 256 * 256));
   }
   if (const char* br_env = getenv("HVB200_TT_BLOCK_ROWS")) block_rows = static_cast<uint32_t>(atoi(br_env));
-  TT6Params p{bins8, ldb, rows, F, F16, D, W, B, id, val, tie, out, w0, wcount, ldo, slices, block_rows,
+  TT6Params p{bins8, ldb, rows, F, Fpad, D, W, B, id, val, tie, out, w0, wcount, ldo, slices, block_rows,
               (rows + block_rows - 1) / block_rows, counter, perm ? 1u : 0u};
 #define HV_TT6(NPR, G, MB, N)                                            \
   if (s.npr == NPR && s.g == G && s.minb == MB && nh == N) {             \
