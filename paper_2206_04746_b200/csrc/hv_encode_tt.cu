@@ -182,10 +182,12 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const uint32_t col = (8 * i + lr) ^ (lq << 3);
-          Sw[(4 * lq + 0) * 32 + col] = (ld4[i].x & 0x0F0F0F0Fu) * 8u;
-          Sw[(4 * lq + 1) * 32 + col] = (ld4[i].y & 0x0F0F0F0Fu) * 8u;
-          Sw[(4 * lq + 2) * 32 + col] = (ld4[i].z & 0x0F0F0F0Fu) * 8u;
-          Sw[(4 * lq + 3) * 32 + col] = (ld4[i].w & 0x0F0F0F0Fu) * 8u;
+          // bins arrive validated (< B <= 16), so no nibble mask: the shift alone
+          // turns 4 bins into 4 table offsets (b * 8 < 128, no carry between bytes)
+          Sw[(4 * lq + 0) * 32 + col] = ld4[i].x << 3;
+          Sw[(4 * lq + 1) * 32 + col] = ld4[i].y << 3;
+          Sw[(4 * lq + 2) * 32 + col] = ld4[i].z << 3;
+          Sw[(4 * lq + 3) * 32 + col] = ld4[i].w << 3;
         }
       };
       stage();
