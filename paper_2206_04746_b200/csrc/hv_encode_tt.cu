@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
       }
       uint4 ld4[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) ld4[i] = ok[i] ? __ldg(src[i]) : make_uint4(0, 0, 0, 0);
+      for (int i = 0; i < 4; ++i) ld4[i] = __ldg(src[i]);  // rows past the block read row 0 (results not stored)
       // transpose into [w][r ^ 8*(w>>2)], bins scaled to table byte offsets (b*8)
       auto stage = [&]() {
 #pragma unroll
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
         const bool more = ch + 1 < nchunks;
         if (more) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) ld4[i] = ok[i] ? __ldg(src[i] + (ch + 1) * (kChunk / 16)) : make_uint4(0, 0, 0, 0);
+          for (int i = 0; i < 4; ++i) ld4[i] = __ldg(src[i] + (ch + 1) * (kChunk / 16));
         }
         const uint32_t tch = ch * (kChunk * kFeatBytes);  // 256-aligned chunk base (byte offset in sm6)
         int i = 0;
