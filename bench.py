@@ -323,22 +323,11 @@ def impl_engine(args):
     ms_step = ms / args.steps
     value = rows / (ms_step / 1e3)
 
-    # parity spot check of the timed result against the oracle (outside timing)
-    check = None
-    if rank == 0:
-        try:
-            sys.path.insert(0, str(ROOT / "tests"))
-            import oracle_ref as O
-            idx = np.array([0, 1, 17, n_tr - 1, n_tr, n_tr + n_te - 1])
-            idx = idx[(idx >= 0) & (idx < n_tr + n_te)]
-            gl = np.where(idx < n_tr, tr_lo + idx, te_lo + (idx - n_tr))
-            b = np.stack([O.synth_c(int(g), 1, F, Cc, B, w["label_kind"], w["data_seed"])[0][0] for g in gl])
-            want = O.encode_batch(b, cbk.id_vectors.cpu().numpy().view(np.uint32),
-                                  cbk.value_vectors.cpu().numpy().view(np.uint32), B, D, O.BIND_ID_LEVEL,
-                                  cbk.encode_tiebreak.cpu().numpy().view(np.uint32))
-            check = bool(np.array_equal(enc[idx].cpu().numpy().view(np.uint32), want))
-        except Exception as e:  # pragma: no cover - reporting only
-            check = f"skipped: {e}"
+    # parity of the timed step's own outputs (outside timing): sampled encoded
+    # rows vs the oracle's encoder, the class vectors vs an independent torch
+    # recount of every train row binarised by the oracle, and >= 1000 sampled
+    # predicted labels vs the oracle's predict against those class vectors
+    check = verify_step(rank, world, eng, cbk, bins8, enc, yt, cv, pred, n_tr, n_te, tr_lo, te_lo)
 
     # ---- roofline of the dominant kernel (encoder) ----
     enc_avg_ms = sum(enc_ms) / max(1, len(enc_ms))
@@ -414,6 +403,69 @@ def impl_engine(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def verify_step(rank, world, eng, cbk, bins8, enc, yt, cv, pred, n_tr, n_te, tr_lo, te_lo):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    w = WORKLOAD
+    F, Cc, D, B = w["features"], w["classes"], w["dim"], w["bins"]
+    u32 = lambda t: t.cpu().numpy().view(np.uint32)
+    try:
+        sys.path.insert(0, str(ROOT / "tests"))
+        import oracle_ref as O
+        out = {}
+        # 1. encoded rows
+        rng = np.random.default_rng(rank)
+        idx = np.unique(np.concatenate([[0, 1, n_tr - 1, n_tr, n_tr + n_te - 1],
+                                        rng.integers(0, n_tr + n_te, 59)]))
+        idx = idx[(idx >= 0) & (idx < n_tr + n_te)]
+        gl = np.where(idx < n_tr, tr_lo + idx, te_lo + (idx - n_tr))
+        b = np.concatenate([O.synth_c(int(g), 1, F, Cc, B, w["label_kind"], w["data_seed"])[0] for g in gl])
+        want = O.encode_batch(b, u32(cbk.id_vectors), u32(cbk.value_vectors), B, D, O.BIND_ID_LEVEL,
+                              u32(cbk.encode_tiebreak))
+        out["encoded_rows"] = int(idx.size)
+        ok = bool(np.array_equal(u32(enc[torch.as_tensor(idx, device=enc.device)]), want))
+        # 2. class vectors: torch recount of this rank's train rows, summed over ranks
+        Wd = enc.shape[1]
+        shifts = torch.arange(32, device=enc.device, dtype=torch.int32)
+        cnt = torch.zeros((Cc, 32 * Wd), dtype=torch.int64, device=enc.device)
+        for r0 in range(0, n_tr, 65536):
+            e = enc[r0:min(n_tr, r0 + 65536)]
+            bits = ((e.unsqueeze(-1) >> shifts) & 1).to(torch.uint8).reshape(e.shape[0], 32 * Wd)
+            yy = yt[r0:r0 + e.shape[0]].long()
+            for c in range(Cc):
+                m = yy == c
+                if m.any():
+                    cnt[c] += bits[m].sum(0, dtype=torch.int64)
+        nrow = torch.bincount(yt.long(), minlength=Cc).to(torch.int64)
+        if world > 1:
+            dist.all_reduce(cnt)
+            dist.all_reduce(nrow)
+        cntn, nrn = cnt.cpu().numpy().astype(np.uint64), nrow.cpu().numpy()
+        tb = u32(cbk.model_tiebreak)
+        tb_bits = O.unpack_rows(tb.reshape(1, -1), D).reshape(-1)
+        for c in range(Cc):
+            wc = O.pack_rows(O.majority_binarize(cntn[c, :D], int(nrn[c]), tb_bits).reshape(1, -1))
+            ok &= bool(np.array_equal(u32(cv[c]).reshape(1, -1), wc))
+        out["class_vectors"] = f"{Cc} x {D} bits vs oracle majority of a torch recount of all train rows"
+        # 3. sampled predicted labels
+        ti = np.unique(np.concatenate([[0, n_te - 1], rng.integers(0, n_te, 1200)]))
+        ti = ti[(ti >= 0) & (ti < n_te)]
+        m = O.NaiveModel(Cc, D, tb)
+        m.cv = O.unpack_rows(u32(cv), D).copy()
+        ol, _ = m.predict(u32(enc[n_tr:][torch.as_tensor(ti, device=enc.device)]))
+        ok &= bool(np.array_equal(pred[torch.as_tensor(ti, device=pred.device)].cpu().numpy(), ol))
+        out["labels_sampled"] = int(ti.size)
+        flag = torch.tensor([int(ok)], dtype=torch.int32, device=enc.device)
+        if world > 1:
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        out["ok"] = bool(flag.item())
+        return out
+    except Exception as e:  # pragma: no cover - reporting only
+        return {"ok": None, "skipped": str(e)}
 
 
 def run_e2e(args, rank, world, local, rows, ntrain, ntest, tr, te, eng, cbk):

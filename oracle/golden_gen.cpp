@@ -15,6 +15,8 @@
 #include <iostream>
 #include <map>
 #include <sstream>
+#include <span>
+#include <bit>
 #include <string>
 #include <vector>
 
@@ -296,6 +298,109 @@ void gen_pipeline(const std::string& name, std::size_t rows, std::size_t feature
   c.packed("cosine_online_cv", con.class_vectors);
 }
 
+// FNV-1a 64 over 32-bit words / 64-bit patterns: row and class digests for
+// the large pipelines, whose full arrays would be too big to commit.
+std::uint64_t fnv_words(std::span<const std::uint32_t> w) {
+  std::uint64_t h = 1469598103934665603ull;
+  for (std::uint32_t x : w) h = (h ^ x) * 1099511628211ull;
+  return h;
+}
+std::uint64_t fnv_doubles(std::span<const double> v) {
+  std::uint64_t h = 1469598103934665603ull;
+  for (double d : v) h = (h ^ std::bit_cast<std::uint64_t>(d)) * 1099511628211ull;
+  return h;
+}
+
+// run_fold_packed at D = 10000 and the benchmark shapes (UCI-HAR, ISOLET,
+// MNIST at D = 20000), thousands of rows: inputs are regenerated by the
+// oracle's make_synth restatement (pinned by the small pipelines' X), so only
+// digests of X / bins / encoded rows / accumulators are stored, plus the
+// small outputs (class vectors, weights, counts, labels, distances) in full.
+void gen_pipeline_big(const std::string& name, std::size_t rows, std::size_t features, std::size_t classes,
+                      std::size_t dim, std::uint64_t seed, std::vector<std::size_t> batch_sizes, double gamma,
+                      std::size_t threads) {
+  Case c("bigpipe_" + name);
+  synth::SynthSpec spec;
+  spec.rows = rows;
+  spec.features = features;
+  spec.classes = classes;
+  spec.seed = seed;
+  Dataset ds = synth::make_synth(spec);
+  const std::size_t train_rows = std::min(rows - 1, std::max<std::size_t>(1, rows * 4 / 5));
+  const std::size_t bins_n = 16;
+  Discretizer disc = fit_discretizer(std::span<const double>(ds.X.data(), train_rows * features), train_rows,
+                                     features, bins_n);
+  std::vector<std::uint32_t> bins = discretize_matrix(ds.X, rows, disc);
+  Codebook cb = make_codebook(GenerationStrategy::kRandom, BindingStrategy::kIdLevel, features, bins_n, dim,
+                              derive_seed(seed, 1));
+  PackedBitMatrix etb = generate_random(1, dim, derive_seed(seed, 2));
+  PackedBitMatrix enc = encode_batch(bins, rows, cb, etb, threads);
+  c.set("rows", rows);
+  c.set("features", features);
+  c.set("classes", classes);
+  c.set("dim", dim);
+  c.set("seed", seed);
+  c.set("train_rows", train_rows);
+  c.set("gamma_bits", std::bit_cast<std::uint64_t>(gamma));
+  std::vector<std::uint64_t> xh(rows), bh(rows), eh(rows);
+  for (std::size_t r = 0; r < rows; ++r) {
+    xh[r] = fnv_doubles(std::span<const double>(ds.X.data() + r * features, features));
+    bh[r] = fnv_words(std::span<const std::uint32_t>(bins.data() + r * features, features));
+    eh[r] = fnv_words(enc.row(r));
+  }
+  c.put("X_fnv", xh);
+  c.put("bins_fnv", bh);
+  c.put("encoded_fnv", eh);
+  c.put("y", ds.y);
+  c.put("min", disc.min);
+  c.put("max", disc.max);
+
+  PackedBitMatrix train(train_rows, dim), test(rows - train_rows, dim);
+  for (std::size_t r = 0; r < rows; ++r) {
+    auto src = enc.row(r);
+    auto dst = r < train_rows ? train.row(r) : test.row(r - train_rows);
+    std::copy(src.begin(), src.end(), dst.begin());
+  }
+  std::vector<int> ytrain(ds.y.begin(), ds.y.begin() + static_cast<long>(train_rows));
+  ModelConfig cfg{classes, dim, Metric::kHamming, gamma, seed};
+  auto acc_fnv = [&](const HDModel& m) {
+    std::vector<std::uint64_t> h(classes);
+    for (std::size_t k = 0; k < classes; ++k) {
+      h[k] = fnv_doubles(std::span<const double>(m.accumulators.data() + k * dim, dim));
+    }
+    return h;
+  };
+  HDModel cl = train_classical(train, ytrain, cfg);
+  c.put("classical_acc_fnv", acc_fnv(cl));
+  c.put("classical_weight", cl.class_weight);
+  c.put("classical_counts", cl.sample_counts);
+  c.packed("classical_cv", cl.class_vectors);
+  c.packed("model_tiebreak", cl.tiebreak);
+  auto preds = predict(cl, test, threads);
+  std::vector<int> pl;
+  std::vector<double> pd;
+  for (const auto& p : preds) {
+    pl.push_back(p.label);
+    pd.insert(pd.end(), p.distances.begin(), p.distances.end());
+  }
+  c.put("classical_pred", pl);
+  c.put("classical_dist", pd, {preds.size(), classes});
+  std::vector<std::uint64_t> bs(batch_sizes.begin(), batch_sizes.end());
+  c.put("batch_sizes", bs);
+  for (std::size_t b : batch_sizes) {
+    HDModel on = train_online(train, ytrain, b, cfg);
+    const std::string k = "online_b" + std::to_string(b);
+    c.put(k + "_acc_fnv", acc_fnv(on));
+    c.put(k + "_weight", on.class_weight);
+    c.put(k + "_counts", on.sample_counts);
+    c.packed(k + "_cv", on.class_vectors);
+    auto op = predict(on, test, threads);
+    std::vector<int> ol;
+    for (const auto& p : op) ol.push_back(p.label);
+    c.put(k + "_pred", ol);
+  }
+}
+
 // One online_update on random packed state (test_model.cpp:180-205 shape).
 void gen_online_update() {
   Case c("online_update");
@@ -448,6 +553,10 @@ int main(int argc, char** argv) {
   gen_pipeline("small", 300, 30, 5, 2048, 11, {1, 7, 64, 1024}, 1.0);
   gen_pipeline("odd", 157, 13, 3, 1000, 12, {5, 50}, 0.6);
   gen_pipeline("isolet", 160, 617, 26, 2000, 13, {32}, 1.0);
+  gen_pipeline_big("har_d10k", 12000, 561, 6, 10000, 21, {256, 1024, 8192}, 1.0, 8);
+  gen_pipeline_big("isolet_d10k", 2500, 617, 26, 10000, 22, {1024}, 1.0, 8);
+  gen_pipeline_big("mnist_d20k", 3000, 784, 10, 20000, 23, {1024}, 0.8, 8);
+  gen_pipeline_big("mnist_d1k", 6000, 784, 10, 1024, 24, {1024, 8192}, 1.0, 8);
   gen_online_update();
   gen_synth();
   gen_eval();

@@ -554,6 +554,38 @@ void hvo_synth(uint64_t row0, size_t rows, size_t features, size_t classes, size
 }
 
 /* ======================================================================= */
+/* Reference test-support generator synth::make_synth                      */
+/* (tests/support/synth.cpp:9-47, defaults synth.hpp:14-22): class i % C,   */
+/* feature value = centre of bin centre_bin(c, f) + uniform jitter from one */
+/* mt19937_64 next_unit() per (row, feature) in row-major order.            */
+/* ======================================================================= */
+
+/* synth.cpp:9-14 */
+static size_t synth_centre_bin(size_t cls, size_t feature, size_t grid_bins) {
+  return (cls * (feature + 1) + 3 * feature) % grid_bins;
+}
+
+/* synth.cpp:16-47 (segments = 1: no segment column) */
+int hvo_make_synth(size_t rows, size_t features, size_t classes, size_t grid_bins, double jitter, uint64_t seed,
+                   double* X, int32_t* y) {
+  if (rows == 0 || features == 0 || classes == 0 || grid_bins == 0) return HVO_INVALID_ARGUMENT;
+  hvo_rng* rng = (hvo_rng*)malloc(sizeof(hvo_rng));
+  hvo_rng_seed(rng, seed);
+  const double width = 1.0 / (double)grid_bins;
+  for (size_t i = 0; i < rows; ++i) {
+    const size_t cls = i % classes;
+    y[i] = (int32_t)cls;
+    for (size_t f = 0; f < features; ++f) {
+      const double centre = ((double)synth_centre_bin(cls, f, grid_bins) + 0.5) * width;
+      const double noise = jitter * (2.0 * hvo_rng_next_unit(rng) - 1.0) * 0.5 * width;
+      X[i * features + f] = centre + noise;
+    }
+  }
+  free(rng);
+  return HVO_OK;
+}
+
+/* ======================================================================= */
 /* Evaluation (eval.cpp:12-116)                                            */
 /* ======================================================================= */
 

@@ -245,6 +245,7 @@ void fit_discretizer_device(hv_context* ctx, cudaStream_t st, const double* X, s
 
 void discretize_rows_device(hv_context* ctx, cudaStream_t st, const double* X, size_t F, const uint64_t* idx,
                             size_t n, const double* mn, const double* mx, size_t B, uint8_t* out, size_t ldb) {
+  check_bins_u8(B, "discretize");
   if (n == 0) return;
   ck(cudaMemsetAsync(out, 0, n * ldb, st), "memset bins");
   const uint64_t items = n * F;
@@ -258,6 +259,7 @@ void discretize_rows_device(hv_context* ctx, cudaStream_t st, const double* X, s
 void encode_device(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, size_t ldb, size_t rows, size_t F,
                    const uint32_t* id, const uint32_t* val, size_t B, size_t D, hv_binding binding,
                    const uint32_t* tie, uint32_t* out, bool allow_fast, size_t w0, size_t wcount, size_t ldo) {
+  check_bins_u8(B, "encode");
   const size_t W = words_per_row(D);
   if (rows == 0 || W == 0) return;
   if (D > 0xFFFFFFFFull || F > 0xFFFFFFFFull) invalid("encode: shape too large");
@@ -322,6 +324,7 @@ void encode_device(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, size_
 
 void narrow_device(hv_context* ctx, cudaStream_t st, const uint32_t* bins32, size_t rows, size_t F, size_t B,
                    uint8_t* bins8, size_t ldb, uint64_t flat_base) {
+  check_bins_u8(B, "narrow_bins");
   if (rows == 0) return;
   const uint64_t items = rows * (ldb / 4);
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((items + 255) / 256, uint64_t(ctx->sm_count) * 16));

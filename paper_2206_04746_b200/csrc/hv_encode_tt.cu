@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "hv_internal.cuh"
 
@@ -177,20 +178,24 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
       uint4 ld4[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) ld4[i] = __ldg(src[i]);  // rows past the block read row 0 (results not stored)
-      // transpose into [w][r ^ 8*(w>>2)], bins scaled to table byte offsets (b*8)
-      auto stage = [&]() {
+      // transpose into [w][r ^ 8*(w>>2)], bins scaled to table byte offsets (b*8).
+      // Bins of features < F arrive validated (< B <= 16), so full chunks need no
+      // nibble mask: the shift alone turns 4 bins into 4 table offsets (b * 8 < 128,
+      // no carry between bytes). The last chunk holds the row padding [F, Fpad),
+      // whose bytes the caller need not zero: masked to a nibble they index the
+      // all-zero table rows of features >= F instead of running past the table.
+      auto stage = [&](auto masked) {
+        constexpr uint32_t m = decltype(masked)::value ? 0x0F0F0F0Fu : 0xFFFFFFFFu;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const uint32_t col = (8 * i + lr) ^ (lq << 3);
-          // bins arrive validated (< B <= 16), so no nibble mask: the shift alone
-          // turns 4 bins into 4 table offsets (b * 8 < 128, no carry between bytes)
-          Sw[(4 * lq + 0) * 32 + col] = ld4[i].x << 3;
-          Sw[(4 * lq + 1) * 32 + col] = ld4[i].y << 3;
-          Sw[(4 * lq + 2) * 32 + col] = ld4[i].z << 3;
-          Sw[(4 * lq + 3) * 32 + col] = ld4[i].w << 3;
+          Sw[(4 * lq + 0) * 32 + col] = (ld4[i].x & m) << 3;
+          Sw[(4 * lq + 1) * 32 + col] = (ld4[i].y & m) << 3;
+          Sw[(4 * lq + 2) * 32 + col] = (ld4[i].z & m) << 3;
+          Sw[(4 * lq + 3) * 32 + col] = (ld4[i].w & m) << 3;
         }
       };
-      stage();
+      if (nchunks == 1) stage(std::true_type{}); else stage(std::false_type{});
       __syncwarp();
       const uint32_t* base[4] = {Sw + (lane ^ 0), Sw + (lane ^ 8), Sw + (lane ^ 16), Sw + (lane ^ 24)};
       for (uint32_t ch = 0; ch < nchunks; ++ch) {
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
         }
         if (more) {
           __syncwarp();  // every lane has read its words of this chunk
-          stage();
+          if (ch + 2 == nchunks) stage(std::true_type{}); else stage(std::false_type{});
           __syncwarp();
         }
       }
@@ -349,7 +354,10 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
     const uint64_t br = (rows * slices + want_items - 1) / want_items;
     block_rows = static_cast<uint32_t>(std::max<uint64_t>(256, (br + 255) / 256 * 256));
   }
-  if (const char* br_env = getenv("HVB200_TT_BLOCK_ROWS")) block_rows = static_cast<uint32_t>(atoi(br_env));
+  if (const char* br_env = getenv("HVB200_TT_BLOCK_ROWS")) {  // tuning override: a positive multiple of 32
+    const long v = strtol(br_env, nullptr, 10);
+    if (v >= 32 && v <= (1l << 30)) block_rows = static_cast<uint32_t>(v / 32 * 32);
+  }
   TT6Params p{bins8, ldb, rows, F, Fpad, D, W, B, id, val, tie, out, w0, wcount, ldo, slices, block_rows,
               (rows + block_rows - 1) / block_rows, counter, perm ? 1u : 0u};
 #define HV_TT6(NPR, G, MB, N)                                            \

@@ -169,6 +169,14 @@ void encode_device(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, size_
 void narrow_device(hv_context* ctx, cudaStream_t st, const uint32_t* bins32, size_t rows, size_t F, size_t B,
                    uint8_t* bins8, size_t ldb, uint64_t flat_base);
 inline size_t bins_pitch(size_t F) { return (F + 63) / 64 * 64; }
+// Device bins are one byte each: the reference accepts any bin count >= 2
+// (encoding.cpp:43-55), the device path up to 256 and rejects more, loudly,
+// rather than truncating bins into neighbouring bytes.
+inline void check_bins_u8(size_t B, const char* fn) {
+  if (B > 256) {
+    invalid(std::string(fn) + ": bins = " + std::to_string(B) + " exceeds 256, the device encoder's uint8 bin range");
+  }
+}
 // Discretizer on HBM-resident fp64 features over rows idx[0..n) (idx may be
 // null: rows 0..n): fit (encoding.cpp:93-119) and discretize to uint8 bins.
 void fit_discretizer_device(hv_context* ctx, cudaStream_t st, const double* X, size_t F, const uint64_t* idx,

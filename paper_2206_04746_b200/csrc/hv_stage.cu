@@ -223,6 +223,7 @@ uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, si
                           hv_binding binding, const uint32_t* d_id, const uint32_t* d_val, const uint32_t* d_tie,
                           const ChunkOut& out_for, DevBuf<uint8_t>* b8, size_t chunk, size_t& k,
                           const ChunkAfter& after) {
+  check_bins_u8(B, "encode");
   const size_t ldb = bins_pitch(F);
   HostStager& hs = stager(ctx);
   hs.reserve(chunk * ldb);

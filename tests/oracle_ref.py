@@ -345,6 +345,31 @@ def synth_bins(rows, features, classes, bins, seed, label_kind, start=0):
     return out.astype(np.uint32), y
 
 
+def make_synth(rows, features, classes, seed, grid_bins=16, jitter=0.3):
+    """Reference test-support make_synth (tests/support/synth.cpp:16-47) via
+    the oracle's C restatement: fp64 features (rows x features) and labels."""
+    L = lib()
+    L.hvo_make_synth.restype = C.c_int
+    L.hvo_make_synth.argtypes = [C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, C.c_double, C.c_uint64,
+                                 C.c_void_p, C.c_void_p]
+    X = np.zeros((rows, features), np.float64)
+    y = np.zeros(rows, np.int32)
+    assert L.hvo_make_synth(rows, features, classes, grid_bins, jitter, seed, _p(X), _p(y)) == 0
+    return X, y
+
+
+def fnv_rows(a):
+    """FNV-1a 64 of each row of a 2-D uint32 / float64 array (oracle/golden_gen.cpp
+    fnv_words / fnv_doubles): the digests the big golden pipelines store."""
+    a = np.ascontiguousarray(a)
+    v = a.view(np.uint64) if a.dtype == np.float64 else a.astype(np.uint64)
+    h = np.full(v.shape[0], 1469598103934665603, np.uint64)
+    with np.errstate(over="ignore"):
+        for j in range(v.shape[1]):
+            h = (h ^ v[:, j]) * np.uint64(1099511628211)
+    return h
+
+
 def synth_c(row0, rows, features, classes, bins, kind, seed):
     """The C generator (include/hvb200_synth.h) via the oracle library."""
     L = lib()

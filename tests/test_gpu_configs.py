@@ -1,0 +1,160 @@
+"""Parity at the BASELINE.json config shapes that round 1 left untested.
+
+1. Reference-written pipelines at D = 10000 / 20000 / 1024 (tests/golden/cases/
+   bigpipe_*, written by oracle/golden_gen.cpp linked against the reference
+   library): UCI-HAR (F = 561, C = 6, 12,000 rows, online batches 256 / 1024 /
+   8192), ISOLET (F = 617, C = 26, 2,500 rows), MNIST (F = 784, C = 10,
+   D = 20000 and D = 1024). The whole run_fold_packed path (experiment.cpp:
+   148-178) goes through the engine's C ABI: discretizer fit + discretize,
+   encode, classical and online training, predict. Every encoded row and every
+   fp64 accumulator row is compared through its FNV-1a digest, everything
+   else in full — all bit-exact against the reference itself.
+2. The C oracle at sizes the golden files cannot hold: UCI-HAR online with
+   16,384+ rows at batch 256 / 1024 / 8192, Large online (C = 100, D = 32768,
+   batch 1024, split-K tcgen05 scoring on), MNIST online at D = 1024 and
+   20000 with batch 1024 (model.cpp:250-301, test_model.cpp:278-296).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle_ref as O
+from golden_io import Case, cases
+
+pytestmark = pytest.mark.gpu
+
+hv = pytest.importorskip("paper_2206_04746_b200.hypervec")
+dv = pytest.importorskip("paper_2206_04746_b200.device")
+from paper_2206_04746_b200 import launch_count  # noqa: E402
+
+
+def _u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _acc_fnv(acc2d):
+    return O.fnv_rows(np.ascontiguousarray(acc2d, dtype=np.float64))
+
+
+@pytest.mark.parametrize("name", cases("bigpipe_"))
+def test_reference_pipeline_at_benchmark_shapes(name):
+    c = Case(name)
+    rows, F, C, D, seed = c.int("rows"), c.int("features"), c.int("classes"), c.int("dim"), c.int("seed")
+    ntr = c.int("train_rows")
+    gamma = c.float_bits("gamma_bits")
+    X, y = O.make_synth(rows, F, C, seed)
+    np.testing.assert_array_equal(O.fnv_rows(X), c["X_fnv"])
+    np.testing.assert_array_equal(y, c["y"])
+    before = launch_count()
+    disc = hv.fit_discretizer(X[:ntr], ntr, F, 16)
+    np.testing.assert_array_equal(disc.min, c["min"])
+    np.testing.assert_array_equal(disc.max, c["max"])
+    bins = hv.discretize_matrix(X, rows, disc).reshape(rows, F)
+    np.testing.assert_array_equal(O.fnv_rows(bins.astype(np.uint32)), c["bins_fnv"])
+    cb = hv.make_codebook(hv.GenerationStrategy.kRandom, hv.BindingStrategy.kIdLevel, F, 16, D,
+                          hv.derive_seed(seed, 1))
+    etb = hv.generate_random(1, D, hv.derive_seed(seed, 2))
+    enc = hv.encode_batch(bins, rows, cb, etb)
+    np.testing.assert_array_equal(O.fnv_rows(enc.words), c["encoded_fnv"])
+    train = hv.PackedBitMatrix(ntr, D, enc.words[:ntr])
+    test = hv.PackedBitMatrix(rows - ntr, D, enc.words[ntr:])
+    cfg = hv.ModelConfig(class_count=C, dim=D, gamma=gamma, seed=seed)
+    m = hv.train_classical(train, y[:ntr], cfg)
+    np.testing.assert_array_equal(m.tiebreak.words, c["model_tiebreak"])
+    np.testing.assert_array_equal(_acc_fnv(m.accumulators.reshape(C, D)), c["classical_acc_fnv"])
+    np.testing.assert_array_equal(m.class_weight, c["classical_weight"])
+    np.testing.assert_array_equal(m.sample_counts, c["classical_counts"])
+    np.testing.assert_array_equal(m.class_vectors.words, c["classical_cv"])
+    labels, dist = hv.predict_arrays(m, test)
+    np.testing.assert_array_equal(labels, c["classical_pred"])
+    np.testing.assert_array_equal(dist.view(np.uint64), c["classical_dist"].view(np.uint64))
+    for b in c["batch_sizes"].tolist():
+        k = f"online_b{b}"
+        on = hv.train_online(train, y[:ntr], int(b), cfg)
+        np.testing.assert_array_equal(_acc_fnv(on.accumulators.reshape(C, D)), c[k + "_acc_fnv"], err_msg=k)
+        np.testing.assert_array_equal(on.class_weight.view(np.uint64), c[k + "_weight"].view(np.uint64))
+        np.testing.assert_array_equal(on.sample_counts, c[k + "_counts"])
+        np.testing.assert_array_equal(on.class_vectors.words, c[k + "_cv"])
+        ol, _ = hv.predict_arrays(on, test)
+        np.testing.assert_array_equal(ol, c[k + "_pred"])
+    assert launch_count() > before
+
+
+def _oracle_online(eng, cbk, enc, labels, bsz, C, D, gamma=1.0):
+    acc, weight, counts, cv = eng.train_online(enc, labels, bsz, gamma)
+    eng.dc.check()
+    om = O.NaiveModel(C, D, _u32(cbk.model_tiebreak), O.HAMMING, gamma).train_online(
+        _u32(enc), labels.cpu().numpy(), bsz)
+    np.testing.assert_array_equal(acc.cpu().numpy().view(np.uint64), om.acc.view(np.uint64))
+    np.testing.assert_array_equal(weight.cpu().numpy().view(np.uint64), om.weight.view(np.uint64))
+    np.testing.assert_array_equal(counts.cpu().numpy().astype(np.uint64), om.counts.astype(np.uint64))
+    np.testing.assert_array_equal(_u32(cv), om.class_vectors)
+    return om
+
+
+@pytest.mark.parametrize("bsz", [256, 1024, 8192])
+def test_uci_har_online_batch_sweep_vs_oracle(bsz):
+    """BASELINE configs[1]: UCI-HAR-shaped (F = 561, C = 6, D = 10000) online,
+    18,000 rows (2+ batches even at 8192), bit-exact fp64 accumulators."""
+    F, C, D, rows = 561, 6, 10000, 18000
+    cbk = dv.DeviceCodebook.make(F, 16, D, seed=31)
+    eng = dv.Engine(cbk, C)
+    bins8, labels = eng.synth(0, rows, 0, 3)
+    enc = eng.encode(bins8)
+    om = _oracle_online(eng, cbk, enc, labels, bsz, C, D, gamma=0.9)
+    # the trained model's predictions on fresh rows match the oracle's
+    tb8, _ = eng.synth(rows, 2000, 0, 3)
+    te = eng.encode(tb8)
+    cvt = torch.from_numpy(O.pack_rows(om.cv).view(np.int32)).to(te.device)
+    pred = eng.predict(cvt, te)
+    ol, _ = om.predict(_u32(te))
+    np.testing.assert_array_equal(pred.cpu().numpy(), ol)
+
+
+def test_large_online_tensor_core_scoring_vs_oracle():
+    """BASELINE configs[4] shape: C = 100, D = 32768, batch 1024, 5 batches
+    after the bootstrap — the split-K tcgen05 scoring (default for many
+    classes) against the oracle, not against the engine's own POPC path."""
+    F, C, D, rows, bsz = 617, 100, 32768, 5 * 1024, 1024
+    cbk = dv.DeviceCodebook.make(F, 16, D, seed=41)
+    eng = dv.Engine(cbk, C)
+    bins8, labels = eng.synth(0, rows, 0, 5)
+    enc = eng.encode(bins8)
+    _oracle_online(eng, cbk, enc, labels, bsz, C, D)
+
+
+@pytest.mark.parametrize("D", [1024, 20000])
+def test_mnist_online_batch_1024_vs_oracle(D):
+    """BASELINE configs[2]: MNIST-shaped (F = 784, C = 10) online, batch 1024,
+    at both ends of the D sweep."""
+    F, C, rows = 784, 10, 8192
+    cbk = dv.DeviceCodebook.make(F, 16, D, seed=51)
+    eng = dv.Engine(cbk, C)
+    bins8, labels = eng.synth(0, rows, 0, 6)
+    enc = eng.encode(bins8)
+    _oracle_online(eng, cbk, enc, labels, 1024, C, D, gamma=0.8)
+
+
+def test_fast_encoder_ignores_row_padding_bytes():
+    """bins8 bytes in [features, ldb) are padding the caller need not zero:
+    the table encoder must give the same words as with zero padding (and as
+    the generic encoder, which never reads them)."""
+    F, C, D, rows = 342, 2, 10000, 3000
+    cbk = dv.DeviceCodebook.make(F, 16, D, seed=61)
+    eng = dv.Engine(cbk, C)
+    bins8, _ = eng.synth(0, rows, 1, 4)
+    want = eng.encode(bins8)
+    noisy = bins8.clone()
+    noisy[:, F:] = torch.randint(0, 256, (rows, noisy.shape[1] - F), dtype=torch.uint8, device=noisy.device)
+    assert torch.equal(eng.encode(noisy), want)
+
+
+def test_more_than_256_bins_rejected_loudly():
+    """The device encoder stages one byte per bin: bin counts above 256 are
+    refused with INVALID_ARGUMENT instead of corrupting neighbouring bytes."""
+    F, D, B = 8, 256, 300
+    cb = hv.make_codebook(hv.GenerationStrategy.kRandom, hv.BindingStrategy.kIdLevel, F, B, D, 5)
+    tb = hv.generate_random(1, D, 6)
+    bins = np.full((4, F), 299, np.uint32)
+    with pytest.raises(hv.InvalidArgument, match="exceeds 256"):
+        hv.encode_batch(bins, 4, cb, tb)

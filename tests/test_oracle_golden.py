@@ -181,3 +181,44 @@ def test_eval_oracle_rejects_like_reference():
         O.sample_metrics([1, 0], [1], 1)
     # test_eval.cpp:24-32 known answers
     np.testing.assert_array_equal(O.smooth_labels([0, 1, 0, 1, 1, 1, 0], 3), [0, 0, 1, 1, 1, 1, 1])
+
+
+@pytest.mark.parametrize("name", ["pipeline_small", "pipeline_odd", "pipeline_isolet"])
+def test_make_synth_restatement(name):
+    """The oracle's make_synth (tests/support/synth.cpp:16-47) reproduces the
+    reference-written feature matrices bit for bit."""
+    c = Case(name)
+    X, y = O.make_synth(c.int("rows"), c.int("features"), c.int("classes"), c.int("seed"))
+    np.testing.assert_array_equal(X.view(np.uint64), c["X"].view(np.uint64))
+    np.testing.assert_array_equal(y, c["y"])
+
+
+@pytest.mark.parametrize("name", cases("bigpipe_"))
+def test_big_pipeline_inputs_and_discretizer(name):
+    """The big reference pipelines store digests only: the oracle regenerates
+    their inputs (make_synth -> fit_discretizer -> discretize) exactly."""
+    c = Case(name)
+    rows, F, ntr = c.int("rows"), c.int("features"), c.int("train_rows")
+    X, y = O.make_synth(rows, F, c.int("classes"), c.int("seed"))
+    np.testing.assert_array_equal(O.fnv_rows(X), c["X_fnv"])
+    np.testing.assert_array_equal(y, c["y"])
+    mn, mx = O.fit_discretizer(X[:ntr], 16)
+    np.testing.assert_array_equal(mn, c["min"])
+    np.testing.assert_array_equal(mx, c["max"])
+    bins = O.discretize_matrix(X, mn, mx, 16).reshape(rows, F)
+    np.testing.assert_array_equal(O.fnv_rows(bins.astype(np.uint32)), c["bins_fnv"])
+
+
+def test_big_pipeline_oracle_encode_sample():
+    """Sampled rows of the D = 1024 MNIST reference pipeline: the oracle's
+    encoder gives the reference's encoded-row digests."""
+    c = Case("bigpipe_mnist_d1k")
+    rows, F, D, seed, ntr = c.int("rows"), c.int("features"), c.int("dim"), c.int("seed"), c.int("train_rows")
+    X, _ = O.make_synth(rows, F, c.int("classes"), seed)
+    mn, mx = O.fit_discretizer(X[:ntr], 16)
+    idx = np.array([0, 1, 999, rows - 1])
+    bins = O.discretize_matrix(X[idx], mn, mx, 16).reshape(len(idx), F)
+    idv, val = O.make_codebook(0, F, 16, D, O.derive_seed(seed, 1))
+    etb = O.generate_random(1, D, O.derive_seed(seed, 2))
+    enc = O.encode_batch(bins, idv, val, 16, D, O.BIND_ID_LEVEL, etb)
+    np.testing.assert_array_equal(O.fnv_rows(enc), c["encoded_fnv"][idx])
