@@ -222,7 +222,9 @@ def impl_engine(args):
     bs, _ = eng.synth(te_lo, n_te, w["label_kind"], w["data_seed"])
     bins8 = torch.cat([bt, bs])
     del bt, bs
-    enc = torch.empty((n_tr + n_te, W), dtype=torch.int32, device=eng.dev)
+    # hypervectors in the engine's pitched HBM layout: rows padded to 16 bytes
+    # (W = 313 -> 316 words) so counts and predict read whole rows as uint4 / TMA
+    enc = eng.pitched_empty(n_tr + n_te)
     counts, crow = eng.zero_counts()
     cv = torch.empty((Cc, W), dtype=torch.int32, device=eng.dev)
     pred = torch.empty(n_te, dtype=torch.int32, device=eng.dev)
@@ -367,7 +369,7 @@ def impl_engine(args):
     if args.online and world == 1:
         torch.cuda.synchronize()
         s0 = time.perf_counter()
-        eng.train_online(enc[:n_tr], yt, 1024)
+        eng.train_online(enc[:n_tr].contiguous(), yt, 1024)
         torch.cuda.synchronize()
         online = {"rows": n_tr, "batch_size": 1024, "seconds": round(time.perf_counter() - s0, 4),
                   "dp_per_s": round(n_tr / (time.perf_counter() - s0), 1)}

@@ -280,6 +280,21 @@ hv_status hv_dev_encode(hv_context* ctx, const uint8_t* bins8, size_t ldb, size_
 hv_status hv_dev_class_counts(hv_context* ctx, const uint32_t* encoded, size_t rows, size_t dim,
                               const int32_t* labels, size_t class_count, uint32_t* counts,
                               uint64_t* class_rows);
+/* Pitched hypervector rows (the engine's own HBM layout for resident data):
+ * row r of an encoded matrix at encoded + r * ldw words, ldw >= W. With
+ * ldw = hv_row_pitch_words(dim) (W rounded up to 16 bytes) and a 16-byte
+ * aligned base, class counts stage whole rows with the bulk-copy engine and
+ * predict reads uint4s; any other pitch takes the word-wise kernels. Words
+ * [W, ldw) of a row are never read as data. hv_fold_* keep their rows so. */
+size_t hv_row_pitch_words(size_t dim);
+hv_status hv_dev_class_counts_pitched(hv_context* ctx, const uint32_t* encoded, size_t ldw, size_t rows,
+                                      size_t dim, const int32_t* labels, size_t class_count,
+                                      uint32_t* counts, uint64_t* class_rows);
+/* Pitched predict: fewer than 32 classes (INVALID_ARGUMENT otherwise). */
+hv_status hv_dev_predict_hamming_pitched(hv_context* ctx, const uint32_t* class_vectors,
+                                         size_t class_count, size_t dim, const uint32_t* encoded,
+                                         size_t ldw, size_t rows, int32_t* labels, double* distances,
+                                         uint32_t* popcounts);
 /* Binarise classical counts: bit = 2c > n ? 1 : 2c < n ? 0 : tiebreak. */
 hv_status hv_dev_binarize_counts(hv_context* ctx, const uint32_t* counts,
                                  const uint64_t* class_rows, size_t class_count, size_t dim,
@@ -365,6 +380,10 @@ hv_status hv_dev_class_counts_peers(hv_context* ctx, const uint32_t* encoded, si
                                     const int32_t* labels, size_t class_count,
                                     uint32_t* const* peer_counts, uint64_t* const* peer_class_rows,
                                     size_t world);
+hv_status hv_dev_class_counts_peers_pitched(hv_context* ctx, const uint32_t* encoded, size_t ldw,
+                                            size_t rows, size_t dim, const int32_t* labels,
+                                            size_t class_count, uint32_t* const* peer_counts,
+                                            uint64_t* const* peer_class_rows, size_t world);
 /* After the counts: store `epoch` into flag[rank] of every rank (peer_flags:
  * device array of `world` pointers to each rank's `world` uint32 flags) ... */
 hv_status hv_dev_signal_peers(hv_context* ctx, uint32_t* const* peer_flags, size_t world, size_t rank,

@@ -53,12 +53,26 @@ def _compile(src: Path) -> Path:
     return out
 
 
+def _obj_stale(src: Path) -> bool:
+    """An object is rebuilt when it is missing or older than its source, any
+    shared header (csrc/*.cuh|*.h, include/*.h) or this build script."""
+    out = OBJ / (src.stem + ".o")
+    if not out.exists():
+        return True
+    t = out.stat().st_mtime
+    deps = [src, Path(__file__)] + [p for p in CSRC.glob("*") if p.suffix in (".cuh", ".h")]
+    deps += list((ROOT / "include").glob("*.h"))
+    return any(p.stat().st_mtime > t for p in deps)
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     OBJ.mkdir(exist_ok=True)
+    todo = [s for s in sources() if force or _obj_stale(s)]
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(_compile, sources()))
+        list(ex.map(_compile, todo))
+    objs = [OBJ / (s.stem + ".o") for s in sources()]
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-Xlinker", "-soname=libhvb200.so", "-o", str(tmp), *map(str, objs),
            "-lcudart_static", "-lrt", "-lpthread", "-ldl"]

@@ -132,6 +132,10 @@ SIGNATURES = {
     "hv_shared_close": (ST, [vp, vp]),
     "hv_shared_free": (ST, [vp, vp]),
     "hv_dev_class_counts_peers": (ST, [vp, vp, sz, sz, vp, sz, vp, vp, sz]),
+    "hv_dev_class_counts_peers_pitched": (ST, [vp, vp, sz, sz, sz, vp, sz, vp, vp, sz]),
+    "hv_row_pitch_words": (sz, [sz]),
+    "hv_dev_class_counts_pitched": (ST, [vp, vp, sz, sz, sz, vp, sz, vp, vp]),
+    "hv_dev_predict_hamming_pitched": (ST, [vp, vp, sz, sz, vp, sz, sz, vp, vp, vp]),
     "hv_dev_signal_peers": (ST, [vp, vp, sz, sz, u32]),
     "hv_dev_wait_peers": (ST, [vp, vp, sz, u32]),
     "hv_dataset_create": (ST, [vp, vp, sz, sz, vp, C.POINTER(vp)]),

@@ -7,9 +7,13 @@
 // (a warp covers 128 contiguous bytes), grid-stride loops sized to the SM
 // count, no shared-memory staging needed except where noted.
 
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "hv_internal.cuh"
+#include "hv_scan_tc.cuh"
 
 namespace hvb {
 
@@ -125,94 +129,316 @@ __global__ void majority_kernel(const uint64_t* __restrict__ counts, uint32_t di
 
 // Column counts over a (permuted, segmented) row sequence: for segment s,
 // counts[s][j] += #rows p in segment s with bit j set. The row sequence is
-// perm[p] (or p) for p in [0, seg_off[nseg]). One thread per word column;
-// blockIdx.y walks chunks of `chunk` positions (<= 2048 so 12-bit counters
-// suffice); Harley–Seal accumulation, flushed with atomics at segment ends.
+// perm[p] (or p) for p in [0, seg_off[nseg]).
+//
+// Rows of pitch ldm words, any alignment (the reference's unpitched layout).
+// Work item = (row chunk of `chunk` <= 2048 positions, so 12-bit counters
+// suffice; group of 32 word columns), one warp per item; a lane owns one
+// column. Rows are loaded 32 per batch: 32 independent 4-byte loads in flight
+// per lane (unpitched rows are only 4-byte aligned at odd W, so wider loads
+// are not available). The batch's 32 row indices are fetched by the warp (the
+// next batch's while this one's rows are in flight) and broadcast with
+// shuffles, so a row costs one shuffle + one address per lane. Each column
+// accumulates in a bit-sliced Harley–Seal counter (2 LOP3 per word) and is
+// flushed with atomics at segment and chunk ends. scripts/probe_stream.cu
+// (CHB-MIT, 5.65 M class-sorted rows of random words): 32 rows x 1 column per
+// lane 3.6-3.7 TB/s; 16 x 4 1.9; the round-1 thread-per-column grid 3.47.
+// Pitched, 16-byte aligned rows take column_count_staged_kernel instead.
 template <class CT>
-__global__ void __launch_bounds__(128) column_count_kernel(const uint32_t* __restrict__ m, uint32_t W,
+__global__ void __launch_bounds__(128) column_count_kernel(const uint32_t* __restrict__ m, uint32_t W, uint32_t ldm,
                                                            const uint32_t* __restrict__ perm,
                                                            const uint64_t* __restrict__ seg_off, uint32_t nseg,
                                                            uint64_t npos_fallback, uint32_t chunk, CT* single,
                                                            CT* const* __restrict__ dsts, uint32_t ndst) {
-  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = w < W;
+  constexpr int R = 32;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t groups = (W + 31) / 32;
   const uint64_t npos = seg_off ? seg_off[nseg] : npos_fallback;
-  uint64_t p0 = static_cast<uint64_t>(blockIdx.y) * chunk;
-  if (p0 >= npos) return;
-  const uint64_t p1 = min(npos, p0 + chunk);
-  uint32_t s = 0;
-  if (seg_off) {
-    while (s + 1 < nseg && seg_off[s + 1] <= p0) ++s;
-  }
+  const uint64_t items = (npos + chunk - 1) / chunk * groups;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   const uint64_t stride = 32ull * W;
-  while (p0 < p1) {
-    const uint64_t e = seg_off ? min(p1, seg_off[s + 1]) : p1;
-    if (e > p0) {
-      HSCounter<8> h;
-      // 32 row loads in flight per thread; the permutation of the next batch
-      // is fetched while this one's rows are loaded (two dependent loads per
-      // batch would otherwise serialise)
-      uint32_t rows_nx[32];
+  for (uint64_t it = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; it < items; it += nwarps) {
+    const uint32_t col = static_cast<uint32_t>(it % groups) * 32 + lane;
+    const bool ok = col < W;
+    uint64_t p0 = (it / groups) * chunk;
+    const uint64_t p1 = min(npos, p0 + chunk);
+    uint32_t s = 0;
+    if (seg_off) {
+      while (s + 1 < nseg && seg_off[s + 1] <= p0) ++s;
+    }
+    while (p0 < p1) {
+      const uint64_t e = seg_off ? min(p1, seg_off[s + 1]) : p1;
+      if (e > p0) {
+        HSCounter<8> h;
+        uint32_t n0 = 0;
+        if (p0 + lane < e) n0 = perm ? __ldg(perm + p0 + lane) : static_cast<uint32_t>(p0 + lane);
+        for (uint64_t p = p0; p < e; p += R) {
+          const uint32_t c0 = n0;
+          const uint32_t nvalid = e - p < R ? static_cast<uint32_t>(e - p) : static_cast<uint32_t>(R);
+          const uint32_t* mc = m + col;
+          uint32_t x[R];
 #pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        const uint64_t q = p0 + t;
-        rows_nx[t] = q < e ? (perm ? perm[q] : static_cast<uint32_t>(q)) : 0u;
-      }
-      for (uint64_t p = p0; p < e; p += 32) {
-        uint32_t rr[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) rr[t] = rows_nx[t];
-        uint32_t x[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) x[t] = (active && p + t < e) ? m[static_cast<uint64_t>(rr[t]) * W + w] : 0u;
-        if (p + 32 < e) {
-#pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            const uint64_t q = p + 32 + t;
-            rows_nx[t] = q < e ? (perm ? perm[q] : static_cast<uint32_t>(q)) : 0u;
+          for (int t = 0; t < R; ++t) {
+            const uint32_t r = __shfl_sync(0xFFFFFFFFu, c0, t);
+            x[t] = (ok && t < nvalid) ? __ldcs(mc + static_cast<uint64_t>(r) * ldm) : 0u;
           }
+          const uint64_t q = p + R + lane;
+          if (q < e) n0 = perm ? __ldg(perm + q) : static_cast<uint32_t>(q);
+#pragma unroll
+          for (int j = 0; j < R; j += 16) h.add16(x + j);
         }
-        h.add16(x);
-        h.add16(x + 16);
-      }
-      if (active) {
         // flush into every destination: the local counts, or — fused with the
         // all-reduce — the count buffers of all ranks over peer memory
-        for (uint32_t d = 0; d < ndst; ++d) {
-          CT* dst = (dsts ? dsts[d] : single) + s * stride + 32ull * w;
+        if (ok) {
+          for (uint32_t d = 0; d < ndst; ++d) {
+            CT* dst = (dsts ? dsts[d] : single) + s * stride + 32ull * col;
 #pragma unroll 4
-          for (int t = 0; t < 32; ++t) {
-            const uint32_t c = h.count_of(t);
-            if (c == 0) continue;
-            if (ndst == 1) {
-              atomicAdd(dst + t, static_cast<CT>(c));
-            } else {
-              atomicAdd_system(dst + t, static_cast<CT>(c));  // peer memory: system scope
+            for (int t = 0; t < 32; ++t) {
+              const uint32_t c = h.count_of(t);
+              if (c == 0) continue;
+              if (ndst == 1) {
+                atomicAdd(dst + t, static_cast<CT>(c));
+              } else {
+                atomicAdd_system(dst + t, static_cast<CT>(c));  // peer memory: system scope
+              }
             }
           }
         }
       }
+      p0 = e;
+      ++s;
     }
-    p0 = e;
-    ++s;
   }
 }
 
+// Rows of pitch ldm % 4 == 0 words, 16-byte aligned (the engine's pitched
+// layout): whole row segments are staged into shared memory by the bulk-copy
+// (TMA) engine, so HBM sees each row as one contiguous read — the pattern
+// that streams at ~6 TB/s here (scripts/probe_stream.cu), where per-warp
+// 128-byte slices of 32 different rows stop at ~3.7.
+// CTA = (column range [c0, c0 + ncols), ncols <= 512 words; row chunk of
+// `chunk` positions). Thread j owns column c0 + j. kCsStages stages of
+// kCsRows rows (default 2 x 16): warp 0 issues one cp.async.bulk per row (the row's columns
+// c0 .. c0 + ncols rounded up to 16 bytes) completing on the stage's
+// mbarrier (warp 0: a lane per row); every thread reads its column of each staged row (consecutive
+// words: conflict-free), adds 16 rows at a time into its Harley–Seal
+// counter, and arrives on the stage's `empty` barrier; warp 0 refills the
+// stage when every warp has. Class segments inside a batch (at most C - 1 per
+// call) split the batch.
+constexpr int kCsMaxCols = 512;
+
+template <class CT>
+__device__ __forceinline__ void flush_counts(const HSCounter<8>& h, uint32_t col, uint64_t seg_stride, uint32_t s,
+                                             CT* single, CT* const* __restrict__ dsts, uint32_t ndst) {
+  for (uint32_t d = 0; d < ndst; ++d) {
+    CT* dst = (dsts ? dsts[d] : single) + s * seg_stride + 32ull * col;
+#pragma unroll 4
+    for (int t = 0; t < 32; ++t) {
+      const uint32_t c = h.count_of(t);
+      if (c == 0) continue;
+      if (ndst == 1) {
+        atomicAdd(dst + t, static_cast<CT>(c));
+      } else {
+        atomicAdd_system(dst + t, static_cast<CT>(c));  // peer memory: system scope
+      }
+    }
+  }
+}
+
+template <class CT, int kCsRows, int kCsStages>
+__global__ void __launch_bounds__(kCsMaxCols) column_count_staged_kernel(
+    const uint32_t* __restrict__ m, uint32_t W, uint32_t ldm, const uint32_t* __restrict__ perm,
+    const uint64_t* __restrict__ seg_off, uint32_t nseg, uint64_t npos_fallback, uint32_t chunk, uint32_t ncols,
+    CT* single, CT* const* __restrict__ dsts, uint32_t ndst) {
+  extern __shared__ __align__(128) uint32_t cs_rows[];  // [stage][row][ncols]
+  __shared__ __align__(8) unsigned long long full[kCsStages], empty[kCsStages];
+  const uint32_t c0 = blockIdx.x * ncols;
+  const uint32_t nc = min(ncols, W - c0);
+  const uint32_t bytes = (nc + 3) / 4 * 16;
+  const uint32_t j = threadIdx.x;
+  const bool ok = j < nc;
+  const uint32_t nwarps = blockDim.x >> 5;
+  const uint64_t npos = seg_off ? seg_off[nseg] : npos_fallback;
+  const uint64_t p0 = static_cast<uint64_t>(blockIdx.y) * chunk;
+  if (p0 >= npos) return;
+  const uint64_t p1 = min(npos, p0 + chunk);
+  const uint32_t nbatch = static_cast<uint32_t>((p1 - p0 + kCsRows - 1) / kCsRows);
+  const uint32_t sbase = tc::smem_u32(cs_rows);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < kCsStages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_u32(&full[s])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_u32(&empty[s])), "r"(nwarps) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // warp 0 feeds the stages: lane t copies row t of a batch (one bulk copy per
+  // lane, after lane 0 armed the stage's transaction count), and holds the
+  // permutation entry of the next batch to issue, loaded one batch ahead. A
+  // stage is refilled once every warp has arrived on its `empty` barrier.
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t next_row = 0;
+  auto load_rows = [&](uint32_t b) {
+    const uint64_t q = p0 + static_cast<uint64_t>(b) * kCsRows + lane;
+    if (b < nbatch && lane < kCsRows && q < p1) next_row = perm ? __ldg(perm + q) : static_cast<uint32_t>(q);
+  };
+  auto issue = [&](uint32_t b) {  // warp 0: stage b % kCsStages <- rows of batch b
+    const uint32_t st = b % kCsStages;
+    if (b >= static_cast<uint32_t>(kCsStages)) {
+      tc::mbar_wait(tc::smem_u32(&empty[st]), (b / kCsStages - 1) & 1u);
+    }
+    const uint64_t pb = p0 + static_cast<uint64_t>(b) * kCsRows;
+    const uint32_t n = p1 - pb < kCsRows ? static_cast<uint32_t>(p1 - pb) : static_cast<uint32_t>(kCsRows);
+    const uint32_t mb = tc::smem_u32(&full[st]);
+    if (lane == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(n * bytes) : "memory");
+    }
+    __syncwarp();
+    if (lane < n) {
+      const uint32_t dst = sbase + (st * kCsRows + lane) * ncols * 4u;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                   "l"(m + static_cast<uint64_t>(next_row) * ldm + c0), "r"(bytes), "r"(mb)
+                   : "memory");
+    }
+    load_rows(b + 1);
+  };
+  if (threadIdx.x < 32) {
+    load_rows(0);
+    for (uint32_t b = 0; b < nbatch && b < static_cast<uint32_t>(kCsStages); ++b) issue(b);
+  }
+  uint32_t s = 0;
+  if (seg_off) {
+    while (s + 1 < nseg && seg_off[s + 1] <= p0) ++s;
+  }
+  uint64_t seg_end = seg_off ? seg_off[s + 1] : npos;
+  const uint64_t seg_stride = 32ull * W;
+  const uint32_t jj = ok ? j : 0u;  // idle columns read column 0 (inside the stage), never flushed
+  HSCounter<8> h;
+  for (uint32_t b = 0; b < nbatch; ++b) {
+    const uint32_t st = b % kCsStages;
+    tc::mbar_wait(tc::smem_u32(&full[st]), (b / kCsStages) & 1u);
+    const uint64_t pb = p0 + static_cast<uint64_t>(b) * kCsRows;
+    const uint64_t be = min(p1, pb + kCsRows);
+    const uint32_t* src = cs_rows + st * kCsRows * ncols + jj;
+    if (be == pb + kCsRows && be <= seg_end) {
+      // the common case: a full batch inside one class segment
+      uint32_t x[kCsRows];
+#pragma unroll
+      for (int t = 0; t < kCsRows; ++t) x[t] = src[t * ncols];
+      if constexpr (kCsRows == 8) {
+        h.add8(x);
+      } else {
+        if constexpr (kCsRows == 8) {
+          h.add8(x);
+        } else {
+#pragma unroll
+          for (int t = 0; t < kCsRows; t += 16) h.add16(x + t);
+        }
+      }
+      if (be == seg_end && be < p1) {
+        if (ok) flush_counts(h, c0 + j, seg_stride, s, single, dsts, ndst);
+        h = HSCounter<8>();
+        do {
+          ++s;
+          seg_end = seg_off[s + 1];
+        } while (seg_end <= be && s + 1 < nseg);
+      }
+    } else {
+      uint64_t lo = pb;
+      while (lo < be) {
+        const uint64_t hi = min(be, seg_end);
+        const uint32_t tlo = static_cast<uint32_t>(lo - pb), thi = static_cast<uint32_t>(hi - pb);
+        uint32_t x[kCsRows];
+#pragma unroll
+        for (int t = 0; t < kCsRows; ++t) x[t] = (t >= tlo && t < thi) ? src[t * ncols] : 0u;
+        if constexpr (kCsRows == 8) {
+          h.add8(x);
+        } else {
+#pragma unroll
+          for (int t = 0; t < kCsRows; t += 16) h.add16(x + t);
+        }
+        lo = hi;
+        if (hi == seg_end && hi < p1) {  // class segment ends inside the chunk
+          if (ok) flush_counts(h, c0 + j, seg_stride, s, single, dsts, ndst);
+          h = HSCounter<8>();
+          do {
+            ++s;
+            seg_end = seg_off[s + 1];
+          } while (seg_end <= lo && s + 1 < nseg);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&empty[st])) : "memory");
+    if (threadIdx.x < 32 && b + kCsStages < nbatch) issue(b + kCsStages);
+  }
+  if (ok) flush_counts(h, c0 + j, seg_stride, s, single, dsts, ndst);
+}
+
+// Grid for column_count_kernel: one warp per item (the one-shot grid measured
+// faster than a wave-balanced grid-stride one).
+template <class CT>
+unsigned column_count_grid(uint64_t npos, uint32_t W, uint32_t chunk) {
+  const uint64_t items = (npos + chunk - 1) / chunk * ((W + 31) / 32);
+  return static_cast<unsigned>(std::max<uint64_t>(1, (items + 3) / 4));
+}
+
 void launch_column_count_u32(cudaStream_t st, const uint32_t* m, uint32_t W, const uint32_t* perm,
-                             const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, uint32_t* counts) {
-  launch_column_count_peers(st, m, W, perm, seg_off, nseg, max_pos, counts, nullptr, 1);
+                             const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, uint32_t* counts, uint32_t ldm) {
+  launch_column_count_peers(st, m, W, perm, seg_off, nseg, max_pos, counts, nullptr, 1, ldm);
+}
+
+template <class CT>
+void launch_column_count_any(cudaStream_t st, const uint32_t* m, uint32_t W, uint32_t ldm, const uint32_t* perm,
+                             const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, CT* single,
+                             CT* const* dsts_dev, uint32_t ndst) {
+  if (max_pos == 0 || W == 0) return;
+  if (max_pos > 0xFFFFFFFFull) invalid("class counts: more than 2^32 rows per call");
+  if (ldm == 0) ldm = W;
+  if (ldm < W) invalid("class counts: row pitch < words per row");
+  const uint32_t chunk = 2048;
+  if (ldm % 4 == 0 && (reinterpret_cast<uintptr_t>(m) & 15u) == 0) {
+    // pitched, 16-byte aligned rows: TMA-staged whole-row reads
+    const uint32_t W4 = (W + 3) / 4 * 4;
+    const uint32_t nranges = (W4 + kCsMaxCols - 1) / kCsMaxCols;
+    const uint32_t ncols = (W4 / 4 + nranges - 1) / nranges * 4;  // balanced ranges, multiple of 4
+    const uint32_t threads = (ncols + 31) / 32 * 32;
+    dim3 grid(nranges, static_cast<unsigned>((max_pos + chunk - 1) / chunk));
+    // 16 rows x 2 stages (40 KB: 5 CTAs per SM) measured best at CHB-MIT, 5.65 M
+    // rows: 1.42 ms = 5.0 TB/s; 16 x 3 1.47, 32 x 2 1.50, 16 x 4 1.71, 8 x 4
+    // 1.78, 16 x 6 3.06 (1 CTA per SM) — CTAs per SM matter more than depth
+    int rows_per_stage = 16, stages = 2;
+    if (const char* e = getenv("HVB200_CS_SHAPE")) sscanf(e, "%d,%d", &rows_per_stage, &stages);  // tuning
+    auto go = [&](auto kern, int R, int S) {
+      const size_t smem = static_cast<size_t>(S) * R * ncols * 4;
+      ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+         "cudaFuncSetAttribute");
+      kern<<<grid, threads, smem, st>>>(m, W, ldm, perm, seg_off, nseg, max_pos, chunk, ncols, single, dsts_dev,
+                                        dsts_dev ? ndst : 1u);
+    };
+#define HV_CS(R, S)                                   \
+  if (rows_per_stage == R && stages == S) {           \
+    go(column_count_staged_kernel<CT, R, S>, R, S);   \
+    launched("column_count_staged_kernel");           \
+    return;                                           \
+  }
+    HV_CS(8, 4) HV_CS(16, 3) HV_CS(16, 4) HV_CS(32, 2)
+#undef HV_CS
+    go(column_count_staged_kernel<CT, 16, 2>, 16, 2);
+    launched("column_count_staged_kernel");
+    return;
+  }
+  const unsigned grid = column_count_grid<CT>(max_pos, W, chunk);
+  column_count_kernel<CT><<<grid, 128, 0, st>>>(m, W, ldm, perm, seg_off, nseg, max_pos, chunk, single, dsts_dev,
+                                                dsts_dev ? ndst : 1u);
+  launched("column_count_kernel");
 }
 
 void launch_column_count_peers(cudaStream_t st, const uint32_t* m, uint32_t W, const uint32_t* perm,
                                const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, uint32_t* single,
-                               uint32_t* const* dsts_dev, uint32_t ndst) {
-  if (max_pos == 0 || W == 0) return;
-  if (max_pos > 0xFFFFFFFFull) invalid("class counts: more than 2^32 rows per call");
-  const uint32_t chunk = 2048;
-  dim3 grid(grid_for(W, 128), static_cast<unsigned>((max_pos + chunk - 1) / chunk));
-  column_count_kernel<uint32_t><<<grid, 128, 0, st>>>(m, W, perm, seg_off, nseg, max_pos, chunk, single, dsts_dev,
-                                                      dsts_dev ? ndst : 1u);
-  launched("column_count_kernel");
+                               uint32_t* const* dsts_dev, uint32_t ndst, uint32_t ldm) {
+  launch_column_count_any<uint32_t>(st, m, W, ldm, perm, seg_off, nseg, max_pos, single, dsts_dev, ndst);
 }
 
 __global__ void widen_u64_kernel(const unsigned long long* __restrict__ in, uint32_t dim, uint64_t* __restrict__ out) {
@@ -366,12 +592,9 @@ hv_status hv_vertical_sum(hv_context* ctx, const uint32_t* m, size_t rows, size_
     DevBuf<uint64_t> d_out(dim, ctx->stream);
     d_in.upload(m);
     d_cnt.zero();
-    const uint32_t chunk = 2048;
-    dim3 grid(grid_for(W, 128), static_cast<unsigned>((rows + chunk - 1) / chunk));
     if (rows > 0xFFFFFFFFull) invalid("vertical_sum: more than 2^32 rows");
-    column_count_kernel<unsigned long long><<<grid, 128, 0, ctx->stream>>>(d_in.ptr, W, nullptr, nullptr, 1, rows,
-                                                                          chunk, d_cnt.ptr, nullptr, 1);
-    launched("column_count_kernel");
+    launch_column_count_any<unsigned long long>(ctx->stream, d_in.ptr, W, W, nullptr, nullptr, 1, rows, d_cnt.ptr,
+                                                nullptr, 1);
     widen_u64_kernel<<<grid_for(dim, 256), 256, 0, ctx->stream>>>(d_cnt.ptr, dim, d_out.ptr);
     launched("widen_u64_kernel");
     d_out.download(out);

@@ -146,8 +146,11 @@ inline unsigned grid_for(size_t n, unsigned block, unsigned cap = 1u << 30) {
 }
 
 // Column counts over a permuted, class-segmented row sequence (hv_bits.cu).
+// ldm: row pitch in words (0 = W); pitched 16-byte-aligned rows (ldm % 4 == 0)
+// take the TMA-staged kernel.
 void launch_column_count_u32(cudaStream_t st, const uint32_t* m, uint32_t W, const uint32_t* perm,
-                             const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, uint32_t* counts);
+                             const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, uint32_t* counts,
+                             uint32_t ldm = 0);
 // Label bucketing for class counts (hv_model.cu): histogram (validated, into
 // a zeroed hist), segment offsets, class-sorted permutation; class_rows += hist.
 void label_bucket_device(hv_context* ctx, cudaStream_t st, const int32_t* labels, size_t rows, size_t C,
@@ -157,7 +160,7 @@ void label_bucket_device(hv_context* ctx, cudaStream_t st, const int32_t* labels
 // buffers listed in the device array dsts_dev (every rank's, over peer memory).
 void launch_column_count_peers(cudaStream_t st, const uint32_t* m, uint32_t W, const uint32_t* perm,
                                const uint64_t* seg_off, uint32_t nseg, uint64_t max_pos, uint32_t* single,
-                               uint32_t* const* dsts_dev, uint32_t ndst);
+                               uint32_t* const* dsts_dev, uint32_t ndst, uint32_t ldm = 0);
 
 // Encoder entry points shared with the fold pipeline (hv_encode.cu). Words
 // [w0, w0 + wcount) of every row are written to out[row * ldo + k]; wcount = 0
@@ -296,6 +299,20 @@ struct HSCounter {
     csa(foursB, twos, twos, twosA, twosB);
     csa(eightsB, fours, fours, foursA, foursB);
     csa(sixteens, eights, eights, eightsA, eightsB);
+    add16w(sixteens);
+  }
+  // adds 8 input words
+  __device__ __forceinline__ void add8(const uint32_t x[8]) {
+    uint32_t twosA, twosB, foursA, foursB, eightsA;
+    csa(twosA, ones, ones, x[0], x[1]);
+    csa(twosB, ones, ones, x[2], x[3]);
+    csa(foursA, twos, twos, twosA, twosB);
+    csa(twosA, ones, ones, x[4], x[5]);
+    csa(twosB, ones, ones, x[6], x[7]);
+    csa(foursB, twos, twos, twosA, twosB);
+    csa(eightsA, fours, fours, foursA, foursB);
+    const uint32_t sixteens = eights & eightsA;
+    eights ^= eightsA;
     add16w(sixteens);
   }
   // plane k of the binary count (k < 4 + NH)

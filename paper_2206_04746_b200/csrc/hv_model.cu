@@ -151,25 +151,42 @@ __global__ void refresh_kernel(const double* __restrict__ acc, const double* __r
 // model.cpp:303-320 + 69-79 + 96-104: one warp per query row, C popcounts of
 // row ^ class_vector reduced with REDUX; argmin with strict < (lowest class
 // wins ties). Integer popcounts order exactly like popc/D doubles.
-template <int CB>
+//
+// HBM-bound at few classes (CHB-MIT: 2 x 313 POPC per 1,256-byte row), so the
+// row is streamed with U independent word loads in flight per lane
+// (evict-first: rows are read once); CB classes are scored per pass over the
+// row, class words come from L1.
+template <int CB, int U>
 __global__ void __launch_bounds__(256) predict_hamming_kernel(const uint32_t* __restrict__ cv, uint32_t C, uint32_t D,
-                                                              uint32_t W, const uint32_t* __restrict__ enc,
-                                                              uint64_t rows, int32_t* __restrict__ labels,
-                                                              double* __restrict__ dist, uint32_t* __restrict__ pops) {
+                                                              uint32_t W, uint32_t ldq,
+                                                              const uint32_t* __restrict__ enc, uint64_t rows,
+                                                              int32_t* __restrict__ labels, double* __restrict__ dist,
+                                                              uint32_t* __restrict__ pops) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += stride) {
-    const uint32_t* q = enc + r * W;
+    const uint32_t* q = enc + r * ldq;
     uint32_t best = 0, bestp = 0xFFFFFFFFu;
     for (uint32_t c0 = 0; c0 < C; c0 += CB) {
       uint32_t acc[CB];
 #pragma unroll
       for (int k = 0; k < CB; ++k) acc[k] = 0;
-      for (uint32_t w = lane; w < W; w += 32u) {
-        const uint32_t x = q[w];
+      for (uint32_t w0 = 0; w0 < W; w0 += 32u * U) {
+        uint32_t x[U];
 #pragma unroll
-        for (int k = 0; k < CB; ++k) {
-          if (c0 + k < C) acc[k] += __popc(x ^ cv[static_cast<uint64_t>(c0 + k) * W + w]);
+        for (int u = 0; u < U; ++u) {
+          const uint32_t w = w0 + lane + 32u * u;
+          x[u] = w < W ? __ldcs(q + w) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t w = w0 + lane + 32u * u;
+          if (w < W) {
+#pragma unroll
+            for (int k = 0; k < CB; ++k) {
+              if (c0 + k < C) acc[k] += __popc(x[u] ^ __ldg(cv + static_cast<uint64_t>(c0 + k) * W + w));
+            }
+          }
         }
       }
 #pragma unroll
@@ -189,6 +206,132 @@ __global__ void __launch_bounds__(256) predict_hamming_kernel(const uint32_t* __
       }
     }
     if (lane == 0 && labels) labels[r] = static_cast<int32_t>(best);
+  }
+}
+
+// The same scan over pitched, 16-byte aligned query rows (the engine's own
+// layout, ldq % 4 == 0): each lane reads whole uint4s of the row (U = 3 in
+// flight: 96 words per lane-round), the class vectors are staged once per CTA
+// in shared memory at pitch W4 = ceil(W / 4) uint4s with zero padding, and
+// the words of the last uint4 past W are masked (the row padding is never
+// written by the encoder). scripts/probe_stream.cu at CHB-MIT: 6.1-6.2 TB/s
+// against 4.1 for 4-byte loads of unpitched rows.
+template <int CB>
+__global__ void __launch_bounds__(256) predict_hamming_pitched_kernel(
+    const uint32_t* __restrict__ cv, uint32_t C, uint32_t D, uint32_t W, uint32_t ldq, const uint32_t* __restrict__ enc,
+    uint64_t rows, int32_t* __restrict__ labels, double* __restrict__ dist, uint32_t* __restrict__ pops) {
+  constexpr int U = 3;
+  extern __shared__ uint4 cvs[];  // [C][W4]
+  const uint32_t W4 = (W + 3) / 4;
+  uint32_t* cvw = reinterpret_cast<uint32_t*>(cvs);
+  for (uint32_t i = threadIdx.x; i < C * W4 * 4; i += blockDim.x) {
+    const uint32_t c = i / (W4 * 4), w = i % (W4 * 4);
+    cvw[i] = w < W ? __ldg(cv + static_cast<uint64_t>(c) * W + w) : 0u;
+  }
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t tail = W & 3u;  // valid words of the last uint4 (0 = all four)
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += stride) {
+    const uint4* q = reinterpret_cast<const uint4*>(enc + r * ldq);
+    uint32_t best = 0, bestp = 0xFFFFFFFFu;
+    for (uint32_t c0 = 0; c0 < C; c0 += CB) {
+      uint32_t acc[CB];
+#pragma unroll
+      for (int k = 0; k < CB; ++k) acc[k] = 0;
+      for (uint32_t v0 = 0; v0 < W4; v0 += 32u * U) {
+        uint4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t v = v0 + lane + 32u * u;
+          x[u] = v < W4 ? __ldcs(q + v) : make_uint4(0, 0, 0, 0);
+          if (v == W4 - 1 && tail) {
+            if (tail < 4) x[u].w = 0;
+            if (tail < 3) x[u].z = 0;
+            if (tail < 2) x[u].y = 0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t v = v0 + lane + 32u * u;
+          if (v < W4) {
+#pragma unroll
+            for (int k = 0; k < CB; ++k) {
+              if (c0 + k < C) {
+                const uint4 c = cvs[(c0 + k) * W4 + v];
+                acc[k] += __popc(x[u].x ^ c.x) + __popc(x[u].y ^ c.y) + __popc(x[u].z ^ c.z) + __popc(x[u].w ^ c.w);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < CB; ++k) {
+        const uint32_t tot = __reduce_add_sync(FULL, acc[k]);
+        const uint32_t c = c0 + k;
+        if (c < C) {
+          if (tot < bestp) {
+            bestp = tot;
+            best = c;
+          }
+          if (lane == (c & 31u)) {
+            if (pops) pops[r * C + c] = tot;
+            if (dist) dist[r * C + c] = static_cast<double>(tot) / static_cast<double>(D);
+          }
+        }
+      }
+    }
+    if (lane == 0 && labels) labels[r] = static_cast<int32_t>(best);
+  }
+}
+
+// Two classes, labels only (the CHB-MIT workload): popc(q^c1) < popc(q^c0)
+// <=> 2 popc(d & (q ^ c0)) > popc(d) with d = c0 ^ c1 — on bits where the
+// classes agree both distances count the same, where they differ exactly one
+// does. One LOP3 + one POPC per word instead of two XOR + two POPC, so the
+// scan stays on HBM instead of the XU pipe. Ties (2A == |d|) keep class 0, the
+// reference's strict < (model.cpp:96-104). Pitched 16-byte rows.
+__global__ void __launch_bounds__(256) predict_two_class_kernel(const uint32_t* __restrict__ cv, uint32_t W,
+                                                                uint32_t ldq, const uint32_t* __restrict__ enc,
+                                                                uint64_t rows, int32_t* __restrict__ labels) {
+  constexpr int U = 3;
+  extern __shared__ uint4 cd[];  // [W4] c0, then [W4] d = c0 ^ c1 (zero padded)
+  const uint32_t W4 = (W + 3) / 4;
+  uint32_t* cw = reinterpret_cast<uint32_t*>(cd);
+  uint32_t dpop = 0;
+  for (uint32_t w = threadIdx.x; w < W4 * 4; w += blockDim.x) {
+    const uint32_t a = w < W ? __ldg(cv + w) : 0u, b = w < W ? __ldg(cv + W + w) : 0u;
+    cw[w] = a;
+    cw[W4 * 4 + w] = a ^ b;
+  }
+  __syncthreads();
+  for (uint32_t w = threadIdx.x & 31u; w < W4 * 4; w += 32u) dpop += __popc(cw[W4 * 4 + w]);
+  dpop = __reduce_add_sync(FULL, dpop);  // |d| (every warp computes it)
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += stride) {
+    const uint4* q = reinterpret_cast<const uint4*>(enc + r * ldq);
+    uint32_t a = 0;
+    for (uint32_t v0 = 0; v0 < W4; v0 += 32u * U) {
+      uint4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t v = v0 + lane + 32u * u;
+        x[u] = v < W4 ? __ldcs(q + v) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t v = v0 + lane + 32u * u;
+        if (v < W4) {
+          // the row's padding words meet d's zero padding: no mask needed
+          const uint4 c = cd[v], d = cd[W4 + v];
+          a += __popc((x[u].x ^ c.x) & d.x) + __popc((x[u].y ^ c.y) & d.y) + __popc((x[u].z ^ c.z) & d.z) +
+               __popc((x[u].w ^ c.w) & d.w);
+        }
+      }
+    }
+    a = __reduce_add_sync(FULL, a);
+    if (lane == 0) labels[r] = 2 * a > dpop ? 1 : 0;
   }
 }
 
@@ -597,15 +740,16 @@ void label_bucket_device(hv_context* ctx, cudaStream_t st, const int32_t* labels
 }
 
 // class counts of `rows` encoded rows into counts (C x 32W, added) and class_rows (added)
+// (row pitch ldm words, 0 = W)
 void class_counts_device(hv_context* ctx, cudaStream_t st, const uint32_t* enc, size_t rows, size_t W,
-                         const int32_t* labels, size_t C, uint32_t* counts, uint64_t* class_rows) {
+                         const int32_t* labels, size_t C, uint32_t* counts, uint64_t* class_rows, size_t ldm = 0) {
   if (rows == 0) return;
   DevBuf<uint32_t> hist(C, st), cursor(C, st), perm(rows, st);
   DevBuf<uint64_t> offsets(C + 1, st);
   hist.zero();
   label_bucket_device(ctx, st, labels, rows, C, hist.ptr, offsets.ptr, cursor.ptr, perm.ptr, class_rows);
   launch_column_count_u32(st, enc, static_cast<uint32_t>(W), perm.ptr, offsets.ptr, static_cast<uint32_t>(C), rows,
-                          counts);
+                          counts, static_cast<uint32_t>(ldm));
 }
 
 void binarize_counts_device(hv_context* ctx, cudaStream_t st, const uint32_t* counts, const uint64_t* class_rows,
@@ -617,15 +761,61 @@ void binarize_counts_device(hv_context* ctx, cudaStream_t st, const uint32_t* co
   launched("binarize_counts_kernel");
 }
 
+// (query row pitch ldq words, 0 = W; pitched rows need C < 32)
 void predict_hamming_device(hv_context* ctx, cudaStream_t st, const uint32_t* cv, size_t C, size_t D,
-                            const uint32_t* enc, size_t rows, int32_t* labels, double* dist, uint32_t* pops) {
+                            const uint32_t* enc, size_t rows, int32_t* labels, double* dist, uint32_t* pops,
+                            size_t ldq = 0) {
   if (rows == 0) return;
   const size_t W = words_per_row(D);
+  if (ldq == 0) ldq = W;
+  if (ldq < W) invalid("predict: row pitch < words per row");
+  if (ldq != W) {
+    if (C >= static_cast<size_t>(kScanCls)) invalid("predict: pitched query rows need fewer than 32 classes");
+    const size_t W4 = (W + 3) / 4;
+    const size_t smem = C * W4 * 16;
+    if (C == 2 && !dist && !pops && labels && ldq % 4 == 0 && (reinterpret_cast<uintptr_t>(enc) & 15u) == 0 &&
+        smem <= 96 * 1024) {
+      const unsigned grid = sgrid(ctx, rows * 32, 256, 32);
+      ck(cudaFuncSetAttribute(predict_two_class_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(smem)),
+         "cudaFuncSetAttribute");
+      predict_two_class_kernel<<<grid, 256, smem, st>>>(cv, static_cast<uint32_t>(W), static_cast<uint32_t>(ldq), enc,
+                                                        rows, labels);
+      launched("predict_two_class_kernel");
+      return;
+    }
+    if (ldq % 4 == 0 && (reinterpret_cast<uintptr_t>(enc) & 15u) == 0 && smem <= 96 * 1024) {
+      // 16-byte rows: class vectors staged in shared memory, uint4 row reads
+      const unsigned grid = sgrid(ctx, rows * 32, 256, 32);
+#define HV_PP(CB)                                                                                          \
+  do {                                                                                                     \
+    ck(cudaFuncSetAttribute(predict_hamming_pitched_kernel<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                            static_cast<int>(smem)),                                                       \
+       "cudaFuncSetAttribute");                                                                            \
+    predict_hamming_pitched_kernel<CB><<<grid, 256, smem, st>>>(                                           \
+        cv, static_cast<uint32_t>(C), static_cast<uint32_t>(D), static_cast<uint32_t>(W),                  \
+        static_cast<uint32_t>(ldq), enc, rows, labels, dist, pops);                                        \
+  } while (0)
+      if (C <= 2) {
+        HV_PP(2);
+      } else if (C <= 4) {
+        HV_PP(4);
+      } else if (C <= 8) {
+        HV_PP(8);
+      } else {
+        HV_PP(16);
+      }
+#undef HV_PP
+      launched("predict_hamming_pitched_kernel");
+      return;
+    }
+  }
   // classes: < 32 warp per query; 32..63 CTA-tiled POPC scan; >= 64 tensor
-  // cores — tcgen05 (UMMA kind::i8, TMEM accumulators) by default, the legacy
-  // mma.sync path with HVB200_PREDICT_IMMA=1. Measured at 2 M rows: C = 100,
-  // D = 32768: POPC 65 ms, mma.sync 28.7 ms, tcgen05 21.4 ms; C = 64, D = 10000:
-  // 10.4 / 7.7 / 6.2 ms.
+  // cores — tcgen05 (UMMA kind::f8f6f4 on 0/2^-6 e4m3 bytes, rows in TMEM,
+  // hv_predict_tc.cu) by default, the legacy mma.sync path with
+  // HVB200_PREDICT_IMMA=1. Measured at 2 M rows: C = 100,
+  // D = 32768: POPC 65 ms, mma.sync 27.6 ms, tcgen05 5.87 ms; C = 64,
+  // D = 10000: mma.sync 7.3 ms, tcgen05 3.0 ms.
   const bool many = C >= 64 && getenv("HVB200_PREDICT_WARP") == nullptr && getenv("HVB200_PREDICT_POPC") == nullptr;
   if (many && getenv("HVB200_PREDICT_IMMA") == nullptr) {
     DevBuf<unsigned long long> best(rows, st);
@@ -693,14 +883,29 @@ void predict_hamming_device(hv_context* ctx, cudaStream_t st, const uint32_t* cv
     }
     return;
   }
-  const unsigned grid = sgrid(ctx, rows * 32, 256, 8);
-  if (C <= 2) {
-    predict_hamming_kernel<2><<<grid, 256, 0, st>>>(cv, C, D, W, enc, rows, labels, dist, pops);
-  } else if (C <= 4) {
-    predict_hamming_kernel<4><<<grid, 256, 0, st>>>(cv, C, D, W, enc, rows, labels, dist, pops);
-  } else {
-    predict_hamming_kernel<8><<<grid, 256, 0, st>>>(cv, C, D, W, enc, rows, labels, dist, pops);
+  // 16 CTAs of 8 warps per SM (two resident waves), 4 words in flight per
+  // lane per round: scripts/probe_stream.cu at CHB-MIT, 1.41 M rows — 4.11 TB/s
+  // against 3.37 for one word per lane at 8 CTAs/SM and 3.84 for 10 words
+  const unsigned grid = sgrid(ctx, rows * 32, 256, 16);
+#define HV_PH(CB, U) \
+  predict_hamming_kernel<CB, U><<<grid, 256, 0, st>>>(cv, C, D, W, ldq, enc, rows, labels, dist, pops)
+#define HV_PH_U(CB) \
+  if (W <= 64) {    \
+    HV_PH(CB, 2);   \
+  } else {          \
+    HV_PH(CB, 4);   \
   }
+  if (C <= 2) {
+    HV_PH_U(2)
+  } else if (C <= 4) {
+    HV_PH_U(4)
+  } else if (C <= 8) {
+    HV_PH_U(8)
+  } else {
+    HV_PH_U(16)
+  }
+#undef HV_PH_U
+#undef HV_PH
   launched("predict_hamming_kernel");
 }
 
@@ -1042,6 +1247,19 @@ hv_status hv_dev_class_counts(hv_context* ctx, const uint32_t* encoded, size_t r
   });
 }
 
+hv_status hv_dev_class_counts_pitched(hv_context* ctx, const uint32_t* encoded, size_t ldw, size_t rows, size_t dim,
+                                      const int32_t* labels, size_t class_count, uint32_t* counts,
+                                      uint64_t* class_rows) {
+  return guarded([&] {
+    require(ctx);
+    if (class_count == 0) invalid("class_counts: need at least one class");
+    class_counts_device(ctx, ctx->stream, encoded, rows, words_per_row(dim), labels, class_count, counts, class_rows,
+                        ldw);
+  });
+}
+
+size_t hv_row_pitch_words(size_t dim) { return (words_per_row(dim) + 3) / 4 * 4; }
+
 hv_status hv_dev_binarize_counts(hv_context* ctx, const uint32_t* counts, const uint64_t* class_rows, size_t class_count,
                                  size_t dim, const uint32_t* tiebreak, uint32_t* class_vectors) {
   return guarded([&] {
@@ -1058,6 +1276,17 @@ hv_status hv_dev_predict_hamming(hv_context* ctx, const uint32_t* class_vectors,
     if (class_count == 0 || dim == 0) invalid("predict: empty model");
     predict_hamming_device(ctx, ctx->stream, class_vectors, class_count, dim, encoded, rows, labels, distances,
                            popcounts);
+  });
+}
+
+hv_status hv_dev_predict_hamming_pitched(hv_context* ctx, const uint32_t* class_vectors, size_t class_count,
+                                         size_t dim, const uint32_t* encoded, size_t ldw, size_t rows, int32_t* labels,
+                                         double* distances, uint32_t* popcounts) {
+  return guarded([&] {
+    require(ctx);
+    if (class_count == 0 || dim == 0) invalid("predict: empty model");
+    predict_hamming_device(ctx, ctx->stream, class_vectors, class_count, dim, encoded, rows, labels, distances,
+                           popcounts, ldw);
   });
 }
 
@@ -1190,6 +1419,7 @@ hv_status hv_dev_apply_online_delta(hv_context* ctx, size_t class_count, size_t 
 // experiment.cpp:159-177 with HBM-resident hypervectors.
 struct hv_fold {
   size_t train_rows = 0, test_rows = 0, F = 0, D = 0, W = 0, C = 0;
+  size_t ldw = 0;  // row pitch of enc: W rounded up to 16 bytes (uint4 / TMA row reads)
   hvb::DevBuf<uint32_t> enc, counts;
   hvb::DevBuf<uint64_t> class_rows;
 };
@@ -1251,8 +1481,10 @@ hv_status hv_fold_encode_train(hv_context* ctx, const uint32_t* train_bins, size
     fold->D = dim;
     fold->W = W;
     fold->C = class_count;
+    fold->ldw = hv_row_pitch_words(dim);
+    const size_t ldw = fold->ldw;
     cudaStream_t st = ctx->stream;
-    fold->enc = DevBuf<uint32_t>(rows * W, st);
+    fold->enc = DevBuf<uint32_t>(rows * ldw, st);
     fold->counts = DevBuf<uint32_t>(class_count * 32 * W, st);
     fold->class_rows = DevBuf<uint64_t>(class_count, st);
     fold->counts.zero();
@@ -1269,7 +1501,8 @@ hv_status hv_fold_encode_train(hv_context* ctx, const uint32_t* train_bins, size
     size_t k = 0;
     uint32_t* enc = fold->enc.ptr;
     uint64_t bad = encode_host_bins(ctx, train_bins, train_rows, features, bins, dim, HV_BIND_ID_LEVEL, d_id.ptr,
-                                    d_val.ptr, d_tie.ptr, [&](size_t r0, size_t) { return enc + r0 * W; }, b8, chunk, k);
+                                    d_val.ptr, d_tie.ptr, [&](size_t r0, size_t) { return enc + r0 * ldw; }, b8,
+                                    chunk, k, {}, ldw);
     if (bad == ~0ull) {
       // classical counts of the train rows overlap the staging/encode of the test rows
       cudaEvent_t ev;
@@ -1278,9 +1511,10 @@ hv_status hv_fold_encode_train(hv_context* ctx, const uint32_t* train_bins, size
       ck(cudaStreamWaitEvent(ctx->stream, ev, 0), "wait");
       cudaEventDestroy(ev);
       class_counts_device(ctx, ctx->stream, enc, train_rows, W, d_y.ptr, class_count, fold->counts.ptr,
-                          fold->class_rows.ptr);
+                          fold->class_rows.ptr, ldw);
       bad = encode_host_bins(ctx, test_bins, test_rows, features, bins, dim, HV_BIND_ID_LEVEL, d_id.ptr, d_val.ptr,
-                             d_tie.ptr, [&](size_t r0, size_t) { return enc + (train_rows + r0) * W; }, b8, chunk, k);
+                             d_tie.ptr, [&](size_t r0, size_t) { return enc + (train_rows + r0) * ldw; }, b8, chunk,
+                             k, {}, ldw);
       if (bad != ~0ull) bad += train_rows * features;
     }
     ck(cudaStreamSynchronize(ctx->aux), "sync aux");
@@ -1319,8 +1553,18 @@ hv_status hv_fold_predict(hv_context* ctx, hv_fold* fold, const uint32_t* model_
     DevBuf<int32_t> lab(fold->test_rows, st);
     tie.upload(model_tiebreak);
     binarize_counts_device(ctx, st, fold->counts.ptr, fold->class_rows.ptr, fold->C, fold->D, tie.ptr, cv.ptr);
-    predict_hamming_device(ctx, st, cv.ptr, fold->C, fold->D, fold->enc.ptr + fold->train_rows * fold->W,
-                           fold->test_rows, lab.ptr, nullptr, nullptr);
+    const uint32_t* test = fold->enc.ptr + fold->train_rows * fold->ldw;
+    DevBuf<uint32_t> packed;
+    size_t ldq = fold->ldw;
+    if (fold->C >= 32 && fold->ldw != fold->W) {  // the many-class scans read unpitched rows
+      packed = DevBuf<uint32_t>(fold->test_rows * fold->W, st);
+      ck(cudaMemcpy2DAsync(packed.ptr, fold->W * 4, test, fold->ldw * 4, fold->W * 4, fold->test_rows,
+                           cudaMemcpyDeviceToDevice, st),
+         "unpitch test rows");
+      test = packed.ptr;
+      ldq = fold->W;
+    }
+    predict_hamming_device(ctx, st, cv.ptr, fold->C, fold->D, test, fold->test_rows, lab.ptr, nullptr, nullptr, ldq);
     lab.download(labels_out);
     sync(ctx);
   });

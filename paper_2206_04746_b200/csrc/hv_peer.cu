@@ -107,9 +107,10 @@ hv_status hv_shared_free(hv_context* ctx, void* dev_ptr) {
   });
 }
 
-hv_status hv_dev_class_counts_peers(hv_context* ctx, const uint32_t* encoded, size_t rows, size_t dim,
-                                    const int32_t* labels, size_t class_count, uint32_t* const* peer_counts,
-                                    uint64_t* const* peer_class_rows, size_t world) {
+hv_status hv_dev_class_counts_peers_pitched(hv_context* ctx, const uint32_t* encoded, size_t ldw, size_t rows,
+                                            size_t dim, const int32_t* labels, size_t class_count,
+                                            uint32_t* const* peer_counts, uint64_t* const* peer_class_rows,
+                                            size_t world) {
   return guarded([&] {
     require(ctx);
     if (class_count == 0) invalid("class_counts: need at least one class");
@@ -122,11 +123,18 @@ hv_status hv_dev_class_counts_peers(hv_context* ctx, const uint32_t* encoded, si
     hist.zero();
     label_bucket_device(ctx, st, labels, rows, C, hist.ptr, offsets.ptr, cursor.ptr, perm.ptr);
     launch_column_count_peers(st, encoded, static_cast<uint32_t>(W), perm.ptr, offsets.ptr, static_cast<uint32_t>(C),
-                              rows, nullptr, peer_counts, static_cast<uint32_t>(world));
+                              rows, nullptr, peer_counts, static_cast<uint32_t>(world), static_cast<uint32_t>(ldw));
     add_rows_peers_kernel<<<grid_for(C * world, 128), 128, 0, st>>>(hist.ptr, static_cast<uint32_t>(C),
                                                                    peer_class_rows, static_cast<uint32_t>(world));
     launched("add_rows_peers_kernel");
   });
+}
+
+hv_status hv_dev_class_counts_peers(hv_context* ctx, const uint32_t* encoded, size_t rows, size_t dim,
+                                    const int32_t* labels, size_t class_count, uint32_t* const* peer_counts,
+                                    uint64_t* const* peer_class_rows, size_t world) {
+  return hv_dev_class_counts_peers_pitched(ctx, encoded, 0, rows, dim, labels, class_count, peer_counts,
+                                           peer_class_rows, world);
 }
 
 hv_status hv_dev_signal_peers(hv_context* ctx, uint32_t* const* peer_flags, size_t world, size_t rank,

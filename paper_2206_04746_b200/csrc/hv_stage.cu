@@ -222,7 +222,7 @@ size_t stage_chunk_rows(size_t rows, size_t F) {
 uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, size_t F, size_t B, size_t D,
                           hv_binding binding, const uint32_t* d_id, const uint32_t* d_val, const uint32_t* d_tie,
                           const ChunkOut& out_for, DevBuf<uint8_t>* b8, size_t chunk, size_t& k,
-                          const ChunkAfter& after) {
+                          const ChunkAfter& after, size_t ldo) {
   check_bins_u8(B, "encode");
   const size_t ldb = bins_pitch(F);
   HostStager& hs = stager(ctx);
@@ -240,7 +240,12 @@ uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, si
     if (bad != ~0ull) return r0 * F + bad;
     ck(cudaMemcpyAsync(b8[k & 1].ptr, hs.slot[s], n * ldb, cudaMemcpyHostToDevice, st), "H2D bins");
     ck(cudaEventRecord(hs.done[s], st), "cudaEventRecord");
-    encode_device(ctx, st, b8[k & 1].ptr, ldb, n, F, d_id, d_val, B, D, binding, d_tie, out_for(r0, k));
+    if (ldo == 0 || ldo == words_per_row(D)) {
+      encode_device(ctx, st, b8[k & 1].ptr, ldb, n, F, d_id, d_val, B, D, binding, d_tie, out_for(r0, k));
+    } else {
+      encode_device(ctx, st, b8[k & 1].ptr, ldb, n, F, d_id, d_val, B, D, binding, d_tie, out_for(r0, k), true, 0,
+                    words_per_row(D), ldo);
+    }
     if (after) after(r0, n, k, st);
   }
   return ~0ull;

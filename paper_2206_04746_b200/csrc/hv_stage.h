@@ -66,7 +66,7 @@ size_t stage_chunk_rows(size_t rows, size_t F);
 
 // Host uint32 bin rows -> (narrow on host, pinned slot, H2D, encode) in chunks
 // alternating the context's two streams. Chunk k (rows r0 .. r0+n) is encoded
-// into out_for(r0, k); b8 = two device chunk buffers of chunk * bins_pitch(F)
+// into out_for(r0, k) (row pitch ldo words, 0 = unpitched); b8 = two device chunk buffers of chunk * bins_pitch(F)
 // bytes; `after(r0, n, k, stream)` runs per chunk (e.g. to enqueue a D2H of it
 // on its stream). Returns the first offending flat bin index (relative to
 // `bins`) or ~0; on an error the remaining chunks are not enqueued.
@@ -75,7 +75,7 @@ using ChunkAfter = std::function<void(size_t r0, size_t n, size_t k, cudaStream_
 uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, size_t F, size_t B, size_t D,
                           hv_binding binding, const uint32_t* d_id, const uint32_t* d_val, const uint32_t* d_tie,
                           const ChunkOut& out_for, DevBuf<uint8_t>* b8, size_t chunk, size_t& k,
-                          const ChunkAfter& after = {});
+                          const ChunkAfter& after = {}, size_t ldo = 0);
 
 // Copies `bytes` of (pageable) host memory to the device on the context
 // stream through the pinned staging ring (host threads fill a slot while the

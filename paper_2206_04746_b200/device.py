@@ -27,6 +27,20 @@ def _ptr(t: torch.Tensor | None):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+def _rows_view(t: torch.Tensor, W: int) -> int:
+    """Row pitch (in words) of a (rows, W) int32 matrix view whose words are
+    contiguous within a row; rejects anything else."""
+    if t.dim() != 2 or t.shape[1] != W or (t.shape[0] > 1 and t.stride(1) != 1) or t.stride(0) < W:
+        raise ValueError(f"expected a (rows, {W}) int32 row view with unit word stride, got shape "
+                         f"{tuple(t.shape)} strides {t.stride()}")
+    return t.stride(0)
+
+
+def _contig_rows(t: torch.Tensor, W: int, what: str) -> None:
+    if _rows_view(t, W) != W and t.shape[0] > 1:
+        raise ValueError(f"{what}: needs unpitched (contiguous) rows; got row stride {t.stride(0)}")
+
+
 def words_per_row(dim: int) -> int:
     return (dim + 31) // 32
 
@@ -122,13 +136,28 @@ class Engine:
         return out
 
     # -- encode --------------------------------------------------------------
-    def encode(self, bins8: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    def pitched_empty(self, rows: int) -> torch.Tensor:
+        """(rows, W) int32 view of rows padded to hv_row_pitch_words(D) words
+        (16-byte rows: uint4 / TMA row reads in class counts and predict)."""
+        ldw = N.lib().hv_row_pitch_words(self.D)
+        return torch.empty((rows, ldw), dtype=I32, device=self.dev)[:, :self.W]
+
+    def encode(self, bins8: torch.Tensor, out: torch.Tensor | None = None, pitched: bool = False) -> torch.Tensor:
+        """Encode uint8 bins; `out` (or a new tensor, pitched if asked) may have
+        any row stride >= W — the encoder writes words [0, W) of each row."""
         rows, ldb = bins8.shape
         if out is None:
-            out = torch.empty((rows, self.W), dtype=I32, device=self.dev)
-        N.check(N.lib().hv_dev_encode(self.dc.h, _ptr(bins8), ldb, rows, self.cb.features, _ptr(self.cb.id_vectors),
-                                      _ptr(self.cb.value_vectors), self.cb.bins, self.D, self.cb.binding,
-                                      _ptr(self.cb.encode_tiebreak), _ptr(out)))
+            out = self.pitched_empty(rows) if pitched else torch.empty((rows, self.W), dtype=I32, device=self.dev)
+        if out.stride(0) == self.W:
+            N.check(N.lib().hv_dev_encode(self.dc.h, _ptr(bins8), ldb, rows, self.cb.features,
+                                          _ptr(self.cb.id_vectors), _ptr(self.cb.value_vectors), self.cb.bins, self.D,
+                                          self.cb.binding, _ptr(self.cb.encode_tiebreak), _ptr(out)))
+        else:
+            _rows_view(out, self.W)
+            N.check(N.lib().hv_dev_encode_words(self.dc.h, _ptr(bins8), ldb, rows, self.cb.features,
+                                                _ptr(self.cb.id_vectors), _ptr(self.cb.value_vectors), self.cb.bins,
+                                                self.D, self.cb.binding, _ptr(self.cb.encode_tiebreak), 0, self.W,
+                                                _ptr(out), out.stride(0)))
         return out
 
     def encode_words(self, bins8: torch.Tensor, word_begin: int, words: int,
@@ -150,8 +179,9 @@ class Engine:
                 torch.zeros(self.C, dtype=torch.int64, device=self.dev))
 
     def class_counts(self, enc: torch.Tensor, labels: torch.Tensor, counts: torch.Tensor, class_rows: torch.Tensor):
-        N.check(N.lib().hv_dev_class_counts(self.dc.h, _ptr(enc), enc.shape[0], self.D, _ptr(labels), self.C,
-                                            _ptr(counts), _ptr(class_rows)))
+        ldw = _rows_view(enc, self.W)
+        N.check(N.lib().hv_dev_class_counts_pitched(self.dc.h, _ptr(enc), ldw, enc.shape[0], self.D, _ptr(labels),
+                                                    self.C, _ptr(counts), _ptr(class_rows)))
 
     def binarize(self, counts: torch.Tensor, class_rows: torch.Tensor, out: torch.Tensor | None = None):
         if out is None:
@@ -177,13 +207,15 @@ class Engine:
         rows = enc.shape[0]
         if labels is None:
             labels = torch.empty(rows, dtype=I32, device=self.dev)
-        N.check(N.lib().hv_dev_predict_hamming(self.dc.h, _ptr(cv), self.C, self.D, _ptr(enc), rows, _ptr(labels),
-                                               _ptr(distances), _ptr(popcounts)))
+        ldw = _rows_view(enc, self.W)
+        N.check(N.lib().hv_dev_predict_hamming_pitched(self.dc.h, _ptr(cv), self.C, self.D, _ptr(enc), ldw, rows,
+                                                       _ptr(labels), _ptr(distances), _ptr(popcounts)))
         return labels
 
     # -- online --------------------------------------------------------------
     def train_online(self, enc: torch.Tensor, labels: torch.Tensor, batch_size: int, gamma: float = 1.0):
         """Exact single-GPU online training (bit-identical to the reference)."""
+        _contig_rows(enc, self.W, "train_online")
         acc = torch.empty((self.C, self.D), dtype=torch.float64, device=self.dev)
         weight = torch.empty(self.C, dtype=torch.float64, device=self.dev)
         counts = torch.empty(self.C, dtype=torch.int64, device=self.dev)
@@ -204,6 +236,7 @@ class Engine:
         identically everywhere. The bootstrap classical pass on batch 0 is an
         all-reduced count like train_classical.
         """
+        _contig_rows(enc_shard, self.W, "train_online_sharded")
         import torch.distributed as dist
 
         # bootstrap: classical on global batch 0
@@ -356,9 +389,10 @@ class PeerCounts(PeerShared):
     def count(self, enc: torch.Tensor, labels: torch.Tensor) -> int:
         self.epoch += 1
         par = self.epoch & 1
-        N.check(N.lib().hv_dev_class_counts_peers(self.e.dc.h, _ptr(enc), enc.shape[0], self.e.D, _ptr(labels),
-                                                  self.e.C, _ptr(self.peer_ptrs(par)),
-                                                  _ptr(self.peer_ptrs(par, self.off_rows)), self.world))
+        ldw = _rows_view(enc, self.e.W)
+        N.check(N.lib().hv_dev_class_counts_peers_pitched(self.e.dc.h, _ptr(enc), ldw, enc.shape[0], self.e.D,
+                                                          _ptr(labels), self.e.C, _ptr(self.peer_ptrs(par)),
+                                                          _ptr(self.peer_ptrs(par, self.off_rows)), self.world))
         self.signal(self.epoch)
         return self.epoch
 

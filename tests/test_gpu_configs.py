@@ -158,3 +158,99 @@ def test_more_than_256_bins_rejected_loudly():
     bins = np.full((4, F), 299, np.uint32)
     with pytest.raises(hv.InvalidArgument, match="exceeds 256"):
         hv.encode_batch(bins, 4, cb, tb)
+
+
+@pytest.mark.parametrize("D,C,rows", [(10000, 2, 9000), (10000, 3, 5000), (1024, 10, 7000), (32768, 5, 2500),
+                                      (96, 4, 3000), (4000, 7, 4100), (20000, 31, 1500)])
+def test_pitched_rows_counts_and_predict_match_unpitched(D, C, rows):
+    """The engine's pitched HBM layout (rows padded to 16 bytes; TMA-staged
+    class counts, uint4 predict) gives exactly the unpitched kernels' counts,
+    labels, popcounts and distances — several row chunks, class segments that
+    end inside a staged batch, two column ranges at D = 32768 — and garbage in
+    the padding words is never read as data."""
+    cbk = dv.DeviceCodebook.make(64, 16, D, seed=D + C)
+    eng = dv.Engine(cbk, C)
+    bins8, _ = eng.synth(0, rows, 0, 3)
+    labels = torch.randint(0, C, (rows,), dtype=torch.int32, device="cuda")
+    flat = eng.encode(bins8)
+    pit = eng.pitched_empty(rows)
+    pit.as_strided((rows, pit.stride(0)), (pit.stride(0), 1)).fill_(-1)  # poison the padding words
+    eng.encode(bins8, out=pit)
+    assert torch.equal(pit, flat)
+    c1, r1 = eng.zero_counts()
+    c2, r2 = eng.zero_counts()
+    eng.class_counts(flat, labels, c1, r1)
+    eng.class_counts(pit, labels, c2, r2)
+    eng.dc.check()
+    assert torch.equal(c1, c2) and torch.equal(r1, r2)
+    cv = eng.binarize(c1, r1)
+    n = rows
+    d1 = torch.empty((n, C), dtype=torch.float64, device="cuda")
+    d2 = torch.empty_like(d1)
+    p1 = torch.empty((n, C), dtype=torch.int32, device="cuda")
+    p2 = torch.empty_like(p1)
+    l1 = eng.predict(cv, flat, distances=d1, popcounts=p1)
+    l2 = eng.predict(cv, pit, distances=d2, popcounts=p2)
+    eng.dc.check()
+    assert torch.equal(l1, l2) and torch.equal(p1, p2) and torch.equal(d1.view(torch.int64), d2.view(torch.int64))
+    # and against the oracle on a sample
+    idx = np.arange(0, n, max(1, n // 50))
+    m = O.NaiveModel(C, D, _u32(cbk.model_tiebreak))
+    m.cv = O.unpack_rows(_u32(cv), D).copy()
+    ol, od = m.predict(_u32(flat[torch.as_tensor(idx, device="cuda")]))
+    np.testing.assert_array_equal(l2[torch.as_tensor(idx, device="cuda")].cpu().numpy(), ol)
+
+
+def test_pitched_rows_rejected_for_many_classes():
+    D, C = 4096, 40
+    cbk = dv.DeviceCodebook.make(32, 16, D, seed=1)
+    eng = dv.Engine(cbk, C)
+    bins8, _ = eng.synth(0, 100, 0, 3)
+    pit = eng.encode(bins8, pitched=True)
+    if pit.stride(0) == pit.shape[1]:
+        pytest.skip("W already a multiple of 4: pitched == unpitched")
+    cv = torch.zeros((C, eng.W), dtype=torch.int32, device="cuda")
+    with pytest.raises(Exception, match="fewer than 32 classes"):
+        eng.predict(cv, pit)
+    with pytest.raises(ValueError, match="unpitched"):
+        eng.train_online(pit, torch.zeros(100, dtype=torch.int32, device="cuda"), 10)
+
+
+@pytest.mark.parametrize("D", [10000, 1024, 333])
+def test_two_class_label_scan_matches_full_scan_with_ties(D):
+    """The two-class labels-only scan (2 popc(d & (q ^ c0)) > popc(d)) gives the
+    same labels as the full two-distance scan, including exact ties (which keep
+    class 0, the reference's strict <) and the extremes q = c0, q = c1."""
+    C, rows = 2, 4000
+    cbk = dv.DeviceCodebook.make(16, 16, D, seed=7)
+    eng = dv.Engine(cbk, C)
+    W = eng.W
+    rng = np.random.default_rng(D)
+    cvb = rng.integers(0, 2, (2, D), dtype=np.uint8)
+    diff = np.nonzero(cvb[0] != cvb[1])[0]
+    if diff.size % 2:
+        cvb[1, diff[-1]] ^= 1
+        diff = diff[:-1]
+    q = np.repeat(cvb[:1], rows, axis=0)
+    # exact ties: every third row takes class 1's value on half the differing bits
+    for i in range(0, rows, 3):
+        sel = rng.choice(diff, diff.size // 2, replace=False)
+        q[i, sel] = cvb[1, sel]
+    noise = rng.random((rows, D)) < 0.3
+    q[1::3] ^= noise[1::3].astype(np.uint8)
+    q[2] = cvb[1]
+    qw = O.pack_rows(q)
+    cvw = O.pack_rows(cvb)
+    ldw = eng.pitched_empty(1).stride(0)
+    store = torch.full((rows, ldw), -1, dtype=torch.int32, device="cuda")
+    store[:, :W] = torch.from_numpy(qw.view(np.int32)).cuda()
+    pit = store[:, :W]
+    cv = torch.from_numpy(cvw.view(np.int32)).cuda()
+    fast = eng.predict(cv, pit)
+    pops = torch.empty((rows, 2), dtype=torch.int32, device="cuda")
+    full = eng.predict(cv, pit, popcounts=pops)
+    eng.dc.check()
+    assert torch.equal(fast, full)
+    p = pops.cpu().numpy()
+    assert (p[::3, 0] == p[::3, 1]).all() and (fast[::3] == 0).all()
+    assert fast[2].item() == 1
