@@ -12,8 +12,8 @@
 // pre-scaled by 8, PRMT splices the byte into the 256-aligned chunk base) and
 // the per-pair offsets are immediates. Counting is a bit-sliced Harley–Seal
 // carry-save tree over 64 features (2 LOP3 per bound word) rippling into the
-// high planes once per 64 features, then a bit-sliced compare against F/2
-// with the tiebreak word.
+// high planes once per 64 features; the counter starts biased so that the
+// majority is its top plane (majority_biased).
 //
 // Binding ceilings per SM and clock: shared memory delivers 32 bound words
 // (128 B), the ALU pipe 64 LOP3 = 32 bound words — both are saturated
@@ -85,21 +85,21 @@ __device__ __forceinline__ Words<NW> hs_tree(uint32_t (&s)[6][NW], Load& ld) {
   return h;
 }
 
-// bit = 2c > F ? 1 : 2c < F ? 0 : tie; plane k < 6 is s[k] (weight 2^k), plane 6+k is hi[k]
+// Majority by a biased counter. The planes (s[0..5], hi[0..NH-1]: K = 6 + NH
+// bits, F < 2^K) start at b = 2^(K-1) - T, T = ceil(F / 2), so the count
+// c + b never overflows K bits and
+//     2c > F  <=>  c >= T + (F even)   2c == F  <=>  c == T (F even)
+// c >= T is the top plane; c == T is the top plane with every lower plane
+// zero. So bit = top for odd F, top & (any lower plane | tie) for even F:
+// 4-6 LOP3 per word instead of a 2-op-per-plane compare against F / 2 with
+// per-plane selects on the runtime F (round 1: ~50 ops per output word).
 template <int NH>
-__device__ __forceinline__ uint32_t majority6(const uint32_t (&pl)[6 + NH], uint32_t F, uint32_t tie) {
-  const uint32_t half_f = F >> 1;
-  uint32_t gt = 0u, eq = 0xFFFFFFFFu;
+__device__ __forceinline__ uint32_t majority_biased(const uint32_t (&pl)[6 + NH], bool odd, uint32_t tie) {
+  constexpr int K = 6 + NH;
+  uint32_t any = 0;
 #pragma unroll
-  for (int k = 5 + NH; k >= 0; --k) {
-    if ((half_f >> k) & 1u) {
-      eq &= pl[k];
-    } else {
-      gt |= eq & pl[k];
-      eq &= ~pl[k];
-    }
-  }
-  return gt | ((F & 1u) ? 0u : (eq & tie));
+  for (int k = 0; k < K - 1; ++k) any |= pl[k];
+  return pl[K - 1] & (odd ? 0xFFFFFFFFu : (any | tie));
 }
 
 template <int NPR, int G, int NH, int MINB, bool PERM>
@@ -156,15 +156,18 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
     }
     const uint64_t r_begin = block * p.block_rows;
     const uint64_t r_end = min(p.rows, r_begin + p.block_rows);
+    // counter bias b = 2^(K-1) - ceil(F / 2) as per-plane all-ones / zero masks
+    const uint32_t bias = (1u << (5 + NH)) - ((p.F + 1) >> 1);
+    const bool odd = p.F & 1u;
     for (uint64_t wrow0 = r_begin + 32ull * warp; wrow0 < r_end; wrow0 += 32ull * G) {
       uint32_t s[6][NW];
       uint32_t hi[NH][NW];
 #pragma unroll
       for (int i = 0; i < NW; ++i) {
 #pragma unroll
-        for (int k = 0; k < 6; ++k) s[k][i] = 0;
+        for (int k = 0; k < 6; ++k) s[k][i] = 0u - ((bias >> k) & 1u);
 #pragma unroll
-        for (int k = 0; k < NH; ++k) hi[k][i] = 0;
+        for (int k = 0; k < NH; ++k) hi[k][i] = 0u - ((bias >> (6 + k)) & 1u);
       }
       // coalesced loads: request i -> row 8i + lr, bytes 16*lq .. 16*lq+15 of the chunk
       const uint4* src[4];
@@ -197,7 +200,6 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
       };
       if (nchunks == 1) stage(std::true_type{}); else stage(std::false_type{});
       __syncwarp();
-      const uint32_t* base[4] = {Sw + (lane ^ 0), Sw + (lane ^ 8), Sw + (lane ^ 16), Sw + (lane ^ 24)};
       for (uint32_t ch = 0; ch < nchunks; ++ch) {
         const bool more = ch + 1 < nchunks;
         if (more) {
@@ -208,7 +210,9 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
         int i = 0;
         uint32_t word = 0;
         auto ld = [&]() -> Words<NW> {
-          if ((i & 3) == 0) word = base[(i >> 4) & 3][(i >> 2) * 32];
+          // (indexing Sw directly keeps this an LDS; through an array of pointers it
+          // compiled to generic LD.E plus a local-memory pointer table)
+          if ((i & 3) == 0) word = Sw[(lane ^ ((static_cast<uint32_t>(i) >> 4 & 3u) << 3)) + (i >> 2) * 32];
           const uint32_t off = __byte_perm(word, tch, 0x7650 | (i & 3));
           const uint8_t* e = sm6 + off + i * kFeatBytes;
           Words<NW> v;
@@ -258,11 +262,12 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
         for (int j = 0; j < NW; ++j) {
           uint32_t c = carry.v[j];
 #pragma unroll
-          for (int k = 0; k < NH; ++k) {
+          for (int k = 0; k < NH - 1; ++k) {
             const uint32_t t = hi[k][j] & c;
             hi[k][j] ^= c;
             c = t;
           }
+          hi[NH - 1][j] ^= c;  // the biased count stays below 2^K: no carry out of the top plane
         }
         if (more) {
           __syncwarp();  // every lane has read its words of this chunk
@@ -282,7 +287,7 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
             for (int k = 0; k < 6; ++k) pl[k] = s[k][j];
 #pragma unroll
             for (int k = 0; k < NH; ++k) pl[6 + k] = hi[k][j];
-            o[wb + j] = majority6<NH>(pl, p.F, __ldg(p.tie + w)) & valid_mask(w, p.D);
+            o[wb + j] = majority_biased<NH>(pl, odd, __ldg(p.tie + w)) & valid_mask(w, p.D);
           }
         }
       }
