@@ -191,6 +191,40 @@ PackedBitMatrix encode(std::span<const std::uint32_t> bins, const Codebook& code
 }
 
 // ------------------------------------------------------------ model.hpp ----
+double hamming_distance_words(std::span<const std::uint32_t> a, std::span<const std::uint32_t> b, std::size_t dim) {
+  double d = 0.0;
+  check(hv_hamming_distance(ctx(), a.data(), b.data(), dim, &d));
+  return d;
+}
+
+double hamming_distance(const PackedBitMatrix& a, std::size_t row_a, const PackedBitMatrix& b, std::size_t row_b) {
+  if (a.dim() != b.dim()) {
+    throw std::invalid_argument("hamming_distance: dimensions " + std::to_string(a.dim()) + " vs " +
+                                std::to_string(b.dim()));
+  }
+  return hamming_distance_words(a.row(row_a), b.row(row_b), a.dim());
+}
+
+double cosine_similarity(std::span<const double> acc, std::span<const std::uint32_t> packed_row, std::size_t dim) {
+  double s = 0.0;
+  check(hv_cosine_similarity(ctx(), acc.data(), acc.size(), packed_row.data(), dim, &s));
+  return s;
+}
+
+HDModel make_empty_model(const ModelConfig& config) {
+  HDModel m = allocate(config);
+  hv_model v = view(m);
+  check(hv_make_empty_model(&v));
+  return m;
+}
+
+ModelSnapshot freeze(const HDModel& model) {
+  // model.cpp:246-248: the batch-start copy of the class vectors (and the
+  // accumulators the cosine metric scores against)
+  return ModelSnapshot{model.class_vectors, model.accumulators};
+}
+
+
 void HDModel::refresh_binarization(std::size_t c) {
   hv_model v = view(*this);
   check(hv_refresh_binarization(ctx(), &v, c));

@@ -252,6 +252,14 @@ hv_status hv_experiment_finish(hv_context* ctx, hv_experiment* ex, size_t class_
                                int positive_class, hv_eval_report* report, uint64_t* n_tested,
                                uint64_t* tested_rows, int32_t* truth, int32_t* predicted, int32_t* final_labels);
 
+/* model.hpp:67-70 hamming_distance / hamming_distance_words on the device:
+ * popc(a ^ b) / dim in double (one row of the predict scan). */
+hv_status hv_hamming_distance(hv_context* ctx, const uint32_t* a, const uint32_t* b, size_t dim, double* out);
+/* model.hpp:74-75 cosine_similarity(acc, packed_row, dim): sequential fp64 dot
+ * and norm like the reference; INVALID_ARGUMENT when acc_len != dim, DOMAIN
+ * ("cosine_similarity: zero vector") for a zero accumulator or empty row. */
+hv_status hv_cosine_similarity(hv_context* ctx, const double* acc, size_t acc_len, const uint32_t* row, size_t dim,
+                               double* out);
 /* model.hpp:67-70 hamming_distance_words (host-side helper, no device) */
 double hv_hamming_distance_words(const uint32_t* a, const uint32_t* b, size_t dim);
 

@@ -237,10 +237,10 @@ void hvo_unpack(const uint32_t* words, size_t rows, size_t dim, uint8_t* out) {
 }
 
 /* ======================================================================= */
-/* Byte-per-bit kernels (reference.cpp:149-227)                            */
+/* Byte-per-bit kernels (reference.cpp:77-155)                            */
 /* ======================================================================= */
 
-/* reference.cpp:149-163 (broadcast when b has one row) */
+/* reference.cpp:77-91 (broadcast when b has one row) */
 int hvo_xor_bind(const uint8_t* a, size_t a_rows, const uint8_t* b, size_t b_rows, size_t dim,
                  uint8_t* out) {
   if (b_rows != a_rows && b_rows != 1) return HVO_INVALID_ARGUMENT;
@@ -251,7 +251,7 @@ int hvo_xor_bind(const uint8_t* a, size_t a_rows, const uint8_t* b, size_t b_row
   return HVO_OK;
 }
 
-/* reference.cpp:165-176: out bit (j + s) mod d = in bit j */
+/* reference.cpp:93-104: out bit (j + s) mod d = in bit j */
 void hvo_rotate(const uint8_t* m, size_t rows, size_t dim, size_t shift, uint8_t* out) {
   if (dim == 0) return;
   const size_t s = shift % dim;
@@ -260,7 +260,7 @@ void hvo_rotate(const uint8_t* m, size_t rows, size_t dim, size_t shift, uint8_t
   }
 }
 
-/* reference.cpp:178-186 */
+/* reference.cpp:106-114 */
 void hvo_horizontal_sum(const uint8_t* m, size_t rows, size_t dim, uint64_t* out) {
   for (size_t r = 0; r < rows; ++r) {
     uint64_t s = 0;
@@ -269,14 +269,14 @@ void hvo_horizontal_sum(const uint8_t* m, size_t rows, size_t dim, uint64_t* out
   }
 }
 
-/* reference.cpp:188-196 */
+/* reference.cpp:116-124 */
 void hvo_transpose(const uint8_t* m, size_t rows, size_t dim, uint8_t* out) {
   for (size_t r = 0; r < rows; ++r) {
     for (size_t j = 0; j < dim; ++j) out[j * rows + r] = m[r * dim + j];
   }
 }
 
-/* reference.cpp:198-206 */
+/* reference.cpp:126-134 */
 void hvo_vertical_sum(const uint8_t* m, size_t rows, size_t dim, uint64_t* out) {
   for (size_t j = 0; j < dim; ++j) out[j] = 0;
   for (size_t r = 0; r < rows; ++r) {
@@ -284,7 +284,7 @@ void hvo_vertical_sum(const uint8_t* m, size_t rows, size_t dim, uint64_t* out) 
   }
 }
 
-/* reference.cpp:208-227 (2c > n -> 1, 2c < n -> 0, else tiebreak) */
+/* reference.cpp:136-155 (2c > n -> 1, 2c < n -> 0, else tiebreak) */
 long long hvo_majority_binarize(const uint64_t* counts, size_t dim, uint64_t n,
                                 const uint8_t* tiebreak, uint8_t* out) {
   for (size_t j = 0; j < dim; ++j) {
@@ -333,7 +333,7 @@ void hvo_discretize_matrix(const double* data, size_t rows, size_t features, con
 }
 
 /* ======================================================================= */
-/* Encode (reference.cpp:274-339; bin checks as encoding.cpp:43-55)        */
+/* Encode (reference.cpp:202-267; bin checks as encoding.cpp:43-55)        */
 /* ======================================================================= */
 
 int hvo_encode_batch(const uint32_t* bin_rows, size_t rows, size_t features,
@@ -356,21 +356,21 @@ int hvo_encode_batch(const uint32_t* bin_rows, size_t rows, size_t features,
     if (status != HVO_OK) break;
     uint8_t* o = out + r * dim;
     switch (binding) {
-      case HVO_BIND_ID_LEVEL: /* reference.cpp:289-298 */
+      case HVO_BIND_ID_LEVEL: /* reference.cpp:217-226 */
         for (size_t j = 0; j < dim; ++j) counts[j] = 0;
         for (size_t f = 0; f < features; ++f) {
           for (size_t j = 0; j < dim; ++j) counts[j] += id_dense[f * dim + j] ^ value_dense[b[f] * dim + j];
         }
         hvo_majority_binarize(counts, dim, features, tiebreak, o);
         break;
-      case HVO_BIND_PERMUTATION: /* reference.cpp:299-309 */
+      case HVO_BIND_PERMUTATION: /* reference.cpp:227-237 */
         for (size_t j = 0; j < dim; ++j) counts[j] = 0;
         for (size_t f = 0; f < features; ++f) {
           for (size_t j = 0; j < dim; ++j) counts[j] += value_dense[b[f] * dim + (j + dim - (f % dim)) % dim];
         }
         hvo_majority_binarize(counts, dim, features, tiebreak, o);
         break;
-      case HVO_BIND_APPENDING: { /* reference.cpp:310-321 */
+      case HVO_BIND_APPENDING: { /* reference.cpp:238-249 */
         const size_t seg = dim / features;
         if (seg == 0) { status = HVO_INVALID_ARGUMENT; break; }
         memset(o, 0, dim);
@@ -387,10 +387,10 @@ int hvo_encode_batch(const uint32_t* bin_rows, size_t rows, size_t features,
 }
 
 /* ======================================================================= */
-/* Model (reference.cpp:93-145, 341-460)                                   */
+/* Model (reference.cpp:21-73, 269-388)                                   */
 /* ======================================================================= */
 
-/* reference.cpp:341-354 */
+/* reference.cpp:269-282 */
 void hvo_refresh_binarization(hvo_model* m, size_t c) {
   const size_t d = m->dim;
   const double total = m->class_weight[c];
@@ -404,7 +404,7 @@ void hvo_refresh_binarization(hvo_model* m, size_t c) {
   }
 }
 
-/* reference.cpp:93-127 */
+/* reference.cpp:21-55 */
 static int class_scores(const hvo_model* m, const uint8_t* cv, const double* acc,
                         const uint8_t* row, double* scores) {
   const size_t cc = m->class_count, d = m->dim;
@@ -431,7 +431,7 @@ static int class_scores(const hvo_model* m, const uint8_t* cv, const double* acc
   return HVO_OK;
 }
 
-/* reference.cpp:129-137: strict comparison, lowest index wins ties */
+/* reference.cpp:57-65: strict comparison, lowest index wins ties */
 static size_t pick_label(int metric, const double* s, size_t n) {
   size_t best = 0;
   for (size_t c = 1; c < n; ++c) {
@@ -441,14 +441,14 @@ static size_t pick_label(int metric, const double* s, size_t n) {
   return best;
 }
 
-/* reference.cpp:141-145 */
+/* reference.cpp:69-73 */
 static double score_to_delta(int metric, double score) {
   if (metric == HVO_METRIC_HAMMING) return score;
   if (isinf(score)) return 1.0;
   return (1.0 - score) / 2.0;
 }
 
-/* reference.cpp:364-389 */
+/* reference.cpp:292-317 */
 int hvo_train_classical(hvo_model* m, const uint8_t* encoded, size_t rows, const int32_t* labels) {
   const size_t cc = m->class_count, d = m->dim;
   for (size_t i = 0; i < cc * d; ++i) m->accumulators[i] = 0.0;
@@ -464,7 +464,7 @@ int hvo_train_classical(hvo_model* m, const uint8_t* encoded, size_t rows, const
   return HVO_OK;
 }
 
-/* reference.cpp:391-423 */
+/* reference.cpp:319-351 */
 int hvo_online_update(hvo_model* m, const uint8_t* batch, size_t rows, const int32_t* labels,
                       const uint8_t* snap_cv, const double* snap_acc) {
   const size_t cc = m->class_count, d = m->dim;
@@ -498,7 +498,7 @@ int hvo_online_update(hvo_model* m, const uint8_t* batch, size_t rows, const int
   return status;
 }
 
-/* reference.cpp:425-448 (bootstrap on the first batch, then every batch
+/* reference.cpp:353-376 (bootstrap on the first batch, then every batch
  * including the first gets an online pass against its start snapshot) */
 int hvo_train_online(hvo_model* m, const uint8_t* encoded, size_t rows, const int32_t* labels,
                      size_t batch_size) {
@@ -520,7 +520,7 @@ int hvo_train_online(hvo_model* m, const uint8_t* encoded, size_t rows, const in
   return status;
 }
 
-/* reference.cpp:450-460 */
+/* reference.cpp:378-388 */
 int hvo_predict(const hvo_model* m, const uint8_t* encoded, size_t rows, int32_t* labels,
                 double* distances) {
   const size_t cc = m->class_count, d = m->dim;

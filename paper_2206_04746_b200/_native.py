@@ -110,6 +110,8 @@ SIGNATURES = {
     "hv_train_online": (ST, [vp, vp, sz, sz, vp, sz, sz, C.POINTER(Model)]),
     "hv_predict": (ST, [vp, C.POINTER(Model), vp, sz, sz, vp, vp]),
     "hv_hamming_distance_words": (dbl, [vp, vp, sz]),
+    "hv_hamming_distance": (ST, [vp, vp, vp, sz, C.POINTER(dbl)]),
+    "hv_cosine_similarity": (ST, [vp, vp, sz, vp, sz, C.POINTER(dbl)]),
     "hv_host_narrow_bins": (ST, [vp, sz, sz, sz, vp, sz, C.POINTER(u64)]),
     "hv_dev_check": (ST, [vp]),
     "hv_dev_narrow_bins": (ST, [vp, vp, sz, sz, sz, vp, sz]),

@@ -1067,6 +1067,51 @@ hv_status hv_make_empty_model(hv_model* m) {
   });
 }
 
+// model.cpp:169-181 hamming_distance(_words): popc(a ^ b) / dim in double, the
+// same one-row Hamming scan as predict (class = b, query = a).
+hv_status hv_hamming_distance(hv_context* ctx, const uint32_t* a, const uint32_t* b, size_t dim, double* out) {
+  return guarded([&] {
+    require(ctx);
+    if (dim == 0) invalid("hamming_distance: dim must be >= 1");
+    const size_t W = words_per_row(dim);
+    cudaStream_t st = ctx->stream;
+    DevBuf<uint32_t> da(W, st), db(W, st);
+    DevBuf<double> dd(1, st);
+    da.upload(a);
+    db.upload(b);
+    predict_hamming_device(ctx, st, db.ptr, 1, dim, da.ptr, 1, nullptr, dd.ptr, nullptr);
+    dd.download(out);
+    sync(ctx);
+  });
+}
+
+// model.cpp:183-196 cosine_similarity: dot(acc, row) / (|acc| sqrt(popc(row))),
+// sequential fp64 like the reference; a zero accumulator or an empty row is
+// a domain error.
+hv_status hv_cosine_similarity(hv_context* ctx, const double* acc, size_t acc_len, const uint32_t* row, size_t dim,
+                               double* out) {
+  return guarded([&] {
+    require(ctx);
+    if (acc_len != dim) invalid("cosine_similarity: accumulator length != dim");
+    if (dim == 0) invalid("cosine_similarity: dim must be >= 1");
+    const size_t W = words_per_row(dim);
+    cudaStream_t st = ctx->stream;
+    DevBuf<double> dacc(dim, st), dd(1, st);
+    DevBuf<uint32_t> dr(W, st);
+    dacc.upload(acc);
+    dr.upload(row);
+    cosine_scores_device(ctx, st, dacc.ptr, 1, dim, dr.ptr, 1, dd.ptr, 0);
+    dd.download(out);
+    sync(ctx);
+    unsigned long long l[kErrKinds];
+    read_latch(ctx, l);
+    if (l[kErrZeroQuery] != ~0ull || std::isinf(*out)) {
+      reset_latch(ctx);
+      fail(HV_ERR_DOMAIN, "cosine_similarity: zero vector");
+    }
+  });
+}
+
 hv_status hv_refresh_binarization(hv_context* ctx, hv_model* m, size_t class_index) {
   return guarded([&] {
     require(ctx);

@@ -403,9 +403,22 @@ def predict_arrays(model: HDModel, encoded: PackedBitMatrix, distances: bool = T
 
 
 def hamming_distance_words(a, b, dim: int) -> float:
+    """model.cpp:178-181 on the device (one row of the predict scan)."""
     a = np.ascontiguousarray(a, np.uint32)
     b = np.ascontiguousarray(b, np.uint32)
-    return float(N.lib().hv_hamming_distance_words(_p(a), _p(b), dim))
+    out = C.c_double()
+    N.check(N.lib().hv_hamming_distance(_ctx(), _p(a), _p(b), dim, C.byref(out)))
+    return out.value
+
+
+def cosine_similarity(acc, packed_row, dim: int) -> float:
+    """model.cpp:183-196: cosine of an accumulator row against a packed row
+    (sequential fp64 like the reference); DomainError on a zero vector."""
+    acc = np.ascontiguousarray(acc, np.float64)
+    row = np.ascontiguousarray(packed_row, np.uint32)
+    out = C.c_double()
+    N.check(N.lib().hv_cosine_similarity(_ctx(), _p(acc), acc.size, _p(row), dim, C.byref(out)))
+    return out.value
 
 
 def hamming_distance(a: PackedBitMatrix, row_a: int, b: PackedBitMatrix, row_b: int) -> float:

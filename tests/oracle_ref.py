@@ -242,7 +242,7 @@ def discretize_matrix(data, mn, mx, bins):
 
 
 def encode_batch(bins, id_words, value_words, n_bins, dim, binding, tiebreak_words):
-    """Packed codebook in, packed HVs out; computed byte-per-bit (reference.cpp:274-339)."""
+    """Packed codebook in, packed HVs out; computed byte-per-bit (reference.cpp:202-267)."""
     bins = np.ascontiguousarray(bins, np.uint32)
     rows, feats = bins.shape
     idd = unpack_rows(id_words, dim)

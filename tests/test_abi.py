@@ -101,10 +101,14 @@ def test_compute_fails_loudly_without_gpu():
 
 
 def test_hamming_distance_words_host_helper():
-    from paper_2206_04746_b200 import hypervec as hv
+    """The C ABI's host-only helper (the Python/drop-in API uses the device
+    version hv_hamming_distance, tested on the GPU)."""
+    import ctypes as C
+    from paper_2206_04746_b200 import _native as N
     a = O.pack_rows(np.array([[1, 1, 0, 0, 1]], np.uint8))
     b = O.pack_rows(np.array([[1, 0, 0, 1, 1]], np.uint8))
-    assert hv.hamming_distance_words(a[0], b[0], 5) == 2.0 / 5.0
+    got = N.lib().hv_hamming_distance_words(a.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p), 5)
+    assert got == 2.0 / 5.0
 
 
 def test_host_narrowing_matches_numpy_and_finds_first_bad_bin():

@@ -254,3 +254,29 @@ def test_two_class_label_scan_matches_full_scan_with_ties(D):
     p = pops.cpu().numpy()
     assert (p[::3, 0] == p[::3, 1]).all() and (fast[::3] == 0).all()
     assert fast[2].item() == 1
+
+
+def test_single_pair_hamming_and_cosine_on_device():
+    """model.cpp:169-196 single-pair helpers (drop-in overrides): device
+    Hamming distance and sequential-fp64 cosine equal the oracle's, and zero
+    vectors are domain errors like the reference."""
+    rng = np.random.default_rng(5)
+    for D in (1, 31, 333, 10000):
+        a = O.pack_rows(rng.integers(0, 2, (1, D), dtype=np.uint8))[0]
+        b = O.pack_rows(rng.integers(0, 2, (1, D), dtype=np.uint8))[0]
+        want = float(np.unpackbits((a ^ b).view(np.uint8)).sum()) / D
+        assert hv.hamming_distance_words(a, b, D) == want
+        acc = rng.integers(-50, 50, D).astype(np.float64) * 0.37
+        m = O.NaiveModel(1, D, O.generate_random(1, D, 3), O.COSINE)
+        m.acc[:] = acc
+        bits = O.unpack_rows(a.reshape(1, -1), D)[0]
+        if bits.any():
+            got = hv.cosine_similarity(acc, a, D)
+            _, od = m.predict(a.reshape(1, -1))
+            assert got == od[0, 0]
+    with pytest.raises(hv.DomainError):
+        hv.cosine_similarity(np.zeros(64), np.array([3, 0], np.uint32), 64)
+    with pytest.raises(hv.DomainError):
+        hv.cosine_similarity(np.ones(64), np.zeros(2, np.uint32), 64)
+    with pytest.raises(hv.InvalidArgument, match="accumulator length != dim"):
+        hv.cosine_similarity(np.ones(63), np.zeros(2, np.uint32), 64)
