@@ -53,7 +53,10 @@ def parse():
     ap.add_argument("--rows", type=int, default=WORKLOAD["rows"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--online", action="store_true", help="also time the exact online trainer (extra field)")
+    ap.add_argument("--no-online", action="store_true",
+                    help="skip the extra online-training line item (exact trainer; word-sliced at N > 1)")
+    ap.add_argument("--online-batch", type=int, default=1024)
+    ap.add_argument("--dump", default=None, help="directory for the timed step's class vectors and labels (tests)")
     return ap.parse_args()
 
 
@@ -365,14 +368,16 @@ def impl_engine(args):
     if not args.no_e2e:
         e2e = run_e2e(args, rank, world, local, rows, ntrain, ntest, (tr_lo, tr_hi), (te_lo, te_hi), eng, cbk)
 
+    if args.dump:
+        os.makedirs(args.dump, exist_ok=True)
+        np.save(os.path.join(args.dump, f"pred_{rank}.npy"), pred.cpu().numpy())
+        np.save(os.path.join(args.dump, f"pred_lo_{rank}.npy"), np.array([te_lo - ntrain]))
+        if rank == 0:
+            np.save(os.path.join(args.dump, "cv.npy"), cv.cpu().numpy())
+
     online = None
-    if args.online and world == 1:
-        torch.cuda.synchronize()
-        s0 = time.perf_counter()
-        eng.train_online(enc[:n_tr].contiguous(), yt, 1024)
-        torch.cuda.synchronize()
-        online = {"rows": n_tr, "batch_size": 1024, "seconds": round(time.perf_counter() - s0, 4),
-                  "dp_per_s": round(n_tr / (time.perf_counter() - s0), 1)}
+    if not args.no_online:
+        online = run_online(args, rank, world, eng, cbk, ntrain, bins8[:n_tr], yt)
 
     if rank == 0:
         base = None if args.no_cpu else cpu_baseline()
@@ -401,7 +406,7 @@ def impl_engine(args):
             "parity_check": check,
         }
         if online:
-            line["online_extra"] = online
+            line["online"] = online
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -468,6 +473,74 @@ def verify_step(rank, world, eng, cbk, bins8, enc, yt, cv, pred, n_tr, n_te, tr_
         return out
     except Exception as e:  # pragma: no cover - reporting only
         return {"ok": None, "skipped": str(e)}
+
+
+def run_online(args, rank, world, eng, cbk, ntrain, bins_tr, y_tr):
+    """Extra line item: encode + exact online training of the train rows
+    (batch --online-batch, model.cpp:282-301), whole-job datapoints/s.
+    N = 1: the persistent single-GPU trainer. N > 1: word-sliced exact mode
+    (device.DSlicedOnline): every rank encodes its slice of the words of ALL
+    train rows and owns those accumulator columns; the per-batch rows x C
+    popcount all-reduce is fused into the partial kernel over peer memory
+    (device.PeerPopc, NCCL all-reduce if that is unavailable). Accumulators,
+    class vectors and labels are bit-identical to one GPU for any N."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2206_04746_b200 import device as dv
+
+    w = WORKLOAD
+    bsz = args.online_batch
+    W = eng.W
+    stream = torch.cuda.current_stream()
+    if world == 1:
+        bins_all, y_all = bins_tr, y_tr
+    else:  # every rank needs every train row's bins (position-separable encode)
+        bins_all, y_all = eng.synth(0, ntrain, w["label_kind"], w["data_seed"])
+    w0, nw = dv.word_slice(W, rank, world)
+    sl = torch.empty((ntrain, nw), dtype=torch.int32, device=eng.dev)
+    peers = None
+    mode = "single GPU, persistent exact trainer" if world == 1 else "word-sliced exact, popcount all-reduce"
+    if world > 1 and os.environ.get("HVB200_ONLINE_PEERS", "1") == "1":
+        try:
+            peers = dv.PeerPopc(eng, rank, world, bsz)
+            mode = "word-sliced exact, popcount all-reduce fused over peer memory"
+        except Exception as exc:  # pragma: no cover
+            print(f"rank {rank}: PeerPopc unavailable ({exc}); NCCL all-reduce", file=sys.stderr)
+            mode = "word-sliced exact, NCCL popcount all-reduce"
+
+    def once():
+        eng.encode_words(bins_all, w0, nw, out=sl)
+        if world == 1:
+            return eng.train_online(sl, y_all, bsz)
+        return dv.DSlicedOnline(eng, sl, y_all, bsz, w0).run(peers=peers)
+
+    once()  # warm-up (lazy module loading, allocator)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    acc, weight, counts, cvs = once()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=eng.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+        dist.barrier()
+    if args.dump:
+        np.save(os.path.join(args.dump, f"online_cv_{rank}.npy"), cvs.cpu().numpy())
+        np.save(os.path.join(args.dump, f"online_acc_{rank}.npy"), acc.cpu().numpy())
+        np.save(os.path.join(args.dump, f"online_w0_{rank}.npy"), np.array([w0, nw]))
+    if peers is not None:
+        peers.close()
+    return {"metric": "encode + exact online training datapoints/s (train rows)", "value": round(ntrain / (ms / 1e3), 1),
+            "unit": "datapoints/s", "rows": ntrain, "batch_size": bsz, "ms": round(ms, 3), "mode": mode,
+            "batches": (ntrain + bsz - 1) // bsz}
 
 
 def run_e2e(args, rank, world, local, rows, ntrain, ntest, tr, te, eng, cbk):

@@ -413,7 +413,14 @@ class PeerPopc(PeerShared):
 
     def __init__(self, engine: "Engine", rank: int, world: int, batch_size: int, group=None, local_ranks=None):
         self.bsz = batch_size
+        self.epoch = 0
         super().__init__(engine, rank, world, self.payload(engine, batch_size), group, local_ranks)
+
+    def next_epoch(self) -> int:
+        """Epochs must grow across runs: a peer's flag passes wait(e) once it
+        holds any epoch >= e, so restarting at 1 would skip the wait."""
+        self.epoch += 1
+        return self.epoch
 
     @staticmethod
     def payload(engine: "Engine", batch_size: int) -> int:
@@ -507,9 +514,10 @@ class DSlicedOnline:
         partial kernel over peer memory; otherwise, with >1 torch.distributed
         rank, the popcounts are all-reduced (NCCL)."""
         if peers is not None:
-            for b, (start, n) in enumerate(self.batches()):
-                self.peer_partial(peers, start, n, b + 1)
-                self.peer_update(peers, start, n, b + 1)
+            for start, n in self.batches():
+                ep = peers.next_epoch()
+                self.peer_partial(peers, start, n, ep)
+                self.peer_update(peers, start, n, ep)
             return self.acc, self.weight, self.counts, self.cv
         dist = torch.distributed
         multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
