@@ -18,36 +18,132 @@
 namespace hvb {
 
 // --------------------------------------------------------------- pack ----
-// kernels.cpp:44-61. One thread per output word; validates bytes <= 1.
-__global__ void pack_kernel(const uint8_t* __restrict__ dense, uint64_t rows, uint32_t dim, uint32_t W,
-                            uint32_t* __restrict__ out, unsigned long long* err) {
-  const uint64_t total = rows * W;
+// kernels.cpp:44-73. HBM-streaming byte <-> bit conversions in two shapes:
+//
+// * rows of a multiple of 16 bytes (D = 1024, 10000, 20000, 32768 ...): a
+//   thread owns 16 dense bytes = half a packed word. pack: one 128-bit load,
+//   each 4-byte group of 0/1 bytes becomes 4 bits with one multiply (the
+//   top byte of (x & 0x01010101) * 0x01020408 is b0 + 2 b1 + 4 b2 + 8 b3; the
+//   lower partial products stay below 2^24), the 16 bits are stored as one
+//   16-bit half of the output word. unpack: the inverse, a nibble spread to
+//   4 bytes by (n * 0x00204081) & 0x01010101, one 128-bit store.
+// * rows of a multiple of 4 bytes: 8 lanes per word, one 4-byte group each
+//   (the same multiply), OR-reduced with 3 shuffles;
+// * any other D: a warp per output word, lane l owns dense byte 32 w + l of
+//   the row; pack = __ballot_sync of the bytes (32 coalesced byte loads), and
+//   unpack = one bit per lane.
+//
+// Non-binary bytes latch the first (row-major) offending flat index, the
+// reference's error (kernels.cpp:45-51).
+__device__ __forceinline__ uint32_t nibble_of(uint32_t x) { return ((x & 0x01010101u) * 0x01020408u) >> 24; }
+__device__ __forceinline__ uint32_t spread_nibble(uint32_t n) { return (n * 0x00204081u) & 0x01010101u; }
+
+__global__ void pack16_kernel(const uint4* __restrict__ dense, uint64_t rows, uint32_t dim, uint32_t W,
+                              uint16_t* __restrict__ out, unsigned long long* err) {
+  const uint32_t per_row = dim / 16;  // 16-byte chunks per row
+  const uint64_t total = rows * per_row;
+  const bool odd_half = (dim % 32) != 0;  // the last word of a row has a zero high half
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t r = i / W;
-    const uint32_t w = static_cast<uint32_t>(i % W);
-    const uint8_t* src = dense + r * dim + w * 32u;
-    const uint32_t n = min(32u, dim - w * 32u);
-    uint32_t word = 0;
-    for (uint32_t t = 0; t < n; ++t) {
-      const uint32_t b = src[t];
-      if (b > 1u) latch(err, kErrByte, r * dim + w * 32u + t);
-      word |= (b & 1u) << t;
+    const uint4 v = __ldcs(dense + i);
+    const uint32_t bad = (v.x | v.y | v.z | v.w) & 0xFEFEFEFEu;
+    if (bad) {  // rare: find the first non-binary byte of the chunk
+      const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t bk = q[k] & 0xFEFEFEFEu;
+        if (bk) {
+          latch(err, kErrByte, i * 16 + 4 * k + (__ffs(bk) - 1) / 8);
+          break;
+        }
+      }
     }
-    out[i] = word;
+    const uint32_t bits = nibble_of(v.x) | (nibble_of(v.y) << 4) | (nibble_of(v.z) << 8) | (nibble_of(v.w) << 12);
+    const uint64_t r = i / per_row;
+    const uint32_t c = static_cast<uint32_t>(i % per_row);  // half-word index within the row
+    uint16_t* o = out + (r * W) * 2 + c;
+    o[0] = static_cast<uint16_t>(bits);
+    if (odd_half && c == per_row - 1) o[1] = 0;  // padding bits of the row's last word stay zero
   }
 }
 
-// kernels.cpp:63-73. One thread per input word, 32 byte stores.
-__global__ void unpack_kernel(const uint32_t* __restrict__ words, uint64_t rows, uint32_t dim, uint32_t W,
-                              uint8_t* __restrict__ dense) {
-  const uint64_t total = rows * W;
+__global__ void unpack16_kernel(const uint16_t* __restrict__ words, uint64_t rows, uint32_t dim, uint32_t W,
+                                uint4* __restrict__ dense) {
+  const uint32_t per_row = dim / 16;
+  const uint64_t total = rows * per_row;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = i / per_row;
+    const uint32_t c = static_cast<uint32_t>(i % per_row);
+    const uint32_t h = __ldg(words + (r * W) * 2 + c);
+    __stcs(dense + i, make_uint4(spread_nibble(h & 15u), spread_nibble((h >> 4) & 15u), spread_nibble((h >> 8) & 15u),
+                                 spread_nibble(h >> 12)));
+  }
+}
+
+// Rows of a multiple of 4 bytes (D = 1000, 100 ...): 8 lanes per output
+// word, each with one 4-byte group (4 bits), OR-reduced across the 8 lanes.
+__global__ void pack4_kernel(const uint32_t* __restrict__ dense, uint64_t rows, uint32_t dim, uint32_t W,
+                             uint32_t* __restrict__ out, unsigned long long* err) {
+  const uint32_t k = threadIdx.x & 7u;  // 4-byte group within the word
+  const uint32_t groups = dim / 4;
+  const uint64_t total = rows * W;
+  const uint64_t ngroups = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 3;
+  for (uint64_t g = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 3; g < total; g += ngroups) {
+    const uint64_t r = g / W;
+    const uint32_t w = static_cast<uint32_t>(g % W);
+    const uint32_t q = 8u * w + k;
+    const uint32_t x = q < groups ? __ldcs(dense + r * groups + q) : 0u;
+    const uint32_t badb = x & 0xFEFEFEFEu;
+    if (badb) latch(err, kErrByte, r * dim + 4ull * q + (__ffs(badb) - 1) / 8);
+    uint32_t v = nibble_of(x) << (4u * k);
+    v |= __shfl_xor_sync(0xFFFFFFFFu, v, 1);
+    v |= __shfl_xor_sync(0xFFFFFFFFu, v, 2);
+    v |= __shfl_xor_sync(0xFFFFFFFFu, v, 4);
+    if (k == 0) out[g] = v;
+  }
+}
+
+__global__ void unpack4_kernel(const uint32_t* __restrict__ words, uint64_t rows, uint32_t dim, uint32_t W,
+                               uint32_t* __restrict__ dense) {
+  const uint32_t k = threadIdx.x & 7u;
+  const uint32_t groups = dim / 4;
+  const uint64_t total = rows * W;
+  const uint64_t ngroups = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 3;
+  for (uint64_t g = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 3; g < total; g += ngroups) {
+    const uint64_t r = g / W;
+    const uint32_t w = static_cast<uint32_t>(g % W);
+    const uint32_t q = 8u * w + k;
+    const uint32_t v = __ldg(words + g);
+    if (q < groups) __stcs(dense + r * groups + q, spread_nibble((v >> (4u * k)) & 15u));
+  }
+}
+
+__global__ void pack_ballot_kernel(const uint8_t* __restrict__ dense, uint64_t rows, uint32_t dim, uint32_t W,
+                                   uint32_t* __restrict__ out, unsigned long long* err) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t total = rows * W;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < total; i += nwarps) {
     const uint64_t r = i / W;
     const uint32_t w = static_cast<uint32_t>(i % W);
-    const uint32_t v = words[i];
-    uint8_t* dst = dense + r * dim + w * 32u;
-    const uint32_t n = min(32u, dim - w * 32u);
-    for (uint32_t t = 0; t < n; ++t) dst[t] = static_cast<uint8_t>((v >> t) & 1u);
+    const uint32_t col = w * 32u + lane;
+    const uint32_t b = col < dim ? dense[r * dim + col] : 0u;
+    const uint32_t bad = __ballot_sync(0xFFFFFFFFu, b > 1u);
+    if (bad && lane == 0) latch(err, kErrByte, r * dim + w * 32u + (__ffs(bad) - 1));
+    const uint32_t word = __ballot_sync(0xFFFFFFFFu, b & 1u);
+    if (lane == 0) out[i] = word;
+  }
+}
+
+__global__ void unpack_ballot_kernel(const uint32_t* __restrict__ words, uint64_t rows, uint32_t dim, uint32_t W,
+                                     uint8_t* __restrict__ dense) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t total = rows * W;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < total; i += nwarps) {
+    const uint64_t r = i / W;
+    const uint32_t w = static_cast<uint32_t>(i % W);
+    const uint32_t v = __ldg(words + i);
+    const uint32_t col = w * 32u + lane;
+    if (col < dim) dense[r * dim + col] = static_cast<uint8_t>((v >> lane) & 1u);
   }
 }
 
@@ -457,6 +553,45 @@ unsigned stream_grid(hv_context* ctx, uint64_t items, unsigned block) {
   return static_cast<unsigned>(want == 0 ? 1 : (want < cap ? want : cap));
 }
 
+void pack_device(hv_context* ctx, cudaStream_t st, const uint8_t* dense, size_t rows, size_t dim, uint32_t* out) {
+  const size_t W = words_per_row(dim);
+  if (rows * W == 0) return;
+  if (dim % 16 == 0 && (reinterpret_cast<uintptr_t>(dense) & 15u) == 0) {
+    pack16_kernel<<<stream_grid(ctx, rows * (dim / 16), 256), 256, 0, st>>>(
+        reinterpret_cast<const uint4*>(dense), rows, static_cast<uint32_t>(dim), static_cast<uint32_t>(W),
+        reinterpret_cast<uint16_t*>(out), ctx->d_err);
+    launched("pack16_kernel");
+  } else if (dim % 4 == 0 && (reinterpret_cast<uintptr_t>(dense) & 3u) == 0) {
+    pack4_kernel<<<stream_grid(ctx, rows * W * 8, 256), 256, 0, st>>>(
+        reinterpret_cast<const uint32_t*>(dense), rows, static_cast<uint32_t>(dim), static_cast<uint32_t>(W), out,
+        ctx->d_err);
+    launched("pack4_kernel");
+  } else {
+    pack_ballot_kernel<<<stream_grid(ctx, rows * W * 32, 256), 256, 0, st>>>(dense, rows, static_cast<uint32_t>(dim),
+                                                                           static_cast<uint32_t>(W), out, ctx->d_err);
+    launched("pack_ballot_kernel");
+  }
+}
+
+void unpack_device(hv_context* ctx, cudaStream_t st, const uint32_t* words, size_t rows, size_t dim, uint8_t* dense) {
+  const size_t W = words_per_row(dim);
+  if (rows * W == 0) return;
+  if (dim % 16 == 0 && (reinterpret_cast<uintptr_t>(dense) & 15u) == 0) {
+    unpack16_kernel<<<stream_grid(ctx, rows * (dim / 16), 256), 256, 0, st>>>(
+        reinterpret_cast<const uint16_t*>(words), rows, static_cast<uint32_t>(dim), static_cast<uint32_t>(W),
+        reinterpret_cast<uint4*>(dense));
+    launched("unpack16_kernel");
+  } else if (dim % 4 == 0 && (reinterpret_cast<uintptr_t>(dense) & 3u) == 0) {
+    unpack4_kernel<<<stream_grid(ctx, rows * W * 8, 256), 256, 0, st>>>(
+        words, rows, static_cast<uint32_t>(dim), static_cast<uint32_t>(W), reinterpret_cast<uint32_t*>(dense));
+    launched("unpack4_kernel");
+  } else {
+    unpack_ballot_kernel<<<stream_grid(ctx, rows * W * 32, 256), 256, 0, st>>>(
+        words, rows, static_cast<uint32_t>(dim), static_cast<uint32_t>(W), dense);
+    launched("unpack_ballot_kernel");
+  }
+}
+
 void check_latch(hv_context* ctx, const uint8_t* dense) {
   unsigned long long l[kErrKinds];
   read_latch(ctx, l);
@@ -479,8 +614,7 @@ hv_status hv_pack(hv_context* ctx, const uint8_t* dense, size_t rows, size_t dim
     DevBuf<uint8_t> d_in(rows * dim, ctx->stream);
     DevBuf<uint32_t> d_out(rows * W, ctx->stream);
     d_in.upload(dense);
-    pack_kernel<<<stream_grid(ctx, rows * W, 256), 256, 0, ctx->stream>>>(d_in.ptr, rows, dim, W, d_out.ptr, ctx->d_err);
-    launched("pack_kernel");
+    pack_device(ctx, ctx->stream, d_in.ptr, rows, dim, d_out.ptr);
     d_out.download(out);
     check_latch(ctx, dense);
   });
@@ -494,8 +628,7 @@ hv_status hv_unpack(hv_context* ctx, const uint32_t* words, size_t rows, size_t 
     DevBuf<uint32_t> d_in(rows * W, ctx->stream);
     DevBuf<uint8_t> d_out(rows * dim, ctx->stream);
     d_in.upload(words);
-    unpack_kernel<<<stream_grid(ctx, rows * W, 256), 256, 0, ctx->stream>>>(d_in.ptr, rows, dim, W, d_out.ptr);
-    launched("unpack_kernel");
+    unpack_device(ctx, ctx->stream, d_in.ptr, rows, dim, d_out.ptr);
     d_out.download(out);
     sync(ctx);
   });

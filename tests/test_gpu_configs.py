@@ -280,3 +280,25 @@ def test_single_pair_hamming_and_cosine_on_device():
         hv.cosine_similarity(np.ones(64), np.zeros(2, np.uint32), 64)
     with pytest.raises(hv.InvalidArgument, match="accumulator length != dim"):
         hv.cosine_similarity(np.ones(63), np.zeros(2, np.uint32), 64)
+
+
+@pytest.mark.parametrize("D", [16, 48, 1024, 10000, 1000, 33, 1, 100, 36, 7])
+def test_pack_unpack_vectorised_and_ballot_paths(D):
+    """pack / unpack (kernels.cpp:44-73) on both device paths — 128-bit
+    chunks when rows are a multiple of 16 bytes, warp ballots otherwise — are
+    exact inverses matching the oracle, keep the padding bits zero, and report
+    the first non-binary byte in row-major order like the reference."""
+    rng = np.random.default_rng(D)
+    rows = 3001
+    dense = rng.integers(0, 2, (rows, D), dtype=np.uint8)
+    p = hv.pack(hv.DenseBitMatrix(rows, D, dense))
+    np.testing.assert_array_equal(p.words, O.pack_rows(dense))
+    assert p.padding_clean()
+    np.testing.assert_array_equal(hv.unpack(p).bits, dense)
+    bad = dense.copy()
+    flat = bad.reshape(-1)
+    hits = sorted(rng.choice(flat.size, 3, replace=False))
+    for k, h in enumerate(hits):
+        flat[h] = 2 + k
+    with pytest.raises(hv.InvalidArgument, match=rf"pack: non-binary entry {2} at flat index {hits[0]}"):
+        hv.pack(hv.DenseBitMatrix(rows, D, bad))
