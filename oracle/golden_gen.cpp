@@ -181,6 +181,10 @@ void gen_encode() {
       {"perm_10240", GenerationStrategy::kRandom, BindingStrategy::kPermutation, 100, 16, 10240, 3, 109},
       {"app_37", GenerationStrategy::kRandom, BindingStrategy::kAppending, 4, 3, 37, 6, 13},
       {"app_10000", GenerationStrategy::kRandom, BindingStrategy::kAppending, 617, 16, 10000, 3, 110},
+      // more than 16 bins: the table encoder's 32-bin tables
+      {"b32_chbmit", GenerationStrategy::kRandom, BindingStrategy::kIdLevel, 342, 32, 10000, 6, 111},
+      {"b24_isolet", GenerationStrategy::kRandom, BindingStrategy::kIdLevel, 617, 24, 10000, 4, 112},
+      {"perm_b32", GenerationStrategy::kRandom, BindingStrategy::kPermutation, 100, 32, 2048, 5, 113},
   };
   for (const Spec& s : specs) {
     Case c(std::string("encode_") + s.name);

@@ -36,7 +36,8 @@
 
 namespace hvb {
 
-constexpr int kTBins = 16;     // table rows per feature (B <= 16)
+// table rows per feature: TB = 16 (B <= 16, the reference default) or 32
+// (B <= 32: twice the table per word pair, so fewer pairs per lane fit)
 constexpr int kChunk = 64;     // features per staged chunk
 
 // Per feature and lane: 1 PRMT + NPR LDS.64 + 2*NW LOP3 (the previous version,
@@ -102,10 +103,12 @@ __device__ __forceinline__ uint32_t majority_biased(const uint32_t (&pl)[6 + NH]
   return pl[K - 1] & (odd ? 0xFFFFFFFFu : (any | tie));
 }
 
-template <int NPR, int G, int NH, int MINB, bool PERM>
+template <int NPR, int G, int NH, int MINB, bool PERM, int TB>
 __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
   constexpr int NW = 2 * NPR;
+  constexpr int kTBins = TB;
   constexpr uint32_t kFeatBytes = NPR * kTBins * 8;  // one feature's entries (all pairs)
+  constexpr uint32_t kBinMask = TB == 16 ? 0x0F0F0F0Fu : 0x1F1F1F1Fu;  // b * 8 <= 248 still fits a byte
   extern __shared__ __align__(256) uint8_t sm6[];
   __shared__ unsigned int s_item;
   const int warp = threadIdx.x >> 5;
@@ -188,7 +191,7 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
       // whose bytes the caller need not zero: masked to a nibble they index the
       // all-zero table rows of features >= F instead of running past the table.
       auto stage = [&](auto masked) {
-        constexpr uint32_t m = decltype(masked)::value ? 0x0F0F0F0Fu : 0xFFFFFFFFu;
+        constexpr uint32_t m = decltype(masked)::value ? kBinMask : 0xFFFFFFFFu;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const uint32_t col = (8 * i + lr) ^ (lq << 3);
@@ -298,11 +301,11 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
 
 namespace {
 
-template <int NPR, int G, int NH, int MINB>
+template <int NPR, int G, int NH, int MINB, int TB>
 void launch_tt6_inst(hv_context* ctx, cudaStream_t st, TT6Params p, size_t smem) {
   // separate instantiations: the permutation table build must not perturb the
   // ID-level kernel's code (it cost 1.5 % there as a runtime branch)
-  auto kern = p.perm ? encode_tt6_kernel<NPR, G, NH, MINB, true> : encode_tt6_kernel<NPR, G, NH, MINB, false>;
+  auto kern = p.perm ? encode_tt6_kernel<NPR, G, NH, MINB, true, TB> : encode_tt6_kernel<NPR, G, NH, MINB, false, TB>;
   ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
      "cudaFuncSetAttribute");
   int per_sm = 0;
@@ -328,12 +331,15 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
   while ((64ull << nh) <= F) ++nh;
   nh = nh <= 3 ? 3 : nh <= 4 ? 4 : nh <= 6 ? 6 : -1;
   if (nh < 0) return false;
-  const size_t pair_table = static_cast<size_t>(Fpad) * kTBins * 8;
+  const int tb = B <= 16 ? 16 : 32;
+  const size_t pair_table = static_cast<size_t>(Fpad) * tb * 8;
   const size_t wstage = 16 * 32 * 4;
   // Shapes (word pairs per lane, warps per CTA, CTAs per SM), preferred first:
   // the most pairs whose tables fit (measured at CHB-MIT: 4 or 3 pairs with 8
   // warps beat 2 pairs with 2 CTAs/SM by 7 %, 1 pair by 22 %).
   struct Shape { int npr, g, minb; };
+  // (32 bins: pair tables are twice as large, so the same list picks fewer
+  // pairs; only the {2,8,1} and {1,8,2} shapes are instantiated for it)
   const Shape shapes[] = {{4, 8, 1}, {3, 8, 1}, {2, 8, 1}, {1, 8, 2}};
   constexpr int kShapes = sizeof(shapes) / sizeof(shapes[0]);
   const size_t two = 113 * 1024, one = std::min<size_t>(ctx->smem_optin, 225 * 1024);
@@ -344,7 +350,8 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
   for (int i = 0; i < kShapes; ++i) {
     const Shape& s = shapes[i];
     const size_t need = s.npr * pair_table + s.g * wstage;
-    const bool fits = need <= (s.minb == 2 ? two : one);
+    const bool inst = tb == 16 || s.npr <= 2;
+    const bool fits = inst && need <= (s.minb == 2 ? two : one);
     if (forced ? (s.npr == enp && s.g == eg && s.minb == emb && fits) : (fits && pick < 0)) pick = i;
   }
   if (pick < 0) return false;
@@ -365,16 +372,18 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
   }
   TT6Params p{bins8, ldb, rows, F, Fpad, D, W, B, id, val, tie, out, w0, wcount, ldo, slices, block_rows,
               (rows + block_rows - 1) / block_rows, counter, perm ? 1u : 0u};
-#define HV_TT6(NPR, G, MB, N)                                            \
-  if (s.npr == NPR && s.g == G && s.minb == MB && nh == N) {             \
-    launch_tt6_inst<NPR, G, N, MB>(ctx, st, p, smem);                    \
+#define HV_TT6(NPR, G, MB, N, TB)                                        \
+  if (s.npr == NPR && s.g == G && s.minb == MB && nh == N && tb == TB) { \
+    launch_tt6_inst<NPR, G, N, MB, TB>(ctx, st, p, smem);                \
     return true;                                                         \
   }
-#define HV_TT6_NH(NPR, G, MB) HV_TT6(NPR, G, MB, 3) HV_TT6(NPR, G, MB, 4) HV_TT6(NPR, G, MB, 6)
-  HV_TT6_NH(4, 8, 1)
-  HV_TT6_NH(3, 8, 1)
-  HV_TT6_NH(2, 8, 1)
-  HV_TT6_NH(1, 8, 2)
+#define HV_TT6_NH(NPR, G, MB, TB) HV_TT6(NPR, G, MB, 3, TB) HV_TT6(NPR, G, MB, 4, TB) HV_TT6(NPR, G, MB, 6, TB)
+  HV_TT6_NH(4, 8, 1, 16)
+  HV_TT6_NH(3, 8, 1, 16)
+  HV_TT6_NH(2, 8, 1, 16)
+  HV_TT6_NH(1, 8, 2, 16)
+  HV_TT6_NH(2, 8, 1, 32)
+  HV_TT6_NH(1, 8, 2, 32)
 #undef HV_TT6_NH
 #undef HV_TT6
   return false;
@@ -385,7 +394,7 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
 bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
                const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
                uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo, bool perm) {
-  if (B > static_cast<uint32_t>(kTBins) || F == 0 || rows == 0 || wcount == 0) return false;
+  if (B > 32u || F == 0 || rows == 0 || wcount == 0) return false;
   if (ldb % kChunk != 0 || (reinterpret_cast<uintptr_t>(bins8) & 15u)) return false;
   // one work counter per launch from the context's ring (concurrent launches on
   // the context's two streams must not share one)

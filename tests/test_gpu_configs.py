@@ -302,3 +302,26 @@ def test_pack_unpack_vectorised_and_ballot_paths(D):
         flat[h] = 2 + k
     with pytest.raises(hv.InvalidArgument, match=rf"pack: non-binary entry {2} at flat index {hits[0]}"):
         hv.pack(hv.DenseBitMatrix(rows, D, bad))
+
+
+@pytest.mark.parametrize("B,binding", [(32, 0), (17, 0), (32, 1), (24, 0)])
+def test_table_encoder_up_to_32_bins_vs_generic_and_oracle(B, binding, monkeypatch):
+    """17..32 bins take the table encoder's 32-bin tables (encoding.cpp:228-255
+    accepts any bin count): equal to the generic kernel on 50,000 CHB-MIT-shaped
+    rows with random bins, and to the oracle on a sample."""
+    F, D, rows = 342, 10000, 50_000
+    cbk = dv.DeviceCodebook.make(F, B, D, seed=77 + B, binding=binding)
+    eng = dv.Engine(cbk, 2)
+    bins = torch.randint(0, B, (rows, dv.bins_pitch(F)), dtype=torch.uint8, device="cuda")
+    before = launch_count()
+    fast = eng.encode(bins)
+    assert launch_count() > before
+    monkeypatch.setenv("HVB200_ENCODE_GENERIC", "1")
+    generic = eng.encode(bins)
+    torch.cuda.synchronize()
+    assert torch.equal(fast, generic)
+    idx = np.array([0, 1, rows // 2, rows - 1])
+    b = bins[torch.as_tensor(idx, device="cuda")][:, :F].cpu().numpy().astype(np.uint32)
+    want = O.encode_batch(b, _u32(cbk.id_vectors), _u32(cbk.value_vectors), B, D,
+                          O.BIND_ID_LEVEL if binding == 0 else O.BIND_PERMUTATION, _u32(cbk.encode_tiebreak))
+    np.testing.assert_array_equal(_u32(fast[torch.as_tensor(idx, device="cuda")]), want)
