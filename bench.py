@@ -354,12 +354,16 @@ def impl_engine(args):
     bound_words = local_rows * F * W
     int_achieved = bound_words / (enc_avg_ms / 1e3) / 1e9
     int_peak = sms * 64 * sm_mhz * 1e6 / 2 / 1e9
-    traffic = None
+    # DRAM bytes per launch: dram__bytes_read + dram__bytes_write per row from
+    # one `ncu --set full` capture of this kernel (profiles/encode_dram_bytes.json,
+    # 1 M rows) scaled to this launch's rows — not measured inside this run
+    traffic, traffic_src = None, None
     prof = ROOT / "profiles" / "encode_dram_bytes.json"
     if prof.exists():
         try:
             p = json.loads(prof.read_text())
-            traffic = p.get("dram_bytes_per_row", 0) * local_rows or None
+            traffic = round(p.get("dram_bytes_per_row", 0) * local_rows) or None
+            traffic_src = f"{p.get('source')}: {p.get('dram_bytes_per_row')} B/row x {local_rows} rows"
         except Exception:
             traffic = None
 
@@ -393,11 +397,18 @@ def impl_engine(args):
                            (n_tr + n_te) * dv.bins_pitch(F) / 1e9, (n_tr + n_te) * 4 * W / 1e9)},
             "roofline": {"bound": "hbm", "kernel": "encode_tt6_kernel", "achieved": round(achieved_gbs, 2),
                          "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved_gbs / hbm_peak, 5),
-                         "traffic": traffic, "peak_source": peak_src,
+                         "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                          "algorithmic_bytes_per_row": F + 4 * W, "avg_launch_ms": round(enc_avg_ms, 4),
-                         "int_pipe": {"achieved_gwords_s": round(int_achieved, 1), "peak_gwords_s": round(int_peak, 1),
-                                      "frac": round(int_achieved / int_peak, 4),
-                                      "model": "bound words (F*W per row) vs SMs*32*f_sm: 2 LOP3/word on the 64-lane ALU pipe = 4 B/word of the 128 B/clk shared-memory table reads"}},
+                         "note": "the HBM fraction is the contract's; the encoder is not HBM-bound — "
+                                 "binding_ceiling is the ceiling that binds it",
+                         "binding_ceiling": {
+                             "resource": "ALU pipe (LOP3) and shared-memory table reads, saturated together",
+                             "achieved_gwords_s": round(int_achieved, 1), "peak_gwords_s": round(int_peak, 1),
+                             "frac": round(int_achieved / int_peak, 4), "unit": "G bound words/s",
+                             "model": "bound words (F*W per row); >= 2 LOP3 per word on the 64 LOP3/clk/SM ALU pipe "
+                                      "and 4 B per word of 128 B/clk/SM shared-memory reads -> SMs * 32 words * f_sm",
+                             "peak_source": "profiles/probe_alu_r2.txt (measured on this GPU: LOP3 64.00 /clk/SM, "
+                                            "LDS.64 conflict-free 128 B/clk/SM) at the run's median SM clock"}},
             "cpu_baseline": base,
             "e2e": e2e,
             "clocks": clocks,
