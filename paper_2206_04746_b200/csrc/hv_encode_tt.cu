@@ -247,10 +247,18 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
               carry.v[j] |= c64;  // at most one weight-64 carry per bit: the chunk adds < 64
             }
           };
-          if (nf >= 16) add16(hs_tree<4, NW>(s, ld));
-          if (nf >= 32) add16(hs_tree<4, NW>(s, ld));
-          if (nf >= 48) add16(hs_tree<4, NW>(s, ld));
-          if (nf & 8u) {
+          // two weight-16 carries enter level 4 through one carry-save adder
+          auto add16x2 = [&](const Words<NW>& ca, const Words<NW>& cb) {
+#pragma unroll
+            for (int j = 0; j < NW; ++j) {
+              uint32_t c32;
+              csa(c32, s[4][j], s[4][j], ca.v[j], cb.v[j]);
+              const uint32_t c64 = s[5][j] & c32;
+              s[5][j] ^= c32;
+              carry.v[j] |= c64;
+            }
+          };
+          auto c8to16 = [&]() {  // a block of 8: its weight-8 carry half-adds into level 3
             const Words<NW> c8 = hs_tree<3, NW>(s, ld);
             Words<NW> c16;
 #pragma unroll
@@ -258,7 +266,23 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
               c16.v[j] = s[3][j] & c8.v[j];
               s[3][j] ^= c8.v[j];
             }
-            add16(c16);
+            return c16;
+          };
+          const uint32_t n16 = nf >> 4;
+          const bool has8 = nf & 8u;
+          if (n16 >= 2) {
+            const Words<NW> ca = hs_tree<4, NW>(s, ld);
+            add16x2(ca, hs_tree<4, NW>(s, ld));
+          }
+          if (n16 == 1 || n16 == 3) {
+            const Words<NW> ca = hs_tree<4, NW>(s, ld);
+            if (has8) {
+              add16x2(ca, c8to16());
+            } else {
+              add16(ca);
+            }
+          } else if (has8) {
+            add16(c8to16());
           }
         }
 #pragma unroll
