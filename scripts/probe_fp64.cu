@@ -44,6 +44,32 @@ __global__ void chain_sel(int iters, const uint32_t* __restrict__ words, const d
   if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
 }
 
+// the same step with the add predicated on the bit instead of selecting +0.0
+__global__ void chain_pred(int iters, const uint32_t* __restrict__ words, const double* __restrict__ v, double* out,
+                           long long* cyc) {
+  __shared__ uint32_t sw[1024];
+  __shared__ double sv[1024];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+    sw[i] = words[i];
+    sv[i] = v[i & 7] * (i + 1);
+  }
+  __syncthreads();
+  double a = 0.0;
+  const uint32_t lane = threadIdx.x & 31;
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll 8
+    for (int k = 0; k < 1024; ++k) {
+      const double val = sv[k];
+      const uint32_t wd = sw[k];
+      if ((wd >> lane) & 1u) a = __dadd_rn(a, val);
+    }
+  }
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a;
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+}
+
 int main() {
   double *v, *out;
   uint32_t* w;
@@ -71,6 +97,11 @@ int main() {
     cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
     printf("replay step (LDS word + LDS value + select + DADD), %d warp(s): %.2f cycles per step\n", warps,
            c / (20.0 * 1024));
+  }
+  for (int warps : {1, 2, 8}) {
+    chain_pred<<<1, 32 * warps>>>(20, w, v, out, cyc);
+    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("replay step, predicated DADD, %d warp(s): %.2f cycles per step\n", warps, c / (20.0 * 1024));
   }
   return 0;
 }
