@@ -306,6 +306,7 @@ __device__ __forceinline__ void load_columns(const OnlineParams& p, uint32_t c, 
 // x + y == 0 rounds to +0.0).
 template <int COLS>
 __device__ __forceinline__ void replay_chunk(const uint32_t* words, const double* val, uint32_t m, double (&a)[COLS]) {
+
   const uint32_t lane = threadIdx.x & 31u, ww = threadIdx.x >> 5;
   constexpr int kUnroll = COLS == 1 ? 8 : 2;  // enough independent loads in flight ahead of the chain
 #pragma unroll kUnroll
@@ -454,9 +455,12 @@ __device__ void replay_merged(const OnlineParams& p, const unsigned long long* b
         if (k < RTile<COLS>::kChunk) s.words[buf][k * RTile<COLS>::kWords + ww] = rw[i];
       }
     };
+    const bool pr = p.prof != nullptr && blockIdx.x == 0 && tid == 0;
+    const unsigned long long q0 = pr ? gtimer() : 0ull;
     load_chunk(0);
     store_chunk(0);
     __syncthreads();
+    const unsigned long long q1 = pr ? gtimer() : 0ull;
     uint32_t buf = 0;
     for (uint32_t ch = 0; ch < n; ch += RTile<COLS>::kChunk, buf ^= 1u) {
       const bool more = ch + RTile<COLS>::kChunk < n;
@@ -475,6 +479,7 @@ __device__ void replay_merged(const OnlineParams& p, const unsigned long long* b
       if (more) store_chunk(buf ^ 1u);  // the other buffer was last read before the previous barrier
       __syncthreads();
     }
+    const unsigned long long q2 = pr ? gtimer() : 0ull;
     if (tid == kOReplay) {
       if (sep) {  // the weight task of class c publishes the batch's final weight
         await_class_weight(p, c, epoch);
@@ -484,7 +489,14 @@ __device__ void replay_merged(const OnlineParams& p, const unsigned long long* b
       }
     }
     const int touched = __syncthreads_or(mine);
+    const unsigned long long q3 = pr ? gtimer() : 0ull;
     if (tid < kOReplay) store_columns<COLS>(p, c, wb, a, s.weight, touched != 0);
+    if (pr) {
+      p.prof[3] += q1 - q0;  // first chunk staged
+      p.prof[4] += q2 - q1;  // chunk loop (replay)
+      p.prof[5] += q3 - q2;  // weight wait
+      p.prof[6] += gtimer() - q3;
+    }
     if (!sep && wb == 0 && tid == kOReplay) {
       p.weight[(par ^ 1u) * p.C + c] = wsum;
       p.counts[c] += ntrue;
@@ -934,7 +946,7 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
                  lval.ptr, llen.ptr, nullptr, lane_class ? 1u : 0u, 1u, nullptr, nullptr, nullptr, wtask ? wflag.ptr : nullptr};
   // HVB200_ONLINE_PROFILE=1: print the time per phase (CTA 0's view, barrier waits included)
   const char* pe = getenv("HVB200_ONLINE_PROFILE");
-  DevBuf<unsigned long long> prof(pe && pe[0] == '1' ? 3 : 0, st);
+  DevBuf<unsigned long long> prof(pe && pe[0] == '1' ? 7 : 0, st);
   if (prof.ptr) {
     prof.zero();
     p.prof = prof.ptr;
@@ -1002,13 +1014,14 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   }
   launched("online_persistent_kernel");
   if (prof.ptr) {
-    unsigned long long h[3];
+    unsigned long long h[7];
     ck(cudaMemcpyAsync(h, prof.ptr, sizeof(h), cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaStreamSynchronize(st), "sync");
     const double nb = static_cast<double>((rows + n - 1) / n);
-    fprintf(stderr, "online phases (us/batch, %s, %d cols, ksplit %u): score %.2f lists %.2f replay %.2f\n",
+    fprintf(stderr, "online phases (us/batch, %s, %d cols, ksplit %u): score %.2f lists %.2f replay %.2f"
+            " [CTA 0 item: stage %.2f chunks %.2f weight-wait %.2f store %.2f]\n",
             merged ? "merged" : "lists", cols8 ? 8 : cols4 ? 4 : 1, p.ksplit, h[0] / nb / 1e3, h[1] / nb / 1e3,
-            h[2] / nb / 1e3);
+            h[2] / nb / 1e3, h[3] / nb / 1e3, h[4] / nb / 1e3, h[5] / nb / 1e3, h[6] / nb / 1e3);
   }
   // MERGED leaves the final weights in the parity row after the last batch
   const size_t nb = (rows + n - 1) / n;
