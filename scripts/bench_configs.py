@@ -90,7 +90,10 @@ def one(tag, F, C, D, rows, trainer, batch, label_kind=0, cpu=True, reps=3):
     eng = dv.Engine(cbk, C)
     eng.dc.bind()
     bins8, labels = eng.synth(0, rows, label_kind, 7)
-    enc = torch.empty((rows, W), dtype=torch.int32, device=eng.dev)
+    # classical with < 32 classes keeps the engine's pitched rows (16-byte rows:
+    # TMA-staged counts, uint4 predict); the online trainer reads unpitched rows
+    pitched = trainer == "classical" and C < 32
+    enc = eng.pitched_empty(rows) if pitched else torch.empty((rows, W), dtype=torch.int32, device=eng.dev)
     ms_enc, _ = timed(lambda: eng.encode(bins8, out=enc), reps)
     yt = labels[:ntr]
     if trainer == "classical":
@@ -108,7 +111,7 @@ def one(tag, F, C, D, rows, trainer, batch, label_kind=0, cpu=True, reps=3):
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     line = {
         "config": tag, "features": F, "classes": C, "dim": D, "rows": rows, "train_rows": ntr, "test_rows": nte,
-        "trainer": trainer, "batch_size": batch if trainer == "online" else None,
+        "trainer": trainer, "batch_size": batch if trainer == "online" else None, "pitched_rows": pitched,
         "dp_per_s": round(rows / (total / 1e3), 1),
         "ms": {"encode": round(ms_enc, 3), "train": round(ms_train, 3), "predict": round(ms_pred, 3)},
         "encode": {"dp_per_s": round(rows / (ms_enc / 1e3), 1),
