@@ -231,8 +231,13 @@ uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, si
   // the first chunks of a call ramp up (1/8, 1/4, 1/2 of a slot) so the SMs
   // start encoding after a short narrow + copy instead of a full slot's
   size_t step = k == 0 ? std::max<size_t>(1, chunk / 8) : chunk;
+  const size_t tail_min = std::max<size_t>(1, chunk / 16);
   for (size_t r0 = 0, n = 0; r0 < rows; r0 += n, ++k, step = std::min(chunk, 2 * step)) {
     n = std::min(step, rows - r0);
+    // ... and ramp down over the last two slots (halving pieces), so the
+    // encode left after the final copy is a short one
+    const size_t left = rows - r0;
+    if (left <= 2 * step && left > tail_min) n = std::max(tail_min, (left + 1) / 2);
     const int s = static_cast<int>(k % HostStager::kSlots);
     cudaStream_t st = streams[k & 1];
     ck(cudaEventSynchronize(hs.done[s]), "stage slot wait");  // its previous H2D has finished
