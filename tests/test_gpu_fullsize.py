@@ -126,3 +126,37 @@ def test_large_full_size_encode_train_predict():
     del bins8
     ntr = N * 4 // 5
     _check_classical_and_predict(eng, cbk, enc, labels, ntr, C, _sample(N - ntr, 1000, 4))
+
+
+def test_chbmit_full_size_online_two_exact_paths_agree():
+    """The whole CHB-MIT online run (5.65 M train rows, 5,516 batches of 1,024)
+    through two independent exact implementations — the persistent single-GPU
+    trainer and the word-sliced multi-GPU mode with 2 ranks emulated on this
+    GPU (different kernels: slice init, partial popcounts summed across ranks,
+    slice update) — must give bit-identical fp64 accumulators, weights, counts
+    and class vectors (model.cpp:250-301). The 32-batch prefix is pinned
+    against the oracle in the test above."""
+    N, F, B, D, C = 7_060_000, 342, 16, 10000, 2
+    ntr = N * 4 // 5
+    cbk = dv.DeviceCodebook.make(F, B, D, seed=20)
+    eng = dv.Engine(cbk, C)
+    bins8, labels = eng.synth(0, ntr, 1, 9)
+    enc = eng.encode(bins8)
+    acc, weight, counts, cv = eng.train_online(enc, labels, 1024)
+    del enc
+    W = eng.W
+    ranks = []
+    for r in range(2):
+        w0, nw = dv.word_slice(W, r, 2)
+        ranks.append(dv.DSlicedOnline(eng, eng.encode_words(bins8, w0, nw), labels, 1024, w0))
+    for start, n in ranks[0].batches():
+        tot = ranks[0].partial(start, n).clone()
+        tot += ranks[1].partial(start, n)
+        for rk in ranks:
+            rk.update(start, n, tot)
+    eng.dc.check()
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([rk.acc for rk in ranks], dim=1), acc)
+    assert torch.equal(torch.cat([rk.cv for rk in ranks], dim=1), cv)
+    for rk in ranks:
+        assert torch.equal(rk.weight, weight) and torch.equal(rk.counts, counts)
