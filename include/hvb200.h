@@ -368,6 +368,19 @@ hv_status hv_dev_online_partial_popc(hv_context* ctx, const uint32_t* class_vect
 hv_status hv_dev_online_partial_popc_peers(hv_context* ctx, const uint32_t* class_vectors,
                                            size_t class_count, size_t words, const uint32_t* batch,
                                            size_t rows, uint32_t* const* peer_popc, size_t world);
+/* Every batch of the word-sliced exact online mode, the popcount exchange
+ * fused over peer memory, enqueued in one call: per batch the partial
+ * popcounts are added into every rank's parity slot (peer_popc0/1: device
+ * arrays of `world` slot pointers; own_popc0/1: this rank's), then signal /
+ * wait on the flags (epochs epoch0+1 ..), score, lists and the slice update,
+ * and this rank's slot is reset. State as hv_dev_online_slice_init left it. */
+hv_status hv_dev_online_sliced_run_peers(hv_context* ctx, const uint32_t* enc_slice, size_t rows, size_t words,
+                                         size_t word_begin, size_t dim, const int32_t* labels, size_t class_count,
+                                         size_t batch_size, double gamma, const uint32_t* tiebreak,
+                                         uint32_t* const* peer_popc0, uint32_t* const* peer_popc1, uint32_t* own_popc0,
+                                         uint32_t* own_popc1, uint32_t* const* peer_flags, const uint32_t* own_flags,
+                                         size_t world, size_t rank, uint32_t epoch0, double* acc, double* weight,
+                                         uint64_t* counts, uint32_t* class_vectors);
 hv_status hv_dev_online_slice_update(hv_context* ctx, const uint32_t* popc, size_t class_count,
                                      size_t dim, size_t word_begin, size_t words,
                                      const uint32_t* batch, size_t rows, const int32_t* labels,

@@ -128,6 +128,8 @@ SIGNATURES = {
     "hv_dev_online_partial_popc": (ST, [vp, vp, sz, sz, vp, sz, vp]),
     "hv_dev_online_partial_popc_peers": (ST, [vp, vp, sz, sz, vp, sz, vp, sz]),
     "hv_dev_online_slice_update": (ST, [vp, vp, sz, sz, sz, sz, vp, sz, vp, dbl, vp, vp, vp, vp, vp]),
+    "hv_dev_online_sliced_run_peers": (ST, [vp, vp, sz, sz, sz, sz, vp, sz, sz, dbl, vp, vp, vp, vp, vp, vp, vp, sz,
+                                            sz, u32, vp, vp, vp, vp]),
     "hv_shared_handle_size": (sz, []),
     "hv_shared_alloc": (ST, [vp, sz, C.POINTER(vp), vp]),
     "hv_shared_open": (ST, [vp, vp, C.POINTER(vp)]),

@@ -1442,6 +1442,68 @@ hv_status hv_dev_online_slice_update(hv_context* ctx, const uint32_t* popc, size
   });
 }
 
+// All batches of the word-sliced exact online mode with the popcount exchange
+// fused over peer memory, enqueued from here in one call (per batch: partial
+// popcounts added into every rank's parity slot, signal, wait, score, lists,
+// slice update, slot reset) — no host round trip and no per-batch allocation.
+// Epochs epoch0 + 1 .. epoch0 + nbatches are used; they must exceed every
+// epoch already signalled on these buffers.
+hv_status hv_dev_online_sliced_run_peers(hv_context* ctx, const uint32_t* enc_slice, size_t rows, size_t words,
+                                         size_t word_begin, size_t dim, const int32_t* labels, size_t class_count,
+                                         size_t batch_size, double gamma, const uint32_t* tiebreak,
+                                         uint32_t* const* peer_popc0, uint32_t* const* peer_popc1, uint32_t* own_popc0,
+                                         uint32_t* own_popc1, uint32_t* const* peer_flags, const uint32_t* own_flags,
+                                         size_t world, size_t rank, uint32_t epoch0, double* acc, double* weight,
+                                         uint64_t* counts, uint32_t* class_vectors) {
+  return guarded([&] {
+    require(ctx);
+    cudaStream_t st = ctx->stream;
+    const size_t C = class_count, W = words_per_row(dim);
+    if (C == 0 || dim == 0) invalid("train_online: empty model");
+    if (batch_size == 0) invalid("train_online: batch_size must be >= 1");
+    if (words == 0 || word_begin + words > W) invalid("online slice: word range outside the row");
+    if (world == 0 || world > 64 || rank >= world) invalid("online_sliced_run_peers: bad world/rank");
+    if (rows == 0) return;
+    const size_t Ds = std::min(dim, 32 * (word_begin + words)) - 32 * word_begin;
+    const size_t cap = std::min(batch_size, rows);
+    OnlineScratch s(C, cap, false, st);
+    uint32_t ep = epoch0;
+    for (size_t b0 = 0; b0 < rows; b0 += batch_size) {
+      const size_t n = std::min(batch_size, rows - b0);
+      ++ep;
+      const bool odd = ep & 1u;
+      uint32_t* const* peers = odd ? peer_popc1 : peer_popc0;
+      uint32_t* own = odd ? own_popc1 : own_popc0;
+      const uint32_t* batch = enc_slice + b0 * words;
+      online_partial_popc_kernel<<<sgrid(ctx, n * 32, 256, 8), 256, 0, st>>>(
+          class_vectors, static_cast<uint32_t>(C), static_cast<uint32_t>(words), batch, n, nullptr, peers,
+          static_cast<uint32_t>(world));
+      launched("online_partial_popc_kernel");
+      if (hv_dev_signal_peers(ctx, peer_flags, world, rank, ep) != HV_OK) fail(HV_ERR_CUDA, hv_last_error());
+      if (hv_dev_wait_peers(ctx, own_flags, world, ep) != HV_OK) fail(HV_ERR_CUDA, hv_last_error());
+      online_score_popc_kernel<<<sgrid(ctx, n, 128), 128, 0, st>>>(own, static_cast<uint32_t>(C),
+                                                                  static_cast<uint32_t>(dim), n, labels + b0, gamma,
+                                                                  s.pred.ptr, s.dtrue.ptr, s.pen.ptr, ctx->d_err);
+      launched("online_score_popc_kernel");
+      online_lists_kernel<<<C, 32, 0, st>>>(labels + b0, s.pred.ptr, s.dtrue.ptr, s.pen.ptr, n, C, s.cap, s.idx.ptr,
+                                            s.val.ptr, s.len.ptr, weight, counts, nullptr);
+      launched("online_lists_kernel");
+      dim3 grid((Ds + 255) / 256, C);
+      online_update_kernel<false><<<grid, 256, 0, st>>>(batch, Ds, words, s.cap, s.idx.ptr, s.val.ptr, s.len.ptr,
+                                                        weight, tiebreak + word_begin, acc, class_vectors);
+      launched("online_update_kernel");
+      ck(cudaMemsetAsync(own, 0, n * C * sizeof(uint32_t), st), "reset popcount slot");
+    }
+    unsigned long long l[kErrKinds];
+    sync(ctx);
+    read_latch(ctx, l);
+    if (l[kErrLabel] != ~0ull) {
+      reset_latch(ctx);
+      invalid("online_update: label out of range at batch row " + std::to_string(l[kErrLabel]));
+    }
+  });
+}
+
 hv_status hv_dev_apply_online_delta(hv_context* ctx, size_t class_count, size_t dim, const double* delta_acc,
                                     const double* delta_weight, const uint64_t* delta_counts, const uint32_t* touched,
                                     const uint32_t* tiebreak, double* acc, double* weight, uint64_t* counts,

@@ -514,10 +514,16 @@ class DSlicedOnline:
         partial kernel over peer memory; otherwise, with >1 torch.distributed
         rank, the popcounts are all-reduced (NCCL)."""
         if peers is not None:
-            for start, n in self.batches():
-                ep = peers.next_epoch()
-                self.peer_partial(peers, start, n, ep)
-                self.peer_update(peers, start, n, ep)
+            # every batch enqueued by one library call (no per-batch host round trip)
+            e, nb = self.e, len(self.batches())
+            own = peers.bases[peers.rank]
+            N.check(N.lib().hv_dev_online_sliced_run_peers(
+                e.dc.h, _ptr(self.enc), self.rows, self.words, self.w0, e.D, _ptr(self.labels), e.C, self.bsz,
+                self.gamma, _ptr(e.cb.model_tiebreak), _ptr(peers.peer_ptrs(0)), _ptr(peers.peer_ptrs(1)),
+                C.c_void_p(own), C.c_void_p(own + peers.slot), _ptr(peers.flags_ptrs),
+                C.c_void_p(own + peers.off_flags), peers.world, peers.rank, peers.epoch, _ptr(self.acc),
+                _ptr(self.weight), _ptr(self.counts), _ptr(self.cv)))
+            peers.epoch += nb
             return self.acc, self.weight, self.counts, self.cv
         dist = torch.distributed
         multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
