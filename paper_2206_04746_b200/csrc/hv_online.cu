@@ -52,6 +52,9 @@ namespace hvb {
 namespace {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
+#ifndef HV_REPLAY_UNROLL
+#define HV_REPLAY_UNROLL 32  // COLS = 1 replay loop unroll: 4 / 8 / 16 / 32 -> 17.0 / 15.5 / 13.4 / 13.0 us per CHB-MIT batch
+#endif
 // A replay item is (class, block of 8*COLS words); each of its 256 replay
 // threads owns COLS bit columns (independent accumulator chains) and the
 // staged tile holds 256/COLS entries x 8*COLS words (2,048 words) either way.
@@ -95,6 +98,8 @@ struct OnlineParams {
   uint32_t* pre;               // optional: bsz x C popcounts of the (single) batch, precomputed;
                                // zeroed as read, and best[0, bsz) is reset after the batch
   uint32_t* wflag;             // MERGED: per-class epoch flags of the separate weight tasks (nullable)
+  uint32_t ablate;             // timing experiments only (HVB200_ONLINE_ABLATE): bit0 no next-chunk loads,
+                               // bit1 no replay loop, bit2 no chunk stores (results are wrong)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* ptr) {
@@ -308,7 +313,7 @@ template <int COLS>
 __device__ __forceinline__ void replay_chunk(const uint32_t* words, const double* val, uint32_t m, double (&a)[COLS]) {
 
   const uint32_t lane = threadIdx.x & 31u, ww = threadIdx.x >> 5;
-  constexpr int kUnroll = COLS == 1 ? 8 : 2;  // enough independent loads in flight ahead of the chain
+  constexpr int kUnroll = COLS == 1 ? HV_REPLAY_UNROLL : 2;  // enough independent loads in flight ahead of the chain
 #pragma unroll kUnroll
   for (uint32_t k = 0; k < m; ++k) {
     const double v = val[k];
@@ -464,9 +469,10 @@ __device__ void replay_merged(const OnlineParams& p, const unsigned long long* b
     uint32_t buf = 0;
     for (uint32_t ch = 0; ch < n; ch += RTile<COLS>::kChunk, buf ^= 1u) {
       const bool more = ch + RTile<COLS>::kChunk < n;
-      if (more) load_chunk(ch + RTile<COLS>::kChunk);  // in flight during the replay below
+      if (more && !(p.ablate & 1u)) load_chunk(ch + RTile<COLS>::kChunk);  // in flight during the replay below
       const uint32_t m = min(static_cast<uint32_t>(RTile<COLS>::kChunk), n - ch);
-      if (tid < kOReplay) {
+      if (p.ablate & 2u) {
+      } else if (tid < kOReplay) {
         replay_chunk<COLS>(s.words[buf], s.val[buf], m, a);  // non-listed rows carry +0.0
       } else if (lane == 0 && !sep) {
 #pragma unroll 8
@@ -476,7 +482,7 @@ __device__ void replay_merged(const OnlineParams& p, const unsigned long long* b
           ntrue += f >> 1;
         }
       }
-      if (more) store_chunk(buf ^ 1u);  // the other buffer was last read before the previous barrier
+      if (more && !(p.ablate & 4u)) store_chunk(buf ^ 1u);  // the other buffer was last read before the previous barrier
       __syncthreads();
     }
     const unsigned long long q2 = pr ? gtimer() : 0ull;
@@ -943,7 +949,9 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   if (wtask) wflag.zero();
   OnlineParams p{enc,     labels,   rows,     static_cast<uint32_t>(D), static_cast<uint32_t>(W),
                  static_cast<uint32_t>(C), n, gamma, tie, acc, wts.ptr, counts, cv, best.ptr, truep.ptr, lidx.ptr,
-                 lval.ptr, llen.ptr, nullptr, lane_class ? 1u : 0u, 1u, nullptr, nullptr, nullptr, wtask ? wflag.ptr : nullptr};
+                 lval.ptr, llen.ptr, nullptr, lane_class ? 1u : 0u, 1u, nullptr, nullptr, nullptr, wtask ? wflag.ptr : nullptr,
+                 0u};
+  if (const char* ab = getenv("HVB200_ONLINE_ABLATE")) p.ablate = static_cast<uint32_t>(atoi(ab));  // timing only
   // HVB200_ONLINE_PROFILE=1: print the time per phase (CTA 0's view, barrier waits included)
   const char* pe = getenv("HVB200_ONLINE_PROFILE");
   DevBuf<unsigned long long> prof(pe && pe[0] == '1' ? 7 : 0, st);
