@@ -70,6 +70,14 @@ struct RTile {
   static constexpr int kWords = 8 * COLS;         // words per item
   static constexpr int kChunk = kOTile / kWords;  // entries per chunk
 };
+// COLS = 1 stages a chunk word-major: word ww of row k at ww * kWordPitch + k
+// (pitch 260 = 256 rows + 4: 16-byte aligned for LDS.128, and the 8 words of
+// one row land in 8 different banks when stored)
+constexpr uint32_t kWordPitch = 260;
+template <int COLS>
+__device__ __forceinline__ uint32_t staged_word(uint32_t k, uint32_t ww) {
+  return COLS == 1 ? ww * kWordPitch + k : k * RTile<COLS>::kWords + ww;
+}
 constexpr uint32_t kMergedMaxC = 2;  // more classes: per-class lists skip the other classes' rows
 constexpr uint32_t kLaneClassMinC = 16;  // measured: tiled wins at C = 26 (25 -> 17 us), loses at C <= 10
 
@@ -311,6 +319,28 @@ __device__ __forceinline__ void load_columns(const OnlineParams& p, uint32_t c, 
 // x + y == 0 rounds to +0.0).
 template <int COLS>
 __device__ __forceinline__ void replay_chunk(const uint32_t* words, const double* val, uint32_t m, double (&a)[COLS]) {
+  if constexpr (COLS == 1) {
+    // word-major staging (word ww of rows k.. at ww * kWordPitch + k, see
+    // staged_word): a warp reads 4 rows' words with one broadcast LDS.128
+    // instead of one LDS per row — 8 warps x 1 wavefront per row was the
+    // replay's shared-memory bill. Rows past m were staged as 0 words and
+    // +0.0 values, so the loop runs in whole groups of 4.
+    const uint32_t lane = threadIdx.x & 31u, ww = threadIdx.x >> 5;
+    const uint32_t* wv = words + ww * kWordPitch;
+    double acc = a[0];
+#pragma unroll 8
+    for (uint32_t k = 0; k < m; k += 4) {
+      const uint4 w4 = *reinterpret_cast<const uint4*>(wv + k);
+      const double2 v01 = *reinterpret_cast<const double2*>(val + k);
+      const double2 v23 = *reinterpret_cast<const double2*>(val + k + 2);
+      acc = __dadd_rn(acc, ((w4.x >> lane) & 1u) ? v01.x : 0.0);
+      acc = __dadd_rn(acc, ((w4.y >> lane) & 1u) ? v01.y : 0.0);
+      acc = __dadd_rn(acc, ((w4.z >> lane) & 1u) ? v23.x : 0.0);
+      acc = __dadd_rn(acc, ((w4.w >> lane) & 1u) ? v23.y : 0.0);
+    }
+    a[0] = acc;
+    return;
+  }
 
   const uint32_t lane = threadIdx.x & 31u, ww = threadIdx.x >> 5;
   constexpr int kUnroll = COLS == 1 ? HV_REPLAY_UNROLL : 2;  // enough independent loads in flight ahead of the chain
@@ -326,7 +356,7 @@ __device__ __forceinline__ void replay_chunk(const uint32_t* words, const double
 }
 
 struct Smem {
-  uint32_t words[2][kOTile];
+  uint32_t words[2][8 * kWordPitch];  // >= kOTile: COLS = 1 uses the padded word-major layout
   double val[2][kLChunk];
   uint8_t flag[2][kLChunk];  // MERGED: bit0 listed, bit1 true sample; lists: true sample
   uint32_t warpcnt[kLChunk / 32];
@@ -457,7 +487,7 @@ __device__ void replay_merged(const OnlineParams& p, const unsigned long long* b
       for (int i = 0; i < kLoadsPer; ++i) {
         const uint32_t e = tid + i * kOThreads;
         const uint32_t k = e / RTile<COLS>::kWords, ww = e % RTile<COLS>::kWords;
-        if (k < RTile<COLS>::kChunk) s.words[buf][k * RTile<COLS>::kWords + ww] = rw[i];
+        if (k < RTile<COLS>::kChunk) s.words[buf][staged_word<COLS>(k, ww)] = rw[i];
       }
     };
     const bool pr = p.prof != nullptr && blockIdx.x == 0 && tid == 0;
@@ -625,7 +655,7 @@ __device__ void replay_lists(const OnlineParams& p, Smem& s, uint64_t b0, uint32
       for (int i = 0; i < kLoadsPer; ++i) {
         const uint32_t e = tid + i * kOThreads;
         const uint32_t k = e / RTile<COLS>::kWords, ww = e % RTile<COLS>::kWords;
-        if (k < RTile<COLS>::kChunk) s.words[buf][k * RTile<COLS>::kWords + ww] = rw[i];
+        if (k < RTile<COLS>::kChunk) s.words[buf][staged_word<COLS>(k, ww)] = rw[i];
       }
     };
     load_chunk(0);
