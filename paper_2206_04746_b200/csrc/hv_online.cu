@@ -403,8 +403,21 @@ __device__ void class_weight_task(const OnlineParams& p, Smem& s, uint64_t b0, u
     if (ch + kLChunk < n) fill(ch + kLChunk, buf ^ 1u);
     if (tid == 0) {
       const uint32_t m = min(static_cast<uint32_t>(kLChunk), n - ch);
+      // four entries per step (two LDS.128 of values, one LDS of four flag
+      // bytes), 32 in flight per unrolled iteration: only the adds are serial
+      const uint32_t m4 = m & ~3u;
 #pragma unroll 8
-      for (uint32_t k = 0; k < m; ++k) {
+      for (uint32_t k = 0; k < m4; k += 4) {
+        const double2 v01 = *reinterpret_cast<const double2*>(&s.val[buf][k]);
+        const double2 v23 = *reinterpret_cast<const double2*>(&s.val[buf][k + 2]);
+        const uint32_t f4 = *reinterpret_cast<const uint32_t*>(&s.flag[buf][k]);
+        wsum = __dadd_rn(wsum, v01.x);
+        wsum = __dadd_rn(wsum, v01.y);
+        wsum = __dadd_rn(wsum, v23.x);
+        wsum = __dadd_rn(wsum, v23.y);
+        ntrue += (f4 * 0x01010101u) >> 24;  // the four 0/1 flag bytes
+      }
+      for (uint32_t k = m4; k < m; ++k) {
         wsum = __dadd_rn(wsum, s.val[buf][k]);
         ntrue += s.flag[buf][k];
       }
