@@ -325,3 +325,34 @@ def test_table_encoder_up_to_32_bins_vs_generic_and_oracle(B, binding, monkeypat
     want = O.encode_batch(b, _u32(cbk.id_vectors), _u32(cbk.value_vectors), B, D,
                           O.BIND_ID_LEVEL if binding == 0 else O.BIND_PERMUTATION, _u32(cbk.encode_tiebreak))
     np.testing.assert_array_equal(_u32(fast[torch.as_tensor(idx, device="cuda")]), want)
+
+
+@pytest.mark.parametrize("extra", [1, 3])
+def test_odd_row_pitch_takes_word_kernels_and_agrees(extra):
+    """Rows whose pitch is not a multiple of 4 words (no 16-byte rows) take the
+    word-wise count and scan kernels with the pitch honoured; results equal
+    the unpitched ones. Empty inputs are no-ops."""
+    D, C, rows = 10000, 3, 4100
+    cbk = dv.DeviceCodebook.make(40, 16, D, seed=extra)
+    eng = dv.Engine(cbk, C)
+    bins8, _ = eng.synth(0, rows, 0, 5)
+    labels = torch.randint(0, C, (rows,), dtype=torch.int32, device="cuda")
+    flat = eng.encode(bins8)
+    store = torch.full((rows, eng.W + extra), -1, dtype=torch.int32, device="cuda")
+    odd = store[:, :eng.W]
+    eng.encode(bins8, out=odd)
+    assert torch.equal(odd, flat)
+    c1, r1 = eng.zero_counts()
+    c2, r2 = eng.zero_counts()
+    eng.class_counts(flat, labels, c1, r1)
+    eng.class_counts(odd, labels, c2, r2)
+    assert torch.equal(c1, c2) and torch.equal(r1, r2)
+    cv = eng.binarize(c1, r1)
+    d1 = torch.empty((rows, C), dtype=torch.float64, device="cuda")
+    d2 = torch.empty_like(d1)
+    assert torch.equal(eng.predict(cv, flat, distances=d1), eng.predict(cv, odd, distances=d2))
+    assert torch.equal(d1, d2)
+    eng.class_counts(odd[:0], labels[:0], c2, r2)
+    eng.predict(cv, odd[:0])
+    eng.dc.check()
+    assert torch.equal(c1, c2)
