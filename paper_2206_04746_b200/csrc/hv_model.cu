@@ -1741,8 +1741,18 @@ void dataset_fold_impl(hv_context* ctx, const hv_dataset* ds, const uint64_t* tr
     d_val.upload(value_vectors);
     d_etb.upload(encode_tiebreak);
     d_mtb.upload(model_tiebreak);
-    DevBuf<uint32_t> enc(n * W, st);
-    encode_device(ctx, st, b8.ptr, ldb, n, F, d_id.ptr, d_val.ptr, bins, D, binding, d_etb.ptr, enc.ptr);
+    // classical Hamming folds with < 32 classes keep the engine's pitched rows
+    // (TMA-staged counts, uint4 / two-class predict); the online trainer and the
+    // cosine scan read unpitched rows
+    const bool pitched = !online && metric == HV_METRIC_HAMMING && C < 32;
+    const size_t ldw = pitched ? hv_row_pitch_words(D) : W;
+    DevBuf<uint32_t> enc(n * ldw, st);
+    if (pitched && ldw != W) {
+      encode_device(ctx, st, b8.ptr, ldb, n, F, d_id.ptr, d_val.ptr, bins, D, binding, d_etb.ptr, enc.ptr, true, 0, W,
+                    ldw);
+    } else {
+      encode_device(ctx, st, b8.ptr, ldb, n, F, d_id.ptr, d_val.ptr, bins, D, binding, d_etb.ptr, enc.ptr);
+    }
     DevBuf<int32_t> ytr(n_train, st), lab(std::max<size_t>(n_test, 1), st);
     gather_labels_kernel<<<sgrid(ctx, n_train, 256), 256, 0, st>>>(ds->y.ptr, idx.ptr, n_train, ytr.ptr);
     launched("gather_labels_kernel");
@@ -1759,7 +1769,7 @@ void dataset_fold_impl(hv_context* ctx, const hv_dataset* ds, const uint64_t* tr
       DevBuf<uint32_t> cnt(C * 32 * W, st);
       cnt.zero();
       counts.zero();
-      class_counts_device(ctx, st, enc.ptr, n_train, W, ytr.ptr, C, cnt.ptr, counts.ptr);
+      class_counts_device(ctx, st, enc.ptr, n_train, W, ytr.ptr, C, cnt.ptr, counts.ptr, ldw);
       binarize_counts_device(ctx, st, cnt.ptr, counts.ptr, C, D, d_mtb.ptr, cv.ptr);
       if (metric == HV_METRIC_COSINE) {
         init_from_counts_kernel<<<sgrid(ctx, C * D, 256), 256, 0, st>>>(cnt.ptr, counts.ptr, C, D, W, acc.ptr,
@@ -1768,9 +1778,9 @@ void dataset_fold_impl(hv_context* ctx, const hv_dataset* ds, const uint64_t* tr
       }
     }
     if (n_test) {
-      const uint32_t* q = enc.ptr + n_train * W;
+      const uint32_t* q = enc.ptr + n_train * ldw;
       if (metric == HV_METRIC_HAMMING) {
-        predict_hamming_device(ctx, st, cv.ptr, C, D, q, n_test, lab.ptr, nullptr, nullptr);
+        predict_hamming_device(ctx, st, cv.ptr, C, D, q, n_test, lab.ptr, nullptr, nullptr, ldw);
       } else {
         DevBuf<double> sc(n_test * C, st);
         cosine_scores_device(ctx, st, acc.ptr, C, D, q, n_test, sc.ptr, 0);
