@@ -786,7 +786,10 @@ void predict_hamming_device(hv_context* ctx, cudaStream_t st, const uint32_t* cv
     }
     if (ldq % 4 == 0 && (reinterpret_cast<uintptr_t>(enc) & 15u) == 0 && smem <= 96 * 1024) {
       // 16-byte rows: class vectors staged in shared memory, uint4 row reads
-      const unsigned grid = sgrid(ctx, rows * 32, 256, 32);
+      // each CTA first stages C x W4 uint4 of class vectors: fewer, longer-lived
+      // CTAs amortise that for C > 2 (env HVB200_PREDICT_CTAS_PER_SM to tune)
+      const char* gp = getenv("HVB200_PREDICT_CTAS_PER_SM");
+      const unsigned grid = sgrid(ctx, rows * 32, 256, gp ? std::max(1, atoi(gp)) : 8);
 #define HV_PP(CB)                                                                                          \
   do {                                                                                                     \
     ck(cudaFuncSetAttribute(predict_hamming_pitched_kernel<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, \

@@ -51,7 +51,7 @@ def main():
         cbk = dv.DeviceCodebook.make(F, 16, D, seed=1)
         eng = dv.Engine(cbk, C)
         bins8, labels = eng.synth(0, rows, 1 if name == "E" else 0, 7)
-        enc = eng.encode(bins8)
+        enc = eng.encode(bins8, pitched=True)  # the engine's resident layout (16-byte rows)
         del bins8
         W = enc.shape[1]
         ntr = rows * 4 // 5
