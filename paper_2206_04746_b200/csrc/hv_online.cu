@@ -42,6 +42,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "hv_internal.cuh"
 #include "hv_scan.cuh"
@@ -78,6 +79,7 @@ template <int COLS>
 __device__ __forceinline__ uint32_t staged_word(uint32_t k, uint32_t ww) {
   return COLS == 1 ? ww * kWordPitch + k : k * RTile<COLS>::kWords + ww;
 }
+constexpr uint32_t kOrderMax = 1024;  // classes ordered longest-list-first when C <= this
 constexpr uint32_t kMergedMaxC = 2;  // more classes: per-class lists skip the other classes' rows
 constexpr uint32_t kLaneClassMinC = 16;  // measured: tiled wins at C = 26 (25 -> 17 us), loses at C <= 10
 
@@ -106,6 +108,7 @@ struct OnlineParams {
   uint32_t* pre;               // optional: bsz x C popcounts of the (single) batch, precomputed;
                                // zeroed as read, and best[0, bsz) is reset after the batch
   uint32_t* wflag;             // MERGED: per-class epoch flags of the separate weight tasks (nullable)
+  uint32_t* item_ctr;          // LISTS: dynamic replay-item counter (nullable: static round robin)
   uint32_t ablate;             // timing experiments only (HVB200_ONLINE_ABLATE): bit0 no next-chunk loads,
                                // bit1 no replay loop, bit2 no chunk stores (results are wrong)
 };
@@ -361,6 +364,8 @@ struct Smem {
   uint8_t flag[2][kLChunk];  // MERGED: bit0 listed, bit1 true sample; lists: true sample
   uint32_t warpcnt[kLChunk / 32];
   double weight;
+  uint32_t dyn_item;
+  uint16_t order[kOrderMax];  // LISTS + dynamic: classes by decreasing list length
 };
 
 // The class weight of class c over the batch's true samples, in sample order
@@ -640,11 +645,41 @@ __device__ void replay_lists(const OnlineParams& p, Smem& s, uint64_t b0, uint32
     const uint32_t c = static_cast<uint32_t>(blockIdx.x - items);
     class_weight_task<true>(p, s, b0, n, c, p.weight + c, p.weight + c, epoch);  // LISTS: weights in place
   }
-  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
-    const uint32_t c = static_cast<uint32_t>(item / nwb);
+  // items are handed out dynamically when a counter is given: per-class list
+  // lengths vary (a class can collect hundreds of mispredicted rows), so a
+  // static round robin left CTAs with long lists as the batch's tail. The
+  // counter advances by exactly items + gridDim.x per batch (every CTA draws
+  // one index past the end), so batch bi's indices start at bi * that.
+  const uint64_t base = static_cast<uint64_t>(b0 / p.bsz) * (items + gridDim.x);
+  // longest lists first (their items are the long ones): every CTA ranks the
+  // classes itself (C^2 / 32 compares per lane), no extra grid barrier
+  const bool ordered = p.item_ctr != nullptr && p.C <= kOrderMax;
+  if (ordered) {
+    for (uint32_t c = tid; c < p.C; c += blockDim.x) {
+      const uint32_t lc = p.llen[c];
+      uint32_t rank = 0;
+      for (uint32_t d = 0; d < p.C; ++d) {
+        const uint32_t ld = p.llen[d];
+        rank += (ld > lc || (ld == lc && d < c)) ? 1u : 0u;
+      }
+      s.order[rank] = static_cast<uint16_t>(c);
+    }
+    __syncthreads();
+  }
+  for (uint64_t item = blockIdx.x;; item += gridDim.x) {
+    if (p.item_ctr) {
+      if (tid == 0) s.dyn_item = static_cast<uint32_t>(atomicAdd(p.item_ctr, 1u) - base);
+      __syncthreads();
+      item = s.dyn_item;
+      __syncthreads();
+    }
+    if (item >= items) break;
+    const uint32_t c = ordered ? s.order[item / nwb] : static_cast<uint32_t>(item / nwb);
     const uint32_t len = p.llen[c];
     if (len == 0) continue;  // untouched class: acc and class vector unchanged
     const uint32_t wb = static_cast<uint32_t>(item % nwb);
+    const bool pr = p.prof != nullptr && blockIdx.x == 0 && tid == 0;
+    const unsigned long long q0 = pr ? gtimer() : 0ull;
     double a[COLS];
     if (tid < kOReplay) load_columns<COLS>(p, c, wb, a);
     const uint32_t* li = p.lidx + static_cast<uint64_t>(c) * p.bsz;
@@ -674,6 +709,7 @@ __device__ void replay_lists(const OnlineParams& p, Smem& s, uint64_t b0, uint32
     load_chunk(0);
     store_chunk(0);
     __syncthreads();
+    const unsigned long long q1 = pr ? gtimer() : 0ull;
     uint32_t buf = 0;
     for (uint32_t k0 = 0; k0 < len; k0 += RTile<COLS>::kChunk, buf ^= 1u) {
       const bool more = k0 + RTile<COLS>::kChunk < len;
@@ -690,8 +726,15 @@ __device__ void replay_lists(const OnlineParams& p, Smem& s, uint64_t b0, uint32
       }
       __syncthreads();
     }
+    const unsigned long long q2 = pr ? gtimer() : 0ull;
     if (tid < kOReplay) store_columns<COLS>(p, c, wb, a, sep ? s.weight : p.weight[c], true);
     if (sep) __syncthreads();  // s.weight reuse by the next item
+    if (pr) {
+      p.prof[3] += q1 - q0;           // columns + first chunk staged
+      p.prof[4] += q2 - q1;           // chunk loop (+ weight wait)
+      p.prof[6] += gtimer() - q2;     // store
+      p.prof[5] += 1;                 // items this CTA ran (reported x1e3 per batch)
+    }
   }
 }
 
@@ -993,7 +1036,8 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   OnlineParams p{enc,     labels,   rows,     static_cast<uint32_t>(D), static_cast<uint32_t>(W),
                  static_cast<uint32_t>(C), n, gamma, tie, acc, wts.ptr, counts, cv, best.ptr, truep.ptr, lidx.ptr,
                  lval.ptr, llen.ptr, nullptr, lane_class ? 1u : 0u, 1u, nullptr, nullptr, nullptr, wtask ? wflag.ptr : nullptr,
-                 0u};
+                 nullptr, 0u};
+  DevBuf<uint32_t> item_ctr(merged ? 0 : 1, st);
   if (const char* ab = getenv("HVB200_ONLINE_ABLATE")) p.ablate = static_cast<uint32_t>(atoi(ab));  // timing only
   // HVB200_ONLINE_PROFILE=1: print the time per phase (CTA 0's view, barrier waits included)
   const char* pe = getenv("HVB200_ONLINE_PROFILE");
@@ -1014,6 +1058,15 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
     grid_est = cooperative_grid<false, 4>(ctx, want);
   } else {
     grid_est = cooperative_grid<false, 1>(ctx, want);
+  }
+  // more replay items than CTAs (many classes, e.g. Large: 1,600 items on 296
+  // CTAs): hand them out dynamically, longest lists first (replay 61.8 -> 47.3
+  // us per batch at C = 100, D = 32768); with at most one item per CTA the
+  // static assignment is already ideal
+  if (!merged && items > grid_est) {
+    item_ctr.zero();
+    const char* dyn = getenv("HVB200_ONLINE_DYNAMIC");  // =0: static round robin (A/B)
+    if (!(dyn && dyn[0] == '0')) p.item_ctr = item_ctr.ptr;
   }
   // many classes: score each batch on the tensor cores (hv_predict_tc.cu) and
   // run the persistent kernel once per batch on the precomputed popcounts
@@ -1052,6 +1105,7 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
       p.enc = enc + b0 * W;
       p.labels = labels + b0;
       p.rows = nn;
+      if (p.item_ctr) ck(cudaMemsetAsync(p.item_ctr, 0, sizeof(uint32_t), st), "item counter");  // batch 0 of this launch
       launch(kern, grid_est);  // parity 0 only: best[0, n) was reset by the previous launch
     }
   } else if (merged) {
@@ -1073,6 +1127,17 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
             " [CTA 0 item: stage %.2f chunks %.2f weight-wait %.2f store %.2f]\n",
             merged ? "merged" : "lists", cols8 ? 8 : cols4 ? 4 : 1, p.ksplit, h[0] / nb / 1e3, h[1] / nb / 1e3,
             h[2] / nb / 1e3, h[3] / nb / 1e3, h[4] / nb / 1e3, h[5] / nb / 1e3, h[6] / nb / 1e3);
+    if (!merged) {  // the last batch's per-class list lengths
+      std::vector<uint32_t> len(C);
+      ck(cudaMemcpy(len.data(), llen.ptr, C * sizeof(uint32_t), cudaMemcpyDeviceToHost), "D2H llen");
+      uint64_t sum = 0, mx = 0;
+      for (uint32_t v : len) {
+        sum += v;
+        mx = std::max<uint64_t>(mx, v);
+      }
+      fprintf(stderr, "online lists (last batch): mean %.1f max %llu entries per class; grid %u CTAs, %llu items\n",
+              double(sum) / C, static_cast<unsigned long long>(mx), grid_est, static_cast<unsigned long long>(items));
+    }
   }
   // MERGED leaves the final weights in the parity row after the last batch
   const size_t nb = (rows + n - 1) / n;
