@@ -493,11 +493,25 @@ void launch_column_count_any(cudaStream_t st, const uint32_t* m, uint32_t W, uin
   if (max_pos > 0xFFFFFFFFull) invalid("class counts: more than 2^32 rows per call");
   if (ldm == 0) ldm = W;
   if (ldm < W) invalid("class counts: row pitch < words per row");
-  const uint32_t chunk = 2048;
+  uint32_t chunk = 2048;
   if (ldm % 4 == 0 && (reinterpret_cast<uintptr_t>(m) & 15u) == 0) {
     // pitched, 16-byte aligned rows: TMA-staged whole-row reads
     const uint32_t W4 = (W + 3) / 4 * 4;
     const uint32_t nranges = (W4 + kCsMaxCols - 1) / kCsMaxCols;
+    // short inputs (an online bootstrap batch, small folds): shorter chunks so
+    // there are ~2 CTAs per SM instead of a handful (1,024 rows at W = 1024
+    // were 2 CTAs)
+    static int sms = 0;
+    if (sms == 0) {
+      int dev = 0;
+      ck(cudaGetDevice(&dev), "cudaGetDevice");
+      ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+    }
+    const uint64_t want_ctas = 2ull * static_cast<uint64_t>(sms);
+    if ((max_pos + chunk - 1) / chunk * nranges < want_ctas) {
+      const uint64_t c = (max_pos * nranges + want_ctas - 1) / want_ctas;
+      chunk = static_cast<uint32_t>(std::max<uint64_t>(64, (c + 15) / 16 * 16));
+    }
     const uint32_t ncols = (W4 / 4 + nranges - 1) / nranges * 4;  // balanced ranges, multiple of 4
     const uint32_t threads = (ncols + 31) / 32 * 32;
     dim3 grid(nranges, static_cast<unsigned>((max_pos + chunk - 1) / chunk));
@@ -524,6 +538,19 @@ void launch_column_count_any(cudaStream_t st, const uint32_t* m, uint32_t W, uin
     go(column_count_staged_kernel<CT, 16, 2>, 16, 2);
     launched("column_count_staged_kernel");
     return;
+  }
+  {  // short inputs: shorter chunks for ~8 warps per SM
+    static int sms2 = 0;
+    if (sms2 == 0) {
+      int dev = 0;
+      ck(cudaGetDevice(&dev), "cudaGetDevice");
+      ck(cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev), "sm count");
+    }
+    const uint64_t groups = (W + 31) / 32, want_warps = 8ull * static_cast<uint64_t>(sms2);
+    if ((max_pos + chunk - 1) / chunk * groups < want_warps) {
+      const uint64_t c = (max_pos * groups + want_warps - 1) / want_warps;
+      chunk = static_cast<uint32_t>(std::max<uint64_t>(64, (c + 31) / 32 * 32));
+    }
   }
   const unsigned grid = column_count_grid<CT>(max_pos, W, chunk);
   column_count_kernel<CT><<<grid, 128, 0, st>>>(m, W, ldm, perm, seg_off, nseg, max_pos, chunk, single, dsts_dev,
