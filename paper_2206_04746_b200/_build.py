@@ -30,8 +30,14 @@ NVCC_FLAGS = [
 ]
 
 
+CXX = os.environ.get("CXX", "g++")
+CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-g", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+
+
 def sources():
-    return sorted(CSRC.glob("*.cu"))
+    """CUDA translation units (nvcc) plus host-only .cpp files (host compiler,
+    for code that needs intrinsics nvcc's front end does not take)."""
+    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
 
 
 def _stale() -> bool:
@@ -44,10 +50,13 @@ def _stale() -> bool:
 
 def _compile(src: Path) -> Path:
     out = OBJ / (src.stem + ".o")
-    cmd = [NVCC, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(out)]
+    if src.suffix == ".cpp":
+        cmd = [CXX, *CXX_FLAGS, "-c", str(src), "-o", str(out)]
+    else:
+        cmd = [NVCC, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(out)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stdout}\n{r.stderr}")
+        raise RuntimeError(f"compile failed for {src.name}:\n{r.stdout}\n{r.stderr}")
     if r.stderr.strip() and os.environ.get("HVB200_PTXAS_VERBOSE"):
         sys.stderr.write(r.stderr)
     return out

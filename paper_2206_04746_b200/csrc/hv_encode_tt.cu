@@ -60,6 +60,10 @@ struct TT6Params {
   uint64_t blocks;      // ceil(rows / block_rows)
   unsigned int* counter;
   uint32_t perm;        // permutation binding: bound word = rotate(V_b, f) (encoding.cpp:273-279)
+  // streamed input (host staging pipeline): rows [0, *ready) of bins8 have
+  // landed; an item waits until its block's rows have; ~0 = aborted (rows
+  // past the landed ones were never validated). nullptr = all resident.
+  const unsigned long long* ready;
 };
 
 template <int NW>
@@ -103,6 +107,12 @@ __device__ __forceinline__ uint32_t majority_biased(const uint32_t (&pl)[6 + NH]
   return pl[K - 1] & (odd ? 0xFFFFFFFFu : (any | tie));
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* a) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+
 template <int NPR, int G, int NH, int MINB, bool PERM, int TB>
 __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
   constexpr int NW = 2 * NPR;
@@ -122,7 +132,19 @@ __global__ void __launch_bounds__(G * 32, MINB) encode_tt6_kernel(TT6Params p) {
   const uint32_t lr = lane >> 2, lq = lane & 3u;
 
   for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(p.counter, 1u);
+    if (threadIdx.x == 0) {
+      const unsigned int it = atomicAdd(p.counter, 1u);
+      s_item = it;
+      if (p.ready != nullptr && it < items) {
+        // the copies that fill bins8 and then advance *ready run on a copy
+        // engine, so waiting here cannot block them (no SM is needed)
+        const uint64_t end = (it / p.slices + 1) * static_cast<uint64_t>(p.block_rows);
+        const unsigned long long need = end < p.rows ? end : p.rows;
+        unsigned long long v;
+        while ((v = ld_acquire_u64(p.ready)) < need) __nanosleep(256);
+        if (v == ~0ull) s_item = 0xFFFFFFFFu;  // the host aborted the call (bad bin): stop, output discarded
+      }
+    }
     __syncthreads();
     const uint64_t item = s_item;
     __syncthreads();
@@ -344,7 +366,8 @@ void launch_tt6_inst(hv_context* ctx, cudaStream_t st, TT6Params p, size_t smem)
 
 bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
                const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
-               uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo, uint32_t* counter, bool perm) {
+               uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo, uint32_t* counter, bool perm,
+               const unsigned long long* ready) {
   // zero-padded feature count: a multiple of 8 (the partial chunk runs blocks of
   // 16 and 8), unless padding to 16 completes a 64-feature chunk (the full-chunk
   // tree is cheaper per feature): CHB-MIT 342 -> 344 (was 352), UCI-HAR 561 -> 576
@@ -395,7 +418,7 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
     if (v >= 32 && v <= (1l << 30)) block_rows = static_cast<uint32_t>(v / 32 * 32);
   }
   TT6Params p{bins8, ldb, rows, F, Fpad, D, W, B, id, val, tie, out, w0, wcount, ldo, slices, block_rows,
-              (rows + block_rows - 1) / block_rows, counter, perm ? 1u : 0u};
+              (rows + block_rows - 1) / block_rows, counter, perm ? 1u : 0u, ready};
 #define HV_TT6(NPR, G, MB, N, TB)                                        \
   if (s.npr == NPR && s.g == G && s.minb == MB && nh == N && tb == TB) { \
     launch_tt6_inst<NPR, G, N, MB, TB>(ctx, st, p, smem);                \
@@ -417,13 +440,14 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
 
 bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
                const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
-               uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo, bool perm) {
+               uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo, bool perm,
+               const unsigned long long* ready) {
   if (B > 32u || F == 0 || rows == 0 || wcount == 0) return false;
   if (ldb % kChunk != 0 || (reinterpret_cast<uintptr_t>(bins8) & 15u)) return false;
   // one work counter per launch from the context's ring (concurrent launches on
   // the context's two streams must not share one)
   unsigned int* counter = ctx->d_counters + (ctx->next_counter++ % hv_context::kCounters);
-  return launch_v6(ctx, st, bins8, ldb, rows, F, id, val, B, D, W, tie, out, w0, wcount, ldo, counter, perm);
+  return launch_v6(ctx, st, bins8, ldb, rows, F, id, val, B, D, W, tie, out, w0, wcount, ldo, counter, perm, ready);
 }
 
 }  // namespace hvb

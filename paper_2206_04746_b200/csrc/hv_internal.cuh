@@ -188,7 +188,8 @@ void discretize_rows_device(hv_context* ctx, cudaStream_t st, const double* X, s
                             size_t n, const double* mn, const double* mx, size_t B, uint8_t* out, size_t ldb);
 bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
                const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
-               uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo, bool perm = false);
+               uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo, bool perm = false,
+               const unsigned long long* ready = nullptr);
 
 // Online training, Hamming metric: every batch in one persistent cooperative
 // kernel (hv_online.cu); acc/weight/counts/cv hold the bootstrap state.

@@ -1604,28 +1604,64 @@ hv_status hv_fold_encode_train(hv_context* ctx, const uint32_t* train_bins, size
     d_id.upload(id_vectors);
     d_val.upload(value_vectors);
     d_tie.upload(encode_tiebreak);
-    d_y.upload(train_labels);
-    const size_t chunk = stage_chunk_rows(rows, features);
-    DevBuf<uint8_t> b8[2] = {DevBuf<uint8_t>(chunk * ldb, st), DevBuf<uint8_t>(chunk * ldb, st)};
-    sync(ctx);
-    size_t k = 0;
     uint32_t* enc = fold->enc.ptr;
-    uint64_t bad = encode_host_bins(ctx, train_bins, train_rows, features, bins, dim, HV_BIND_ID_LEVEL, d_id.ptr,
-                                    d_val.ptr, d_tie.ptr, [&](size_t r0, size_t) { return enc + r0 * ldw; }, b8,
-                                    chunk, k, {}, ldw);
-    if (bad == ~0ull) {
-      // classical counts of the train rows overlap the staging/encode of the test rows
-      cudaEvent_t ev;
-      ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
-      ck(cudaEventRecord(ev, ctx->aux), "event");
-      ck(cudaStreamWaitEvent(ctx->stream, ev, 0), "wait");
-      cudaEventDestroy(ev);
-      class_counts_device(ctx, ctx->stream, enc, train_rows, W, d_y.ptr, class_count, fold->counts.ptr,
-                          fold->class_rows.ptr, ldw);
-      bad = encode_host_bins(ctx, test_bins, test_rows, features, bins, dim, HV_BIND_ID_LEVEL, d_id.ptr, d_val.ptr,
-                             d_tie.ptr, [&](size_t r0, size_t) { return enc + (train_rows + r0) * ldw; }, b8, chunk,
-                             k, {}, ldw);
-      if (bad != ~0ull) bad += train_rows * features;
+    uint64_t bad = ~0ull;
+    // streamed staging (one persistent encoder launch per row set, fed by the
+    // host copies; HVB200_STAGE_STREAM=0 selects the chunked pipeline)
+    const char* se = getenv("HVB200_STAGE_STREAM");
+    bool streamed = !(se && atoi(se) == 0);
+    DevBuf<uint8_t> d_bins;
+    DevBuf<unsigned long long> d_ready;
+    if (streamed) {
+      d_bins = DevBuf<uint8_t>(rows * ldb, st);
+      d_ready = DevBuf<unsigned long long>(2, st);
+      sync(ctx);
+      bad = encode_host_bins_streamed(ctx, train_bins, train_rows, features, bins, dim, d_id.ptr, d_val.ptr,
+                                      d_tie.ptr, d_bins.ptr, enc, ldw, ctx->stream, d_ready.ptr, streamed);
+      if (streamed && bad == ~0ull) {
+        // the train labels go up on the aux stream while the train rows encode
+        // (a pageable upload is synchronous for the host, so it is issued after
+        // the host has fed the launch); the classical counts of the train rows
+        // follow their launch on the main stream, the test rows' launch runs on aux
+        ck(cudaMemcpyAsync(d_y.ptr, train_labels, train_rows * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->aux),
+           "H2D labels");
+        cudaEvent_t ev;
+        ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+        ck(cudaEventRecord(ev, ctx->aux), "event");
+        ck(cudaStreamWaitEvent(ctx->stream, ev, 0), "wait");
+        cudaEventDestroy(ev);
+        class_counts_device(ctx, ctx->stream, enc, train_rows, W, d_y.ptr, class_count, fold->counts.ptr,
+                            fold->class_rows.ptr, ldw);
+        bool s2 = false;
+        bad = encode_host_bins_streamed(ctx, test_bins, test_rows, features, bins, dim, d_id.ptr, d_val.ptr,
+                                        d_tie.ptr, d_bins.ptr + train_rows * ldb, enc + train_rows * ldw, ldw,
+                                        ctx->aux, d_ready.ptr + 1, s2);
+        if (!s2) fail(HV_ERR_CUDA, "fold: streamed encoder refused the test rows");
+        if (bad != ~0ull) bad += train_rows * features;
+      }
+    }
+    if (!streamed) {
+      d_y.upload(train_labels);
+      const size_t chunk = stage_chunk_rows(rows, features);
+      DevBuf<uint8_t> b8[2] = {DevBuf<uint8_t>(chunk * ldb, st), DevBuf<uint8_t>(chunk * ldb, st)};
+      sync(ctx);
+      size_t k = 0;
+      bad = encode_host_bins(ctx, train_bins, train_rows, features, bins, dim, HV_BIND_ID_LEVEL, d_id.ptr, d_val.ptr,
+                             d_tie.ptr, [&](size_t r0, size_t) { return enc + r0 * ldw; }, b8, chunk, k, {}, ldw);
+      if (bad == ~0ull) {
+        // classical counts of the train rows overlap the staging/encode of the test rows
+        cudaEvent_t ev;
+        ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+        ck(cudaEventRecord(ev, ctx->aux), "event");
+        ck(cudaStreamWaitEvent(ctx->stream, ev, 0), "wait");
+        cudaEventDestroy(ev);
+        class_counts_device(ctx, ctx->stream, enc, train_rows, W, d_y.ptr, class_count, fold->counts.ptr,
+                            fold->class_rows.ptr, ldw);
+        bad = encode_host_bins(ctx, test_bins, test_rows, features, bins, dim, HV_BIND_ID_LEVEL, d_id.ptr, d_val.ptr,
+                               d_tie.ptr, [&](size_t r0, size_t) { return enc + (train_rows + r0) * ldw; }, b8,
+                               chunk, k, {}, ldw);
+        if (bad != ~0ull) bad += train_rows * features;
+      }
     }
     ck(cudaStreamSynchronize(ctx->aux), "sync aux");
     sync(ctx);

@@ -17,6 +17,8 @@
 // 3.6x fewer PCIe bytes, and pageable inputs cost the same as pinned ones.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
@@ -87,46 +89,6 @@ void ThreadPool::parallel_for(size_t n, const std::function<void(size_t)>& fn) {
   job_ = nullptr;
 }
 
-// ------------------------------------------------------------ narrowing ----
-namespace {
-
-// rows [r0, r1) of F uint32 bins -> uint8 rows of pitch ldb (zero padded);
-// returns the maximum bin seen (validation is one compare per chunk piece).
-template <int kDummy>
-inline uint32_t narrow_rows_impl(const uint32_t* __restrict__ in, size_t F, size_t r0, size_t r1,
-                                 uint8_t* __restrict__ out, size_t ldb) {
-  uint32_t mx = 0;
-  for (size_t r = r0; r < r1; ++r) {
-    const uint32_t* s = in + r * F;
-    uint8_t* d = out + r * ldb;
-    for (size_t f = 0; f < F; ++f) {
-      const uint32_t v = s[f];
-      mx = v > mx ? v : mx;
-      d[f] = static_cast<uint8_t>(v);
-    }
-    for (size_t f = F; f < ldb; ++f) d[f] = 0;
-  }
-  return mx;
-}
-
-__attribute__((target("avx2"))) uint32_t narrow_rows_avx2(const uint32_t* in, size_t F, size_t r0, size_t r1,
-                                                          uint8_t* out, size_t ldb) {
-  return narrow_rows_impl<1>(in, F, r0, r1, out, ldb);
-}
-
-uint32_t narrow_rows_base(const uint32_t* in, size_t F, size_t r0, size_t r1, uint8_t* out, size_t ldb) {
-  return narrow_rows_impl<0>(in, F, r0, r1, out, ldb);
-}
-
-using NarrowFn = uint32_t (*)(const uint32_t*, size_t, size_t, size_t, uint8_t*, size_t);
-
-NarrowFn narrow_fn() {
-  static const NarrowFn fn = __builtin_cpu_supports("avx2") ? narrow_rows_avx2 : narrow_rows_base;
-  return fn;
-}
-
-}  // namespace
-
 unsigned host_thread_count() {
   if (const char* e = getenv("HVB200_HOST_THREADS")) {
     const int n = atoi(e);
@@ -146,6 +108,9 @@ HostStager::HostStager() : pool(host_thread_count() - 1) {
   for (int i = 0; i < kSlots; ++i) {
     ck(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming), "cudaEventCreate");
   }
+  ck(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaHostAlloc(reinterpret_cast<void**>(&flag), kSlots * sizeof(unsigned long long), cudaHostAllocDefault),
+     "cudaHostAlloc");
 }
 
 HostStager::~HostStager() {
@@ -156,6 +121,11 @@ HostStager::~HostStager() {
     }
     if (slot[i]) cudaFreeHost(slot[i]);
   }
+  if (copy) {
+    cudaStreamSynchronize(copy);
+    cudaStreamDestroy(copy);
+  }
+  if (flag) cudaFreeHost(flag);
 }
 
 void HostStager::reserve(size_t bytes) {
@@ -179,10 +149,9 @@ uint64_t narrow_rows_host(ThreadPool& pool, const uint32_t* in, size_t rows, siz
   const size_t per = (rows + parts - 1) / parts;
   const size_t pieces = (rows + per - 1) / per;
   std::vector<uint32_t> mx(pieces, 0);
-  const NarrowFn fn = narrow_fn();
   pool.parallel_for(pieces, [&](size_t i) {
     const size_t r0 = i * per, r1 = std::min(rows, r0 + per);
-    mx[i] = fn(in, F, r0, r1, out, ldb);
+    mx[i] = narrow_rows(in, F, r0, r1, out, ldb);
   });
   for (size_t i = 0; i < pieces; ++i) {
     if (mx[i] >= B) {  // error path: first offending flat index in this piece
@@ -228,6 +197,12 @@ uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, si
   HostStager& hs = stager(ctx);
   hs.reserve(chunk * ldb);
   cudaStream_t streams[2] = {ctx->stream, ctx->aux};
+  // HVB200_STAGE_PROFILE=1: host time spent waiting for a free slot vs narrowing
+  static const bool prof = getenv("HVB200_STAGE_PROFILE") != nullptr;
+  using clk = std::chrono::steady_clock;
+  const auto t_call = clk::now();
+  double wait_ms = 0, narrow_ms = 0;
+  size_t pieces = 0;
   // the first chunks of a call ramp up (1/8, 1/4, 1/2 of a slot) so the SMs
   // start encoding after a short narrow + copy instead of a full slot's
   size_t step = k == 0 ? std::max<size_t>(1, chunk / 8) : chunk;
@@ -240,8 +215,15 @@ uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, si
     if (left <= 2 * step && left > tail_min) n = std::max(tail_min, (left + 1) / 2);
     const int s = static_cast<int>(k % HostStager::kSlots);
     cudaStream_t st = streams[k & 1];
+    const auto t0 = clk::now();
     ck(cudaEventSynchronize(hs.done[s]), "stage slot wait");  // its previous H2D has finished
+    const auto t1 = clk::now();
     const uint64_t bad = hs.narrow(bins + r0 * F, n, F, B, ldb, s);
+    if (prof) {
+      wait_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+      narrow_ms += std::chrono::duration<double, std::milli>(clk::now() - t1).count();
+      ++pieces;
+    }
     if (bad != ~0ull) return r0 * F + bad;
     ck(cudaMemcpyAsync(b8[k & 1].ptr, hs.slot[s], n * ldb, cudaMemcpyHostToDevice, st), "H2D bins");
     ck(cudaEventRecord(hs.done[s], st), "cudaEventRecord");
@@ -253,7 +235,97 @@ uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, si
     }
     if (after) after(r0, n, k, st);
   }
+  if (prof) {
+    fprintf(stderr, "[stage] rows %zu pieces %zu chunk %zu threads %zu: host %.2f ms (slot wait %.2f, narrow %.2f)\n",
+            rows, pieces, chunk, hs.pool.size() + 1,
+            std::chrono::duration<double, std::milli>(clk::now() - t_call).count(), wait_ms, narrow_ms);
+  }
   return ~0ull;
+}
+
+uint64_t encode_host_bins_streamed(hv_context* ctx, const uint32_t* bins, size_t rows, size_t F, size_t B, size_t D,
+                                   const uint32_t* d_id, const uint32_t* d_val, const uint32_t* d_tie,
+                                   uint8_t* d_bins, uint32_t* out, size_t ldo, cudaStream_t kst,
+                                   unsigned long long* d_ready, bool& launched) {
+  check_bins_u8(B, "encode");
+  launched = false;
+  if (rows == 0) {
+    launched = true;
+    return ~0ull;
+  }
+  const size_t ldb = bins_pitch(F), W = words_per_row(D);
+  if (D > 0xFFFFFFFFull || F > 0xFFFFFFFFull) invalid("encode: shape too large");
+  HostStager& hs = stager(ctx);
+  const size_t chunk = stage_chunk_rows(rows, F);
+  hs.reserve(chunk * ldb);
+  ck(cudaMemsetAsync(d_ready, 0, sizeof(unsigned long long), kst), "ready reset");
+  // the copies (and their ready updates) land after the reset — and must not
+  // wait for the launch itself, which waits for them
+  cudaEvent_t ev;
+  ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+  ck(cudaEventRecord(ev, kst), "event");
+  ck(cudaStreamWaitEvent(hs.copy, ev, 0), "wait");
+  cudaEventDestroy(ev);
+  if (!launch_tt(ctx, kst, d_bins, static_cast<uint32_t>(ldb), rows, static_cast<uint32_t>(F), d_id, d_val,
+                 static_cast<uint32_t>(B), static_cast<uint32_t>(D), static_cast<uint32_t>(W), d_tie, out, 0u,
+                 static_cast<uint32_t>(W), static_cast<uint32_t>(ldo ? ldo : W), false, d_ready)) {
+    return ~0ull;  // nothing launched (the reset alone is harmless)
+  }
+  launched = true;
+  static const bool prof = getenv("HVB200_STAGE_PROFILE") != nullptr;
+  using clk = std::chrono::steady_clock;
+  const auto t_call = clk::now();
+  double wait_ms = 0, narrow_ms = 0;
+  size_t pieces = 0;
+  // publishes rows [0, n) as landed, from slot s's pinned flag word
+  auto publish = [&](unsigned long long n, int s) {
+    hs.flag[s] = n;
+    ck(cudaMemcpyAsync(d_ready, &hs.flag[s], sizeof(unsigned long long), cudaMemcpyHostToDevice, hs.copy),
+       "H2D ready");
+  };
+  uint64_t bad = ~0ull;
+  size_t k = 0;
+  try {
+    // ramp up (1/16, 1/8, ... of a slot): the first 16 k-row work block can
+    // start after a short narrow + copy
+    size_t step = std::max<size_t>(1, chunk / 16);
+    for (size_t r0 = 0, n = 0; r0 < rows; r0 += n, ++k, step = std::min(chunk, 2 * step)) {
+      n = std::min(step, rows - r0);
+      const int s = static_cast<int>(k % HostStager::kSlots);
+      const auto t0 = clk::now();
+      ck(cudaEventSynchronize(hs.done[s]), "stage slot wait");  // slot s (and flag[s]) copied out
+      const auto t1 = clk::now();
+      bad = hs.narrow(bins + r0 * F, n, F, B, ldb, s);
+      if (prof) {
+        wait_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+        narrow_ms += std::chrono::duration<double, std::milli>(clk::now() - t1).count();
+        ++pieces;
+      }
+      if (bad != ~0ull) {
+        bad += r0 * F;
+        publish(~0ull, s);  // abort the launch (its output is discarded by the caller)
+        ck(cudaEventRecord(hs.done[s], hs.copy), "cudaEventRecord");
+        return bad;
+      }
+      ck(cudaMemcpyAsync(d_bins + r0 * ldb, hs.slot[s], n * ldb, cudaMemcpyHostToDevice, hs.copy), "H2D bins");
+      publish(r0 + n, s);
+      ck(cudaEventRecord(hs.done[s], hs.copy), "cudaEventRecord");
+    }
+  } catch (...) {
+    // never leave the launch spinning on rows that will not come
+    // (on the non-blocking copy stream: a legacy-stream copy could queue
+    // behind the launch itself)
+    const unsigned long long abort_all = ~0ull;
+    cudaMemcpyAsync(d_ready, &abort_all, sizeof(abort_all), cudaMemcpyHostToDevice, hs.copy);
+    cudaStreamSynchronize(hs.copy);
+    throw;
+  }
+  if (prof) {
+    fprintf(stderr, "[stage] streamed rows %zu pieces %zu chunk %zu threads %zu: host %.2f ms (slot wait %.2f, "
+            "narrow %.2f)\n", rows, pieces, chunk, hs.pool.size() + 1,
+            std::chrono::duration<double, std::milli>(clk::now() - t_call).count(), wait_ms, narrow_ms);
+  }
+  return bad;
 }
 
 void upload_host(hv_context* ctx, const void* src, size_t bytes, void* dst) {

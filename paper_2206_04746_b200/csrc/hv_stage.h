@@ -46,6 +46,11 @@ struct HostStager {
   uint8_t* slot[kSlots] = {};
   cudaEvent_t done[kSlots] = {};  // recorded after the slot's H2D copy
   size_t cap = 0;
+  // streamed mode (encode_host_bins_streamed): copies run on their own stream
+  // and each is followed by an 8-byte copy of the rows-landed count (pinned
+  // flag[s], reused with slot s) into the encoder's `ready` word
+  cudaStream_t copy = nullptr;
+  unsigned long long* flag = nullptr;
 
   HostStager();
   ~HostStager();
@@ -56,6 +61,9 @@ struct HostStager {
 };
 
 unsigned host_thread_count();
+// rows [r0, r1) of F uint32 bins -> uint8 rows of pitch ldb (zero padded), on
+// the calling thread; returns the largest bin seen (hv_narrow.cpp).
+uint32_t narrow_rows(const uint32_t* in, size_t F, size_t r0, size_t r1, uint8_t* out, size_t ldb);
 // rows x F uint32 bins -> uint8 rows of pitch ldb (zero padded) on the pool;
 // returns the first flat index whose bin is >= B, or ~0.
 uint64_t narrow_rows_host(ThreadPool& pool, const uint32_t* in, size_t rows, size_t F, size_t B, uint8_t* out,
@@ -76,6 +84,22 @@ uint64_t encode_host_bins(hv_context* ctx, const uint32_t* bins, size_t rows, si
                           hv_binding binding, const uint32_t* d_id, const uint32_t* d_val, const uint32_t* d_tie,
                           const ChunkOut& out_for, DevBuf<uint8_t>* b8, size_t chunk, size_t& k,
                           const ChunkAfter& after = {}, size_t ldo = 0);
+
+// Streamed variant for the table encoder: ONE persistent encoder launch on
+// `kst` over all rows of d_bins (rows x bins_pitch(F), device, caller-owned,
+// alive until kst has passed the launch) whose work items wait on *d_ready
+// (rows landed so far); the host narrows chunks into the pinned slots and
+// copies them (and the advancing row count) on the stager's copy stream.
+// No per-chunk kernel boundaries (each cost a wave tail: 81 launches of 87 k
+// rows 116.2 ms on two streams vs 113.8 ms in one launch). `launched` is set
+// false, with nothing enqueued, when the table encoder does not apply (the
+// caller then uses encode_host_bins). Returns the first bad flat bin index or
+// ~0; on an error the launch is aborted (ready = ~0: work items not yet
+// started are skipped) and its output is garbage.
+uint64_t encode_host_bins_streamed(hv_context* ctx, const uint32_t* bins, size_t rows, size_t F, size_t B, size_t D,
+                                   const uint32_t* d_id, const uint32_t* d_val, const uint32_t* d_tie,
+                                   uint8_t* d_bins, uint32_t* out, size_t ldo, cudaStream_t kst,
+                                   unsigned long long* d_ready, bool& launched);
 
 // Copies `bytes` of (pageable) host memory to the device on the context
 // stream through the pinned staging ring (host threads fill a slot while the

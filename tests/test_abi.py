@@ -128,6 +128,26 @@ def test_host_narrowing_matches_numpy_and_finds_first_bad_bin():
         if rows:
             np.testing.assert_array_equal(out[:rows, :F], bins.astype(np.uint8))
             assert not out[:rows, F:].any()
+    # vector-path edges (AVX-512 streaming path needs 16-byte aligned rows; the
+    # others take the AVX2 / scalar path): F a multiple of 16, ldb == F,
+    # unaligned output, ldb not a multiple of 16, full 8-bit range
+    for rows, F, B, ldb, off in [(300, 32, 16, 64, 0), (300, 48, 256, 48, 0), (200, 65, 16, 80, 1),
+                                 (200, 65, 16, 70, 0), (50, 17, 256, 32, 0)]:
+        bins = rng.integers(0, B, (rows, F)).astype(np.uint32)
+        buf = np.full(rows * ldb + 64, 0xAB, np.uint8)
+        base = (-buf.ctypes.data) % 64 + off
+        out = buf[base:base + rows * ldb].reshape(rows, ldb)
+        bad = C.c_uint64()
+        N.check(N.lib().hv_host_narrow_bins(bins.ctypes.data, rows, F, B, out.ctypes.data, ldb, C.byref(bad)))
+        assert bad.value == 2**64 - 1
+        np.testing.assert_array_equal(out[:, :F], bins.astype(np.uint8))
+        assert not out[:, F:].any()
+    bins = rng.integers(0, 16, (100, 40)).astype(np.uint32)
+    bins[77, 39] = 0x100  # truncates to 0 in uint8 but must still be reported
+    out = np.zeros((100, 64), np.uint8)
+    bad = C.c_uint64()
+    N.check(N.lib().hv_host_narrow_bins(bins.ctypes.data, 100, 40, 16, out.ctypes.data, 64, C.byref(bad)))
+    assert bad.value == 77 * 40 + 39
     bins = rng.integers(0, 16, (5000, 30)).astype(np.uint32)
     bins[4321, 7] = 16
     bins[4999, 0] = 99
