@@ -111,6 +111,7 @@ struct OnlineParams {
   uint32_t* item_ctr;          // LISTS: dynamic replay-item counter (nullable: static round robin)
   uint32_t ablate;             // timing experiments only (HVB200_ONLINE_ABLATE): bit0 no next-chunk loads,
                                // bit1 no replay loop, bit2 no chunk stores (results are wrong)
+  uint32_t mw;                 // MERGED: words per replay item (4: replay_merged_mw; 8: replay_merged)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* ptr) {
@@ -363,6 +364,7 @@ struct Smem {
   double val[2][kLChunk];
   uint8_t flag[2][kLChunk];  // MERGED: bit0 listed, bit1 true sample; lists: true sample
   uint32_t warpcnt[kLChunk / 32];
+  uint32_t gmask[2][kLChunk / 32];  // MERGED (mw < 8): listed rows of each 32-row group of a chunk
   double weight;
   uint32_t dyn_item;
   uint16_t order[kOrderMax];  // LISTS + dynamic: classes by decreasing list length
@@ -442,6 +444,198 @@ __device__ __forceinline__ void await_class_weight(const OnlineParams& p, uint32
   const unsigned long long t0 = gtimer();
   while (ld_acquire_u32(p.wflag + c) != epoch) {
     if (gtimer() - t0 > 2000000000ull) __trap();  // 2 s: a lost task is a bug, never a hang
+  }
+}
+
+// ------------------------------------------ MERGED replay, narrow items ----
+// Items of MW = 4 words instead of 8, so the dense class's items spread over
+// twice as many SMs, one replay warp per scheduler (a 1,024-row chain runs at
+// ~11 cycles per row alone on its scheduler, ~15.5 with two warps per
+// scheduler: scripts/probe_replay.cu). The CTA's other five warps stage the
+// chunks — raw loads for chunk k+1 issued before chunk k's replay, flags and
+// values (an fp64 division per true sample) formed after it — so the replay
+// warps run nothing but their chains. A 32-row group with no listed row of the
+// item's class is skipped (its adds would all be +0.0): with unbalanced
+// classes (CHB-MIT: 0.3 % positives) the rare class's items replay a few
+// groups; chunks with every group listed take the loop without the tests.
+template <int MW>
+__device__ void replay_merged_mw(const OnlineParams& p, const unsigned long long* bestv, Smem& s, uint64_t b0,
+                                 uint32_t n, uint32_t par) {
+  constexpr uint32_t kRows = kLChunk;  // rows per staged chunk
+  constexpr uint32_t kThr = MW * 32;   // replay threads (warps 0 .. MW-1)
+  constexpr uint32_t kStg = kOThreads - kThr;  // staging threads (the other warps)
+  constexpr int kRowsPer = (kRows + kStg - 1) / kStg;
+  constexpr int kLoads = (kRows * MW + kStg - 1) / kStg;
+  static_assert(kRows + 4 <= kWordPitch && MW <= 8 && kStg % 32 == 0, "staging layout");
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t st = tid - kThr;  // staging thread index (tid >= kThr)
+  const uint32_t nwb = (p.W + MW - 1) / MW;
+  const uint64_t items = static_cast<uint64_t>(p.C) * nwb;
+  const bool sep = p.wflag != nullptr && gridDim.x >= items + p.C;
+  const uint32_t epoch = static_cast<uint32_t>(b0 / p.bsz) + 1u;
+  // the weight tasks take the first C CTAs and the items the next ones: CTAs
+  // past the SM count share an SM with a low-numbered one, and there the rare
+  // class's (short) items cost the co-resident CTA least
+  if (sep && blockIdx.x < p.C) {
+    const uint32_t c = blockIdx.x;
+    class_weight_task<false>(p, s, b0, n, c, p.weight + par * p.C + c, p.weight + (par ^ 1u) * p.C + c, epoch);
+  }
+  const uint32_t first = sep ? p.C : 0u, stride = gridDim.x - first;
+  for (uint64_t item = blockIdx.x - first; blockIdx.x >= first && item < items; item += stride) {
+    const uint32_t c = static_cast<uint32_t>(item / nwb);
+    const uint32_t wb = static_cast<uint32_t>(item % nwb);
+    const uint32_t w = wb * MW + warp, j = w * 32u + lane;
+    const bool col = tid < kThr && w < p.W && j < p.D;
+    double acc = col ? p.acc[static_cast<uint64_t>(c) * p.D + j] : 0.0;
+    double wsum = p.weight[par * p.C + c];
+    uint64_t ntrue = 0;
+    uint32_t mine = 0;  // this thread staged a listed row
+    // staging thread st owns rows st + kStg * i of a chunk and words st + kStg * i
+    bool rok[kRowsPer];
+    int32_t ry[kRowsPer];
+    unsigned long long rb[kRowsPer];
+    uint32_t rt[kRowsPer];
+    uint32_t rw[kLoads];
+    auto load_chunk = [&](uint32_t ch) {  // raw loads only
+#pragma unroll
+      for (int i = 0; i < kRowsPer; ++i) {
+        const uint32_t k = st + kStg * i;
+        rok[i] = k < kRows && ch + k < n;
+        if (rok[i]) {
+          ry[i] = p.labels[b0 + ch + k];
+          rb[i] = bestv[ch + k];
+          rt[i] = p.truep[ch + k];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kLoads; ++i) {
+        const uint32_t e = st + i * kStg;
+        const uint32_t k = e / MW, wl = e % MW;
+        const uint32_t wg = wb * MW + wl;
+        rw[i] = (k < kRows && ch + k < n && wg < p.W) ? __ldg(p.enc + (b0 + ch + k) * p.W + wg) : 0u;
+      }
+    };
+    auto store_chunk = [&](uint32_t buf) {
+#pragma unroll
+      for (int i = 0; i < kRowsPer; ++i) {
+        const uint32_t k = st + kStg * i;
+        uint8_t rf = 0;
+        double rv = 0.0;
+        if (rok[i]) {
+          const bool is_t = ry[i] == static_cast<int32_t>(c);
+          const bool is_p = !is_t && static_cast<uint32_t>(rb[i]) == c;
+          if (is_t) rv = delta_of(rt[i], p.D);
+          if (is_p) rv = penalty_of(rb[i], p.gamma, p.D);
+          rf = (is_t || is_p ? 1 : 0) | (is_t ? 2 : 0);
+        }
+        if (k < kRows) {
+          s.val[buf][k] = rv;
+          s.flag[buf][k] = rf;
+        }
+        mine |= rf & 1u;
+        // rows k of one staging warp and one i are a 32-row group (kStg % 32 == 0)
+        const uint32_t gm = __ballot_sync(kFull, rf & 1u);
+        if (lane == 0 && k < kRows) s.gmask[buf][k >> 5] = gm;
+      }
+#pragma unroll
+      for (int i = 0; i < kLoads; ++i) {
+        const uint32_t e = st + i * kStg;
+        const uint32_t k = e / MW, wl = e % MW;
+        if (k < kRows) s.words[buf][wl * kWordPitch + k] = rw[i];
+      }
+    };
+    const bool pr = p.prof != nullptr && blockIdx.x == first && tid == 0;
+    const unsigned long long q0 = pr ? gtimer() : 0ull;
+    if (tid >= kThr) {
+      load_chunk(0);
+      store_chunk(0);
+    }
+    __syncthreads();
+    const unsigned long long q1 = pr ? gtimer() : 0ull;
+    uint32_t buf = 0;
+    for (uint32_t ch = 0; ch < n; ch += kRows, buf ^= 1u) {
+      const bool more = ch + kRows < n;
+      const uint32_t m = min(kRows, n - ch);
+      if (tid < kThr) {
+        // rows past m were staged as 0 words and +0.0 values: whole groups of 32
+        const uint32_t* wv = s.words[buf] + warp * kWordPitch;
+        const double* val = s.val[buf];
+        const uint32_t ng = (m + 31u) / 32u;
+        auto group = [&](uint32_t g) {
+#pragma unroll
+          for (uint32_t k = g * 32u; k < g * 32u + 32u; k += 4) {
+            const uint4 w4 = *reinterpret_cast<const uint4*>(wv + k);
+            const double2 v01 = *reinterpret_cast<const double2*>(val + k);
+            const double2 v23 = *reinterpret_cast<const double2*>(val + k + 2);
+            acc = __dadd_rn(acc, ((w4.x >> lane) & 1u) ? v01.x : 0.0);
+            acc = __dadd_rn(acc, ((w4.y >> lane) & 1u) ? v01.y : 0.0);
+            acc = __dadd_rn(acc, ((w4.z >> lane) & 1u) ? v23.x : 0.0);
+            acc = __dadd_rn(acc, ((w4.w >> lane) & 1u) ? v23.y : 0.0);
+          }
+        };
+        bool dense = ng == kRows / 32u;
+#pragma unroll
+        for (uint32_t g = 0; g < kRows / 32u; ++g) dense = dense && s.gmask[buf][g] != 0u;
+        if (dense) {
+#pragma unroll 1
+          for (uint32_t g = 0; g < kRows / 32u; g += 2) {  // no tests: 64 rows per iteration
+            group(g);
+            group(g + 1);
+          }
+        } else {
+          for (uint32_t g = 0; g < ng; ++g) {
+            if (s.gmask[buf][g] != 0u) group(g);  // warp-uniform
+          }
+        }
+      } else {
+        if (more && !(p.ablate & 1u)) load_chunk(ch + kRows);
+        if (tid == kOThreads - 32 && !sep) {  // lane 0 of the last warp: the class weight chain
+#pragma unroll 8
+          for (uint32_t k = 0; k < m; ++k) {
+            const uint8_t f = s.flag[buf][k];
+            wsum = __dadd_rn(wsum, (f & 2u) ? s.val[buf][k] : 0.0);
+            ntrue += f >> 1;
+          }
+        }
+        if (more && !(p.ablate & 4u)) store_chunk(buf ^ 1u);  // the other buffer was last read before the previous barrier
+      }
+      __syncthreads();
+    }
+    const unsigned long long q2 = pr ? gtimer() : 0ull;
+    if (tid == kOThreads - 32) {
+      if (sep) {
+        await_class_weight(p, c, epoch);
+        s.weight = p.weight[(par ^ 1u) * p.C + c];
+      } else {
+        s.weight = wsum;
+      }
+    }
+    const int touched = __syncthreads_or(mine);
+    const unsigned long long q3 = pr ? gtimer() : 0ull;
+    if (tid < kThr) {
+      // model.cpp:139-163: accumulators back, touched classes re-binarised
+      if (col) p.acc[static_cast<uint64_t>(c) * p.D + j] = acc;
+      if (touched) {
+        uint32_t bit = 0;
+        if (col) {
+          const double twice = 2.0 * acc, total = s.weight;
+          bit = twice > total ? 1u : (twice < total ? 0u : ((p.tie[w] >> lane) & 1u));
+        }
+        const uint32_t word = __ballot_sync(kFull, bit);
+        if (lane == 0 && w < p.W) p.cv[static_cast<uint64_t>(c) * p.W + w] = word;
+      }
+    }
+    if (pr) {
+      p.prof[3] += q1 - q0;
+      p.prof[4] += q2 - q1;
+      p.prof[5] += q3 - q2;
+      p.prof[6] += gtimer() - q3;
+    }
+    if (!sep && wb == 0 && tid == kOThreads - 32) {
+      p.weight[(par ^ 1u) * p.C + c] = wsum;
+      p.counts[c] += ntrue;
+    }
+    __syncthreads();  // s.weight reuse by the next item
   }
 }
 
@@ -769,7 +963,11 @@ __global__ void __launch_bounds__(kOThreads, 2) online_persistent_kernel(OnlineP
     if (prof) t1 = gtimer();
     t2 = t1;
     if constexpr (MERGED) {
-      replay_merged<COLS>(p, bestv, s, b0, n, par);
+      if (p.mw == 4) {
+        replay_merged_mw<4>(p, bestv, s, b0, n, par);
+      } else {
+        replay_merged<COLS>(p, bestv, s, b0, n, par);
+      }
     } else {
       const uint64_t litems = static_cast<uint64_t>(p.C) * ((p.W + RTile<COLS>::kWords - 1) / RTile<COLS>::kWords);
       const bool sep = p.wflag != nullptr && gridDim.x >= litems + p.C;
@@ -1024,7 +1222,10 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   // long per-class lists (few classes): one chain per thread; short ones: four
   const bool cols4 = !merged && n < 64 * C;
   const bool cols8 = cols4 && n < 16 * C;
-  const uint64_t iw = cols8 ? 64 : cols4 ? 32 : 8;  // words per replay item
+  // MERGED: 4-word items (replay_merged_mw; HVB200_ONLINE_MW=8 restores 8)
+  uint32_t mw = 4;
+  if (const char* e = getenv("HVB200_ONLINE_MW")) mw = atoi(e) == 8 ? 8u : 4u;
+  const uint64_t iw = merged ? mw : cols8 ? 64 : cols4 ? 32 : 8;  // words per replay item
   const uint64_t items = static_cast<uint64_t>(C) * ((W + iw - 1) / iw);
   const uint64_t score_ctas = (n + kOThreads / 32 - 1) / (kOThreads / 32);
   // one extra CTA per class for the separate weight tasks
@@ -1036,7 +1237,7 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   OnlineParams p{enc,     labels,   rows,     static_cast<uint32_t>(D), static_cast<uint32_t>(W),
                  static_cast<uint32_t>(C), n, gamma, tie, acc, wts.ptr, counts, cv, best.ptr, truep.ptr, lidx.ptr,
                  lval.ptr, llen.ptr, nullptr, lane_class ? 1u : 0u, 1u, nullptr, nullptr, nullptr, wtask ? wflag.ptr : nullptr,
-                 nullptr, 0u};
+                 nullptr, 0u, mw};
   DevBuf<uint32_t> item_ctr(merged ? 0 : 1, st);
   if (const char* ab = getenv("HVB200_ONLINE_ABLATE")) p.ablate = static_cast<uint32_t>(atoi(ab));  // timing only
   // HVB200_ONLINE_PROFILE=1: print the time per phase (CTA 0's view, barrier waits included)
@@ -1051,7 +1252,11 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   DevBuf<uint32_t> pscr, arrive;
   unsigned grid_est = 0;
   if (merged) {
-    grid_est = cooperative_grid<true, 1>(ctx, want);
+    // narrow items: at most one CTA per SM. A cooperative grid larger than the
+    // SM count doubles up its lowest-numbered CTAs (blocks 0-11 on six SMs
+    // for 160 CTAs, measured); the few CTAs with two work units get a second
+    // item (with unbalanced classes, usually a rare-class one)
+    grid_est = cooperative_grid<true, 1>(ctx, mw == 4 ? std::min<uint64_t>(want, ctx->sm_count) : want);
   } else if (cols8) {
     grid_est = cooperative_grid<false, 8>(ctx, want);
   } else if (cols4) {
