@@ -381,13 +381,17 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
   const int tb = B <= 16 ? 16 : 32;
   const size_t pair_table = static_cast<size_t>(Fpad) * tb * 8;
   const size_t wstage = 16 * 32 * 4;
-  // Shapes (word pairs per lane, warps per CTA, CTAs per SM), preferred first:
-  // the most pairs whose tables fit (measured at CHB-MIT: 4 or 3 pairs with 8
-  // warps beat 2 pairs with 2 CTAs/SM by 7 %, 1 pair by 22 %).
+  // Shapes (word pairs per lane, warps per CTA, CTAs per SM), preferred first.
+  // Round 2: 12 warps (three per scheduler) with 3 or 2 pairs beat 8 warps
+  // with 4 or 2 pairs by 3.1-3.5 % at every benchmark shape (E 16.43 -> 15.86,
+  // H 27.15 -> 26.30, I 30.24 -> 29.21, M 37.38 -> 36.14 ms per 1 M rows:
+  // profiles/encode_shapes_r2.txt); 10 warps (3+3+2+2 per scheduler) and 16
+  // (128 registers, spills) lose. Round 1: 4 or 3 pairs with 8 warps beat 2
+  // pairs with 2 CTAs/SM by 7 %, 1 pair by 22 %.
   struct Shape { int npr, g, minb; };
   // (32 bins: pair tables are twice as large, so the same list picks fewer
   // pairs; only the {2,8,1} and {1,8,2} shapes are instantiated for it)
-  const Shape shapes[] = {{4, 8, 1}, {3, 8, 1}, {2, 8, 1}, {1, 8, 2}};
+  const Shape shapes[] = {{3, 12, 1}, {2, 12, 1}, {4, 8, 1}, {3, 8, 1}, {2, 8, 1}, {1, 8, 2}};
   constexpr int kShapes = sizeof(shapes) / sizeof(shapes[0]);
   const size_t two = 113 * 1024, one = std::min<size_t>(ctx->smem_optin, 225 * 1024);
   int pick = -1;
@@ -397,7 +401,7 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
   for (int i = 0; i < kShapes; ++i) {
     const Shape& s = shapes[i];
     const size_t need = s.npr * pair_table + s.g * wstage;
-    const bool inst = tb == 16 || s.npr <= 2;
+    const bool inst = (tb == 16 || s.npr <= 2) && (s.g == 8 || tb == 16);
     const bool fits = inst && need <= (s.minb == 2 ? two : one);
     if (forced ? (s.npr == enp && s.g == eg && s.minb == emb && fits) : (fits && pick < 0)) pick = i;
   }
@@ -407,11 +411,14 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
   const uint32_t slices = static_cast<uint32_t>((wcount + 2 * s.npr - 1) / (2 * s.npr));
   // 16k-row blocks (bins of a block stay in L2 while its slices run), smaller
   // when that would leave fewer than ~4 items per CTA (chunked host pipelines)
-  uint32_t block_rows = 16384u;
+  // (a multiple of 32 rows per warp of the CTA, so every warp gets as many
+  // 32-row groups: 16,512 = 43 x 384 for 12 warps)
+  const uint32_t unit = 32u * static_cast<uint32_t>(s.g);
+  uint32_t block_rows = (16384u + unit / 2) / unit * unit;
   const uint64_t want_items = 4ull * ctx->sm_count * s.minb;
   if (((rows + block_rows - 1) / block_rows) * slices < want_items) {
     const uint64_t br = (rows * slices + want_items - 1) / want_items;
-    block_rows = static_cast<uint32_t>(std::max<uint64_t>(256, (br + 255) / 256 * 256));
+    block_rows = static_cast<uint32_t>(std::max<uint64_t>(unit, (br + unit - 1) / unit * unit));
   }
   if (const char* br_env = getenv("HVB200_TT_BLOCK_ROWS")) {  // tuning override: a positive multiple of 32
     const long v = strtol(br_env, nullptr, 10);
@@ -426,6 +433,8 @@ bool launch_v6(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t 
   }
 #define HV_TT6_NH(NPR, G, MB, TB) HV_TT6(NPR, G, MB, 3, TB) HV_TT6(NPR, G, MB, 4, TB) HV_TT6(NPR, G, MB, 6, TB)
   HV_TT6_NH(4, 8, 1, 16)
+  HV_TT6_NH(3, 12, 1, 16)
+  HV_TT6_NH(2, 12, 1, 16)
   HV_TT6_NH(3, 8, 1, 16)
   HV_TT6_NH(2, 8, 1, 16)
   HV_TT6_NH(1, 8, 2, 16)
