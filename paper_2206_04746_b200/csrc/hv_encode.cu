@@ -269,6 +269,16 @@ void encode_device(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, size_
     ldo = W;
   }
   if (w0 + wcount > W || ldo < wcount) invalid("encode: word range outside the row");
+  // the tensor-core encoder (HVB200_ENCODE_TC=1 while it is being evaluated)
+  if (binding == HV_BIND_ID_LEVEL && allow_fast && w0 == 0 && wcount == W) {
+    const char* tc = getenv("HVB200_ENCODE_TC");
+    if (tc && tc[0] == '1' &&
+        launch_tc(ctx, st, bins8, static_cast<uint32_t>(ldb), rows, static_cast<uint32_t>(F), id, val,
+                  static_cast<uint32_t>(B), static_cast<uint32_t>(D), static_cast<uint32_t>(W), tie, out,
+                  static_cast<uint32_t>(ldo))) {
+      return;
+    }
+  }
   if (wcount != W || ldo != W) {
     // a column slice: the fused encoder writes it directly; other bindings
     // encode whole rows into scratch and copy the slice out

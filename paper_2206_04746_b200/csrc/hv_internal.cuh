@@ -186,6 +186,11 @@ void fit_discretizer_device(hv_context* ctx, cudaStream_t st, const double* X, s
                             size_t n, double* mn, double* mx);
 void discretize_rows_device(hv_context* ctx, cudaStream_t st, const double* X, size_t F, const uint64_t* idx,
                             size_t n, const double* mn, const double* mx, size_t B, uint8_t* out, size_t ldb);
+// Tensor-core ID-level encoder (hv_encode_tc.cu): whole rows, B <= 16; false
+// when the shape is not supported (nothing launched).
+bool launch_tc(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
+               const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
+               uint32_t* out, uint32_t ldo);
 bool launch_tt(hv_context* ctx, cudaStream_t st, const uint8_t* bins8, uint32_t ldb, uint64_t rows, uint32_t F,
                const uint32_t* id, const uint32_t* val, uint32_t B, uint32_t D, uint32_t W, const uint32_t* tie,
                uint32_t* out, uint32_t w0, uint32_t wcount, uint32_t ldo, bool perm = false,

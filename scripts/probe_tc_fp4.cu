@@ -17,7 +17,7 @@
 #include <cstdint>
 #include <cstdio>
 
-constexpr int kM = 128, kN = 256;
+constexpr int kM = 128;
 constexpr uint32_t kTmemCols = 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -28,13 +28,14 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
          (static_cast<uint64_t>(sbo >> 4) << 32) | (1ull << 46);
 }
 
-enum Kind { kF8Dense, kF4Dense, kF4Sparse };
+enum Kind { kF8Dense, kF4Dense, kF4Sparse, kF4SparseCommitEach, kF4SparseRing };
 
-template <int KIND>
+template <int KIND, int kN = 256>
 __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long* cyc) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) unsigned long long done;
+  __shared__ __align__(8) unsigned long long ring[8];
   const uint32_t tid = threadIdx.x, warp = tid >> 5;
   // operands: A 128 rows x 64 B, B 256 rows x 64 B (enough for every kind's K step), random bytes
   uint8_t* a = sm;
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long*
   }
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&done)));
+    for (int r = 0; r < 8; ++r) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ring[r])));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("fence.proxy.async.shared::cta;");
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long*
       idesc = (1u << 4) | ((kN >> 3) << 17) | ((kM >> 4) << 24);  // D f32, A/B e4m3, K-major
     } else {
       // block-scaled: A/B e2m1 (MXF4 format 1), scale format ue4m3 (0) for block16, M, N; sparse flag bit 2
-      idesc = (1u << 7) | (1u << 10) | ((kN >> 3) << 17) | ((kM >> 4) << 24) | (KIND == kF4Sparse ? (1u << 2) : 0u);
+      idesc = (1u << 7) | (1u << 10) | ((kN >> 3) << 17) | ((kM >> 4) << 24) | (KIND != kF4Dense ? (1u << 2) : 0u);
     }
     t0 = clock64();
     for (int i = 0; i < iters; ++i) {
@@ -93,6 +95,23 @@ __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long*
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.sp.cta_group::1.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, [%7], %3, [%5], [%6], p;\n\t}\n" ::"r"(d),
             "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb), "r"(meta));
+        if constexpr (KIND == kF4SparseCommitEach) {
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&ring[i & 7]))
+                       : "memory");
+        }
+        if constexpr (KIND == kF4SparseRing) {
+          // a ring of 8 stages: commit to stage i % 8, and before issuing i + 8 wait for its completion
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&ring[i & 7]))
+                       : "memory");
+          if (i >= 7) {
+            const int j = i - 7;  // wait for MMA j (issued 7 ago) before the next issue reuses its stage
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tWAITR_%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                "@!p bra WAITR_%=;\n\t}\n" ::"r"(smem_u32(&ring[j & 7])), "r"((j >> 3) & 1)
+                : "memory");
+          }
+        }
       }
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&done))
@@ -110,12 +129,12 @@ __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long*
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
 }
 
-template <int KIND>
+template <int KIND, int kN = 256>
 void run(const char* name, int sms, int logical_k, int iters = 20000) {
   unsigned long long* cyc;
   cudaMalloc(&cyc, 8);
   const size_t smem = (128 + 256) * 64 + 1024;
-  cudaFuncSetAttribute(tc_rate<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaFuncSetAttribute(tc_rate<KIND, kN>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   float best_ms = 1e30f;
   unsigned long long c = 0;
   for (int rep = 0; rep < 3; ++rep) {
@@ -124,7 +143,7 @@ void run(const char* name, int sms, int logical_k, int iters = 20000) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    tc_rate<KIND><<<sms, 128, smem>>>(iters, cyc);
+    tc_rate<KIND, kN><<<sms, 128, smem>>>(iters, cyc);
     cudaEventRecord(e1);
     cudaError_t err = cudaEventSynchronize(e1);
     if (err != cudaSuccess || cudaGetLastError() != cudaSuccess) {
@@ -139,8 +158,8 @@ void run(const char* name, int sms, int logical_k, int iters = 20000) {
     }
   }
   const double flop = 2.0 * kM * kN * logical_k * static_cast<double>(iters) * sms;
-  printf("%-40s: %.1f cycles per UMMA (M=128 N=256 K=%d), %.0f TFLOP/s dense-equivalent over %d SMs (%.3f ms)\n", name,
-         static_cast<double>(c) / iters, logical_k, flop / (best_ms * 1e-3) / 1e12, sms, best_ms);
+  printf("%-40s: %.1f cycles per UMMA (M=128 N=%d K=%d), %.0f TFLOP/s dense-equivalent over %d SMs (%.3f ms)\n", name,
+         static_cast<double>(c) / iters, kN, logical_k, flop / (best_ms * 1e-3) / 1e12, sms, best_ms);
   cudaFree(cyc);
 }
 
@@ -150,6 +169,12 @@ int main() {
   run<kF8Dense>("kind::f8f6f4 e4m3 dense", sms, 32);
   run<kF4Dense>("kind::mxf4nvf4 e2m1 dense (block16)", sms, 64);
   run<kF4Sparse>("kind::mxf4nvf4 e2m1 2:4 sparse (block16)", sms, 128);
+  run<kF4SparseCommitEach, 192>("sparse N=192, commit after every UMMA", sms, 128);
+  run<kF4SparseRing, 192>("sparse N=192, 8-deep commit/wait ring", sms, 128);
+  run<kF4Sparse, 128>("kind::mxf4nvf4 2:4 sparse N=128", sms, 128);
+  run<kF4Sparse, 176>("kind::mxf4nvf4 2:4 sparse N=176", sms, 128);
+  run<kF4Sparse, 192>("kind::mxf4nvf4 2:4 sparse N=192", sms, 128);
+  run<kF4Sparse, 64>("kind::mxf4nvf4 2:4 sparse N=64", sms, 128);
   // sustained: ~0.5 s per launch (power / clock behaviour of a long encode)
   run<kF4Sparse>("kind::mxf4nvf4 2:4 sparse, 0.5 s launches", sms, 128, 5600000);
   run<kF4Dense>("kind::mxf4nvf4 dense, 0.5 s launches", sms, 64, 7000000);
