@@ -185,15 +185,18 @@ __device__ __forceinline__ void score_rows_all_classes(const OnlineParams& p, un
 
 __device__ void score_warp_per_row(const OnlineParams& p, unsigned long long* best_out, uint64_t b0, uint32_t n,
                                    uint64_t gwarp, uint64_t gwarps, uint32_t lane) {
-  // 3..16 classes, long rows: every class's word of a step in flight together
-  // (per batch of 1,024: UCI-HAR C = 6 19.5 -> 17.9 us, MNIST C = 10 D = 10000
-  // 29.2 -> 27.1 us); two classes keep the per-class passes below (CHB-MIT:
+  // 3..16 classes, long rows whose words do not split evenly over the lanes:
+  // every class's word of a step in flight together (per batch of 1,024:
+  // UCI-HAR C = 6 18.4 -> 16.2 us, MNIST C = 10 D = 10000 29.8 -> 26.7 us);
+  // rows of a multiple of 32 words keep the per-class passes (MNIST D = 8192
+  // 23.4 vs 24.2, D = 16384 33.0 vs 34.9 us), and so do two classes (CHB-MIT:
   // 18.2 vs 20.5 us with this path)
-  if (p.C >= 3 && p.C <= 8 && p.W > 64) {
+  const bool ragged = (p.W & 31u) != 0 && !(p.ablate & 64u);
+  if (p.C >= 3 && p.C <= 8 && p.W > 64 && ragged) {
     score_rows_all_classes<8>(p, best_out, b0, n, gwarp, gwarps, lane);
     return;
   }
-  if (p.C > 8 && p.C <= kWarpC && p.W > 64) {
+  if (p.C > 8 && p.C <= kWarpC && p.W > 64 && ragged) {
     score_rows_all_classes<kWarpC>(p, best_out, b0, n, gwarp, gwarps, lane);
     return;
   }

@@ -7,7 +7,8 @@ usage: HVB200_ONLINE_PROFILE=1 python scripts/online_phases.py H I L E M M20 > p
 import os, sys, torch
 sys.path.insert(0, os.getcwd())
 from paper_2206_04746_b200 import device as dv
-cfgs = {"H": (561, 6, 10000, 200_000, 0), "I": (617, 26, 10000, 100_000, 0), "L": (617, 100, 32768, 60_000, 0), "E": (342, 2, 10000, 200_000, 1), "M": (784, 10, 10000, 100_000, 0), "M20": (784, 10, 20000, 60_000, 0)}
+cfgs = {"H": (561, 6, 10000, 200_000, 0), "I": (617, 26, 10000, 100_000, 0), "L": (617, 100, 32768, 60_000, 0), "E": (342, 2, 10000, 200_000, 1), "M": (784, 10, 10000, 100_000, 0), "M20": (784, 10, 20000, 60_000, 0),
+        "M8k": (784, 10, 8192, 100_000, 0), "M16k": (784, 10, 16384, 60_000, 0)}
 for name in sys.argv[1:]:
     F, C, D, rows, lk = cfgs[name]
     cbk = dv.DeviceCodebook.make(F, 16, D, seed=3)
