@@ -28,7 +28,8 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
          (static_cast<uint64_t>(sbo >> 4) << 32) | (1ull << 46);
 }
 
-enum Kind { kF8Dense, kF4Dense, kF4Sparse, kF4SparseCommitEach, kF4SparseRing };
+enum Kind { kF8Dense, kF4Dense, kF4Sparse, kF4SparseCommitEach, kF4SparseRing, kF4SparseA256, kF4SparseMetaCycle,
+            kF4SparseRing16, kF4SparseRing30 };
 
 template <int KIND, int kN = 256>
 __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long* cyc) {
@@ -36,6 +37,7 @@ __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long*
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) unsigned long long done;
   __shared__ __align__(8) unsigned long long ring[8];
+  __shared__ __align__(8) unsigned long long ring2[32];
   const uint32_t tid = threadIdx.x, warp = tid >> 5;
   // operands: A 128 rows x 64 B, B 256 rows x 64 B (enough for every kind's K step), random bytes
   uint8_t* a = sm;
@@ -54,6 +56,7 @@ __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long*
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&done)));
     for (int r = 0; r < 8; ++r) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ring[r])));
+    for (int r = 0; r < 32; ++r) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ring2[r])));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("fence.proxy.async.shared::cta;");
@@ -64,12 +67,13 @@ __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long*
   unsigned long long t0 = 0, t1 = 0;
   if (tid == 0) {
     // 8-row core matrices 16 B wide: LBO = next core matrix along K (8 rows x 16 B = 128 B), SBO = next 8 rows
-    const uint64_t da = make_desc(smem_u32(a), 128, 64 * 8);
+    // the encoder's compressed A: 32 bytes per row, 8-row core-matrix groups 256 bytes apart
+    const uint64_t da = KIND == kF4SparseA256 ? make_desc(smem_u32(a), 128, 256) : make_desc(smem_u32(a), 128, 64 * 8);
     const uint64_t db = make_desc(smem_u32(b), 128, 64 * 8);
     const uint32_t d = tmem;               // accumulator: columns [0, 256)
     const uint32_t sfa = tmem + 256;       // scale factors / sparse metadata (contents arbitrary)
     const uint32_t sfb = tmem + 320;
-    const uint32_t meta = tmem + 384;
+    const uint32_t meta = KIND == kF4SparseMetaCycle ? tmem + 416 - 86 + 0 : tmem + 384;
     uint32_t idesc;
     if constexpr (KIND == kF8Dense) {
       idesc = (1u << 4) | ((kN >> 3) << 17) | ((kM >> 4) << 24);  // D f32, A/B e4m3, K-major
@@ -94,10 +98,24 @@ __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long*
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.sp.cta_group::1.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, [%7], %3, [%5], [%6], p;\n\t}\n" ::"r"(d),
-            "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb), "r"(meta));
+            "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb),
+            "r"(KIND == kF4SparseMetaCycle ? meta + 2u * static_cast<uint32_t>(i % 43) : meta));
         if constexpr (KIND == kF4SparseCommitEach) {
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&ring[i & 7]))
                        : "memory");
+        }
+        if constexpr (KIND == kF4SparseRing16 || KIND == kF4SparseRing30) {
+          constexpr int R = KIND == kF4SparseRing16 ? 16 : 30;
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&ring2[i % R]))
+                       : "memory");
+          if (i >= R - 1) {
+            const int j = i - (R - 1);
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tWAITQ_%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                "@!p bra WAITQ_%=;\n\t}\n" ::"r"(smem_u32(&ring2[j % R])), "r"((j / R) & 1)
+                : "memory");
+          }
         }
         if constexpr (KIND == kF4SparseRing) {
           // a ring of 8 stages: commit to stage i % 8, and before issuing i + 8 wait for its completion
@@ -169,6 +187,10 @@ int main() {
   run<kF8Dense>("kind::f8f6f4 e4m3 dense", sms, 32);
   run<kF4Dense>("kind::mxf4nvf4 e2m1 dense (block16)", sms, 64);
   run<kF4Sparse>("kind::mxf4nvf4 e2m1 2:4 sparse (block16)", sms, 128);
+  run<kF4SparseA256, 192>("sparse N=192, A layout SBO 256 (encoder)", sms, 128);
+  run<kF4SparseMetaCycle, 192>("sparse N=192, metadata column per K step", sms, 128);
+  run<kF4SparseRing16, 192>("sparse N=192, 16-deep commit/wait ring", sms, 128);
+  run<kF4SparseRing30, 192>("sparse N=192, 30-deep commit/wait ring", sms, 128);
   run<kF4SparseCommitEach, 192>("sparse N=192, commit after every UMMA", sms, 128);
   run<kF4SparseRing, 192>("sparse N=192, 8-deep commit/wait ring", sms, 128);
   run<kF4Sparse, 128>("kind::mxf4nvf4 2:4 sparse N=128", sms, 128);
