@@ -29,7 +29,7 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 enum Kind { kF8Dense, kF4Dense, kF4Sparse, kF4SparseCommitEach, kF4SparseRing, kF4SparseA256, kF4SparseMetaCycle,
-            kF4SparseRing16, kF4SparseRing30 };
+            kF4SparseRing16, kF4SparseRing30, kF4SparseValid, kF4SparseStages };
 
 template <int KIND, int kN = 256>
 __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long* cyc) {
@@ -41,8 +41,9 @@ __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long*
   const uint32_t tid = threadIdx.x, warp = tid >> 5;
   // operands: A 128 rows x 64 B, B 256 rows x 64 B (enough for every kind's K step), random bytes
   uint8_t* a = sm;
-  uint8_t* b = sm + 128 * 64;
-  for (uint32_t i = tid; i < (128 + 256) * 64; i += blockDim.x) {
+  uint8_t* b = sm + (KIND == kF4SparseStages ? 4096 : 128 * 64);  // stages: A 4 KB + B 12 KB per 16 KB
+  const uint32_t nbytes = KIND == kF4SparseStages ? 8u * 16384u : (128u + 256u) * 64u;
+  for (uint32_t i = tid; i < nbytes; i += blockDim.x) {
     uint32_t x = (i + 1) * 0x9E3779B9u;
     x ^= x >> 13;
     // e2m1 nibbles 0 or 1.0 (0x2), e4m3 bytes 0 or 0x08: a 0/1 pattern like the encoder's
@@ -64,6 +65,20 @@ __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long*
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
+  if (KIND == kF4SparseValid || KIND == kF4Dense) {
+    // valid operands: scale factors 1.0 (ue4m3 0x38) over columns 256..383, metadata (idx0, idx1) = (0, 1)
+    const uint32_t lb = (warp * 32u) << 16;
+    for (uint32_t c = 256; c < 384; c += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(tmem + lb + c),
+                   "r"(0x38383838u));
+    for (uint32_t c = 384; c < 512; c += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(tmem + lb + c),
+                   "r"(0x44444444u));
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
   unsigned long long t0 = 0, t1 = 0;
   if (tid == 0) {
     // 8-row core matrices 16 B wide: LBO = next core matrix along K (8 rows x 16 B = 128 B), SBO = next 8 rows
@@ -95,10 +110,12 @@ __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long*
             "tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, %3, [%5], [%6], p;\n\t}\n" ::"r"(d),
             "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb));
       } else {
+        // kF4SparseStages: operands from 8 different 16 KB stages in turn (A 4 KB + B 12 KB), as a pipeline reads them
+        const uint64_t so = KIND == kF4SparseStages ? static_cast<uint64_t>((i & 7) * 16384 >> 4) : 0ull;
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.sp.cta_group::1.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, [%7], %3, [%5], [%6], p;\n\t}\n" ::"r"(d),
-            "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb),
+            "l"(da + so), "l"(db + so), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb),
             "r"(KIND == kF4SparseMetaCycle ? meta + 2u * static_cast<uint32_t>(i % 43) : meta));
         if constexpr (KIND == kF4SparseCommitEach) {
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&ring[i & 7]))
@@ -151,7 +168,7 @@ template <int KIND, int kN = 256>
 void run(const char* name, int sms, int logical_k, int iters = 20000) {
   unsigned long long* cyc;
   cudaMalloc(&cyc, 8);
-  const size_t smem = (128 + 256) * 64 + 1024;
+  const size_t smem = (KIND == kF4SparseStages ? 8 * 16384 : (128 + 256) * 64) + 1024;
   cudaFuncSetAttribute(tc_rate<KIND, kN>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   float best_ms = 1e30f;
   unsigned long long c = 0;
@@ -189,6 +206,9 @@ int main() {
   run<kF4Sparse>("kind::mxf4nvf4 e2m1 2:4 sparse (block16)", sms, 128);
   run<kF4SparseA256, 192>("sparse N=192, A layout SBO 256 (encoder)", sms, 128);
   run<kF4SparseMetaCycle, 192>("sparse N=192, metadata column per K step", sms, 128);
+  run<kF4SparseValid, 192>("sparse N=192, valid SF (1.0) + metadata", sms, 128);
+  run<kF4SparseStages, 192>("sparse N=192, 8 rotating operand stages", sms, 128);
+  run<kF4SparseValid, 256>("sparse N=256, valid SF (1.0) + metadata", sms, 128);
   run<kF4SparseRing16, 192>("sparse N=192, 16-deep commit/wait ring", sms, 128);
   run<kF4SparseRing30, 192>("sparse N=192, 30-deep commit/wait ring", sms, 128);
   run<kF4SparseCommitEach, 192>("sparse N=192, commit after every UMMA", sms, 128);
