@@ -33,16 +33,17 @@
 //
 // STATUS: a correct prototype, opt-in (HVB200_ENCODE_TC=1), bit-exact against
 // the table encoder on every shape tested (tests/test_gpu_encode_tc.py), but
-// SLOWER than it: 25.9 vs 16.0 ms per 1 M CHB-MIT rows. CTA 0's MMA thread
-// (HVB200_TC_PROF=1) spends ~200 cycles issuing each UMMA and ~200 waiting for
-// its stage, against 128 for the UMMA alone: every UMMA needs a fresh 16 KB
-// stage (4 KB A + 12 KB B), so the bulk-copy writes share shared-memory
-// bandwidth with the UMMA's operand reads, and a stage is only refilled
-// after its UMMA completes (~1.8 k cycles after issue, measured) plus an L2
-// round trip. Beating the ALU encoder needs B reused across M tiles (two
-// M tiles per stage, or cta_group::2 with M = 256), which the TMEM budget
-// (accumulators + scale factors + per-K-step metadata in 512 columns) does
-// not allow in this layout. DESIGN.md §8.
+// SLOWER than it: 23.8 vs 15.9 ms per 1 M CHB-MIT rows (19.8 with no bulk
+// copies and no epilogue). The probe's UMMA rates are exactly the operand
+// bytes over 128 B/clk of shared-memory read: N = 128 / 192 / 256 read 4 KB of
+// A + N x 64 B of B = 12 / 16 / 20 KB in 96 / 128 / 160 cycles. So the sparse
+// FP4 UMMA at these shapes is shared-memory bound, not tensor bound, and with
+// a fresh 16 KB stage per UMMA the bulk-copy writes double that traffic:
+// 256 cycles per UMMA = 16.2 ms per 1 M rows, the ALU encoder's time, before
+// any other loss. One mbarrier wait per two stages (28.2 ms) and relaxed
+// waits (23.8) did not help. Only halving the staged bytes per FLOP can beat
+// the ALU path: cta_group::2 (M = 256, B split across the SM pair: 12 KB read
+// + 12 KB written per SM per 128 x 256 block, ~9 ms floor). DESIGN.md §8.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -341,31 +342,41 @@ __global__ void __launch_bounds__(kThreads, 1) encode_tc_kernel(TcParams p) {
           const uint32_t idesc = (1u << 2) | (1u << 7) | (1u << 10) | ((kTN >> 3) << 17) | ((kTM >> 4) << 24);
           // stage descriptors: the start-address field (bits 0-13, 16-byte units) advances by the stage size
           const uint64_t da0 = make_desc(su32(a_s), 128, 256), db0 = make_desc(su32(b_s), 128, 512);
-          const uint32_t meta0 = tmem + kColMeta, dacc = tmem + ab * kTN;
+          const uint32_t dacc = tmem + ab * kTN, sfa = tmem + kColSfa, sfb = tmem + kColSfb;
+          uint32_t meta = tmem + kColMeta;
           uint32_t s = it % kStages, ph = (it / kStages) & 1u;
+          uint64_t da = da0 + s * (kAStage >> 4), db = db0 + s * (kBStage >> 4);
+          uint32_t fb = su32(&full[s]), eb = su32(&empty[s]);
+          // one asm block per K step: wait for the stage, issue, commit the stage back to the loader
+          // (no tcgen05 fence per step: the stage's data arrives through the async proxy; the TMEM
+          // metadata was ordered once, after the a_ready wait)
           for (uint32_t ks = 0; ks < p.ksteps; ++ks) {
-            // (no tcgen05 fence per step: the stage's data arrives through the async
-            // proxy; the TMEM metadata was ordered once, after the a_ready wait)
-            mbar_wait(su32(&full[s]), ph);
-            if (pf) { const long long c1 = clock64(); p.prof[1] += c1 - c0; c0 = c1; }
-            const uint64_t da = da0 + s * (kAStage >> 4);
-            const uint64_t db = db0 + s * (kBStage >> 4);
             const uint32_t acc = ks > 0 ? 1u : 0u;
             asm volatile(
-                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "{\n\t.reg .pred p, q;\n\tWAIT_%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%8], %9;\n\t@!p bra WAIT_%=;\n\t"
+                "setp.ne.b32 q, %4, 0;\n\t"
                 "tcgen05.mma.sp.cta_group::1.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, [%7], %3, [%5], [%6], "
-                "p;\n\t}\n" ::"r"(dacc),
-                "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(tmem + kColSfa), "r"(tmem + kColSfb),
-                "r"(meta0 + 2 * ks));
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             su32(&empty[s]))
-                         : "memory");
-            if (pf) { const long long c1 = clock64(); p.prof[4] += c1 - c0; c0 = c1; }
+                "q;\n\t"
+                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t}\n" ::"r"(dacc),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(sfa), "r"(sfb), "r"(meta), "r"(fb), "r"(ph), "r"(eb)
+                : "memory");
+            meta += 2u;
             if (++s == static_cast<uint32_t>(kStages)) {
               s = 0;
               ph ^= 1u;
+              da = da0;
+              db = db0;
+              fb = su32(&full[0]);
+              eb = su32(&empty[0]);
+            } else {
+              da += kAStage >> 4;
+              db += kBStage >> 4;
+              fb += 8u;
+              eb += 8u;
             }
           }
+          if (pf) { const long long c1 = clock64(); p.prof[4] += c1 - c0; c0 = c1; }
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                            su32(&acc_full[ab]))
                        : "memory");

@@ -29,7 +29,7 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 enum Kind { kF8Dense, kF4Dense, kF4Sparse, kF4SparseCommitEach, kF4SparseRing, kF4SparseA256, kF4SparseMetaCycle,
-            kF4SparseRing16, kF4SparseRing30, kF4SparseValid, kF4SparseStages };
+            kF4SparseRing16, kF4SparseRing30, kF4SparseValid, kF4SparseStages, kF4SparseSpinners, kF4SparseD192 };
 
 template <int KIND, int kN = 256>
 __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long* cyc) {
@@ -80,12 +80,20 @@ __global__ void __launch_bounds__(128, 1) tc_rate(int iters, unsigned long long*
     asm volatile("tcgen05.fence::after_thread_sync;");
   }
   unsigned long long t0 = 0, t1 = 0;
+  if (KIND == kF4SparseSpinners && warp >= 1) {
+    // three warps polling the completion barrier with try_wait while thread 0 issues
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tSPIN_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra SPIN_%=;\n\t}\n" ::"r"(smem_u32(&done))
+        : "memory");
+  }
   if (tid == 0) {
     // 8-row core matrices 16 B wide: LBO = next core matrix along K (8 rows x 16 B = 128 B), SBO = next 8 rows
     // the encoder's compressed A: 32 bytes per row, 8-row core-matrix groups 256 bytes apart
     const uint64_t da = KIND == kF4SparseA256 ? make_desc(smem_u32(a), 128, 256) : make_desc(smem_u32(a), 128, 64 * 8);
     const uint64_t db = make_desc(smem_u32(b), 128, 64 * 8);
-    const uint32_t d = tmem;               // accumulator: columns [0, 256)
+    const uint32_t d = KIND == kF4SparseD192 ? tmem + 192 : tmem;  // accumulator: columns [0, 256) (or from 192)
     const uint32_t sfa = tmem + 256;       // scale factors / sparse metadata (contents arbitrary)
     const uint32_t sfb = tmem + 320;
     const uint32_t meta = KIND == kF4SparseMetaCycle ? tmem + 416 - 86 + 0 : tmem + 384;
@@ -208,6 +216,8 @@ int main() {
   run<kF4SparseMetaCycle, 192>("sparse N=192, metadata column per K step", sms, 128);
   run<kF4SparseValid, 192>("sparse N=192, valid SF (1.0) + metadata", sms, 128);
   run<kF4SparseStages, 192>("sparse N=192, 8 rotating operand stages", sms, 128);
+  run<kF4SparseSpinners, 192>("sparse N=192, 3 warps polling an mbarrier", sms, 128);
+  run<kF4SparseD192, 192>("sparse N=192, accumulator at TMEM column 192", sms, 128);
   run<kF4SparseValid, 256>("sparse N=256, valid SF (1.0) + metadata", sms, 128);
   run<kF4SparseRing16, 192>("sparse N=192, 16-deep commit/wait ring", sms, 128);
   run<kF4SparseRing30, 192>("sparse N=192, 30-deep commit/wait ring", sms, 128);
