@@ -15,7 +15,7 @@
 constexpr int kRows = 1024;
 constexpr int kPitch = kRows + 4;
 
-enum Form { kSelect, kFma, kAndMask, kUncond, kSelect2, kTwoCols, kGroups };
+enum Form { kSelect, kFma, kAndMask, kUncond, kSelect2, kTwoCols, kGroups, kMaskWalk, kMaskWalk4, kMaskWalkLow, kMaskWalkDB };
 
 template <int FORM>
 __global__ void replay(int iters, const uint32_t* __restrict__ gw, const double* __restrict__ gv, double* out,
@@ -30,9 +30,148 @@ __global__ void replay(int iters, const uint32_t* __restrict__ gw, const double*
   const uint32_t lane = threadIdx.x & 31u, ww = threadIdx.x >> 5;
   const uint32_t* wv = words + ww * kPitch;
   double acc = 0.0;
+  // kMaskWalk: each lane's 32-row masks (bit 31 - r = row r of the window has
+  // this lane's bit set), built by a shuffle transpose of the window's words;
+  // stored in place of the words (the walk reads only the masks)
+  uint32_t* tmask = words + 8 * kPitch + 2 * kRows + 64;  // past the values (+ one 0.0 sentinel)
+  if constexpr (FORM == kMaskWalk || FORM == kMaskWalk4 || FORM == kMaskWalkLow || FORM == kMaskWalkDB) {
+    for (uint32_t g = 0; g < kRows / 32; ++g) {
+      // kMaskWalk(4): row 31 - lane, rows reversed so clz gives the next row; kMaskWalkLow: natural order
+      uint32_t x = wv[g * 32 + (FORM == kMaskWalkLow || FORM == kMaskWalkDB ? lane : 31 - lane)];
+#pragma unroll
+      for (uint32_t st = 16; st >= 1; st >>= 1) {
+        const uint32_t m = st == 16 ? 0x0000FFFFu : st == 8 ? 0x00FF00FFu : st == 4 ? 0x0F0F0F0Fu
+                         : st == 2 ? 0x33333333u : 0x55555555u;
+        const bool lo = (lane & st) == 0;
+        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, st);
+        const uint32_t t = __funnelshift_l(y, y, lo ? st : 32 - st);
+        const uint32_t km = lo ? m : ~m;
+        x = (x & km) | (t & ~km);
+      }
+      tmask[(ww * (kRows / 32) + g) * 32 + lane] = x;
+    }
+    if (threadIdx.x == 0) val[kRows] = 0.0;
+    __syncthreads();
+  }
+  // kMaskWalkDB: values permuted so the de Bruijn hash of a row's lowest-bit
+  // word indexes it directly: vdb[g * 32 + ((1 << r) * 0x077CB531 >> 27)] = val[g * 32 + r]
+  double* vdb = reinterpret_cast<double*>(tmask + 8 * kRows + 64);
+  if constexpr (FORM == kMaskWalkDB) {
+    for (int i = threadIdx.x; i < kRows; i += blockDim.x) vdb[(i & ~31) + (((1u << (i & 31)) * 0x077CB531u) >> 27)] = val[i];
+    if (threadIdx.x == 0) vdb[kRows] = 0.0;
+    __syncthreads();
+  }
   const long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
-    if constexpr (FORM == kGroups) {
+    if constexpr (FORM == kMaskWalkDB) {
+      // full-rate ALU only: lb = lowest set bit, its de Bruijn hash indexes the
+      // permuted values; an empty mask reads the 0.0 sentinel
+      const uint32_t* tm = tmask + ww * (kRows / 32) * 32 + lane;
+      for (uint32_t g = 0; g < kRows / 32; ++g) {
+        uint32_t m = tm[g * 32];
+        const uint32_t nb = (__reduce_max_sync(0xFFFFFFFFu, __popc(m)) + 3u) / 4u;
+        const double* vg = vdb + g * 32;
+        auto pop = [&]() -> double {
+          const uint32_t t = m - 1u;
+          const uint32_t lb = m & ~t;
+          m &= t;
+          const double* a = lb ? vg + ((lb * 0x077CB531u) >> 27) : vdb + kRows;
+          return *a;
+        };
+        double n0 = pop(), n1 = pop(), n2 = pop(), n3 = pop();
+#pragma unroll 1
+        for (uint32_t b = 0; b < nb; ++b) {
+          const double v0 = n0, v1 = n1, v2 = n2, v3 = n3;
+          n0 = pop();
+          n1 = pop();
+          n2 = pop();
+          n3 = pop();
+          acc = __dadd_rn(acc, v0);
+          acc = __dadd_rn(acc, v1);
+          acc = __dadd_rn(acc, v2);
+          acc = __dadd_rn(acc, v3);
+        }
+      }
+    } else if constexpr (FORM == kMaskWalkLow) {
+      // natural order: the loop-carried chain is m &= m - 1 (two ALU ops); the
+      // index (ffs) hangs off it
+      const uint32_t* tm = tmask + ww * (kRows / 32) * 32 + lane;
+      for (uint32_t g = 0; g < kRows / 32; ++g) {
+        uint32_t m = tm[g * 32];
+        const uint32_t nb = (__reduce_max_sync(0xFFFFFFFFu, __popc(m)) + 3u) / 4u;
+        const uint32_t base = g * 32;
+        auto pop = [&]() -> double {
+          const uint32_t idx = m ? base + __ffs(m) - 1u : kRows;
+          m &= m - 1u;
+          return val[idx];
+        };
+        // two blocks of 4 in flight: the values added in block b were loaded
+        // during block b - 2 (extra pops past the list read the 0.0 sentinel)
+        double n0 = pop(), n1 = pop(), n2 = pop(), n3 = pop();
+        double q0 = pop(), q1 = pop(), q2 = pop(), q3 = pop();
+#pragma unroll 1
+        for (uint32_t b = 0; b < nb; ++b) {
+          const double v0 = n0, v1 = n1, v2 = n2, v3 = n3;
+          n0 = q0;
+          n1 = q1;
+          n2 = q2;
+          n3 = q3;
+          q0 = pop();
+          q1 = pop();
+          q2 = pop();
+          q3 = pop();
+          acc = __dadd_rn(acc, v0);
+          acc = __dadd_rn(acc, v1);
+          acc = __dadd_rn(acc, v2);
+          acc = __dadd_rn(acc, v3);
+        }
+      }
+    } else if constexpr (FORM == kMaskWalk4) {
+      // the walk in blocks of 4 pops (past the list: the 0.0 sentinel), the
+      // next block's values loaded before this block's adds
+      const uint32_t* tm = tmask + ww * (kRows / 32) * 32 + lane;
+      for (uint32_t g = 0; g < kRows / 32; ++g) {
+        uint32_t m = tm[g * 32];
+        const uint32_t nb = (__reduce_max_sync(0xFFFFFFFFu, __popc(m)) + 3u) / 4u;
+        const uint32_t base = g * 32;
+        auto pop = [&]() -> double {
+          const uint32_t r = __clz(m);
+          const uint32_t idx = m ? base + r : kRows;
+          m &= __funnelshift_rc(0x7FFFFFFFu, 0u, r);
+          return val[idx];
+        };
+        double n0 = pop(), n1 = pop(), n2 = pop(), n3 = pop();
+#pragma unroll 1
+        for (uint32_t b = 0; b < nb; ++b) {
+          const double v0 = n0, v1 = n1, v2 = n2, v3 = n3;
+          if (b + 1 < nb) {
+            n0 = pop();
+            n1 = pop();
+            n2 = pop();
+            n3 = pop();
+          }
+          acc = __dadd_rn(acc, v0);
+          acc = __dadd_rn(acc, v1);
+          acc = __dadd_rn(acc, v2);
+          acc = __dadd_rn(acc, v3);
+        }
+      }
+    } else if constexpr (FORM == kMaskWalk) {
+      // only the rows whose bit is set: per 32-row window, the warp's longest list
+      const uint32_t* tm = tmask + ww * (kRows / 32) * 32 + lane;
+      for (uint32_t g = 0; g < kRows / 32; ++g) {
+        uint32_t m = tm[g * 32];
+        const uint32_t cnt = __reduce_max_sync(0xFFFFFFFFu, __popc(m));
+        const uint32_t base = g * 32;
+#pragma unroll 4
+        for (uint32_t i = 0; i < cnt; ++i) {
+          const uint32_t r = __clz(m);
+          const uint32_t idx = m ? base + r : kRows;
+          m &= __funnelshift_rc(0x7FFFFFFFu, 0u, r);
+          acc = __dadd_rn(acc, val[idx]);
+        }
+      }
+    } else if constexpr (FORM == kGroups) {
       // the product's loop shape: 32-row groups, each skipped when its listed
       // mask (shared memory) is zero; every group listed here
       const uint32_t* gmask = words + 7 * kPitch;  // nonzero words
@@ -126,7 +265,7 @@ __global__ void replay(int iters, const uint32_t* __restrict__ gw, const double*
 template <int FORM>
 void run(const char* name, int sms, const uint32_t* w, const double* v, double* out, long long* cyc) {
   const int iters = 20;
-  const size_t smem = 8 * kPitch * 4 + kRows * 8;
+  const size_t smem = 8 * kPitch * 4 + kRows * 8 + 64 * 4 + 8 * kRows * 4 + 64 * 4 + kRows * 8 + 64;
   cudaFuncSetAttribute(replay<FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   for (int warps : {2, 3, 4, 5, 6, 8}) {
     cudaMemset(cyc, 0, 8);
@@ -137,7 +276,11 @@ void run(const char* name, int sms, const uint32_t* w, const double* v, double* 
       printf("%s: %s\n", name, cudaGetErrorString(e));
       return;
     }
-    printf("%-34s %d warps/SM: %6.2f cycles per row\n", name, warps, c / (double(iters) * kRows));
+    static double h[256];
+    cudaMemcpy(h, out, sizeof h, cudaMemcpyDeviceToHost);
+    unsigned long long hs = 0;
+    for (int i = 0; i < 32 * warps && i < 256; ++i) hs = hs * 1000003ull ^ reinterpret_cast<unsigned long long&>(h[i]);
+    printf("%-34s %d warps/SM: %6.2f cycles per row (result hash %016llx)\n", name, warps, c / (double(iters) * kRows), hs);
   }
 }
 
@@ -227,6 +370,10 @@ int main() {
     printf("product structure (288-thread CTA, 4 replay warps, 256-row chunks + barriers), 79 replay CTAs + %d CTAs "
            "polling a global word: %6.2f cycles per row\n", spin, c / (20.0 * 1024));
   }
+  run<kMaskWalkDB>("mask walk, de Bruijn index (ALU only)", sms, w, v, out, cyc);
+  run<kMaskWalkLow>("mask walk, m &= m - 1, pipelined", sms, w, v, out, cyc);
+  run<kMaskWalk4>("mask walk, 4-pop blocks pipelined", sms, w, v, out, cyc);
+  run<kMaskWalk>("mask walk (set bits only, per lane)", sms, w, v, out, cyc);
   run<kSelect>("select (product form)", sms, w, v, out, cyc);
   run<kGroups>("select, 32-row groups with skip test", sms, w, v, out, cyc);
   run<kSelect2>("select, addends one group ahead", sms, w, v, out, cyc);
