@@ -452,6 +452,9 @@ __device__ void class_weight_task(const OnlineParams& p, Smem& s, uint64_t b0, u
       }
       s.val[buf][k] = v;
       s.flag[buf][k] = is_t ? 1 : 0;
+      // warps 1-8 cover one 32-entry group each (kLChunk = 256)
+      const uint32_t gm = __ballot_sync(kFull, is_t);
+      if ((tid & 31u) == 0) s.gmask[buf][k >> 5] = gm;
     }
   };
   fill(0, 0);
@@ -461,23 +464,32 @@ __device__ void class_weight_task(const OnlineParams& p, Smem& s, uint64_t b0, u
     if (ch + kLChunk < n) fill(ch + kLChunk, buf ^ 1u);
     if (tid == 0) {
       const uint32_t m = min(static_cast<uint32_t>(kLChunk), n - ch);
-      // four entries per step (two LDS.128 of values, one LDS of four flag
-      // bytes), 32 in flight per unrolled iteration: only the adds are serial
-      const uint32_t m4 = m & ~3u;
-#pragma unroll 8
-      for (uint32_t k = 0; k < m4; k += 4) {
-        const double2 v01 = *reinterpret_cast<const double2*>(&s.val[buf][k]);
-        const double2 v23 = *reinterpret_cast<const double2*>(&s.val[buf][k + 2]);
-        const uint32_t f4 = *reinterpret_cast<const uint32_t*>(&s.flag[buf][k]);
-        wsum = __dadd_rn(wsum, v01.x);
-        wsum = __dadd_rn(wsum, v01.y);
-        wsum = __dadd_rn(wsum, v23.x);
-        wsum = __dadd_rn(wsum, v23.y);
-        ntrue += (f4 * 0x01010101u) >> 24;  // the four 0/1 flag bytes
-      }
-      for (uint32_t k = m4; k < m; ++k) {
-        wsum = __dadd_rn(wsum, s.val[buf][k]);
-        ntrue += s.flag[buf][k];
+      // per 32-entry group of true samples: none → skipped; a few → only their
+      // adds (model.cpp adds δ for true samples only; the other entries are
+      // +0.0); many → all 32, four per step (two LDS.128), 32 in flight, only
+      // the adds serial. A rare class's weight chain is then a few adds
+      // instead of a whole batch of +0.0 adds on its items' critical path.
+      for (uint32_t g = 0; g * 32u < m; ++g) {
+        uint32_t gm = s.gmask[buf][g];
+        if (gm == 0u) continue;
+        const double* vg = &s.val[buf][g * 32u];
+        ntrue += __popc(gm);
+        if (__popc(gm) > 8 && !(p.ablate & 256u)) {
+#pragma unroll
+          for (uint32_t k = 0; k < 32u; k += 4) {
+            const double2 v01 = *reinterpret_cast<const double2*>(vg + k);
+            const double2 v23 = *reinterpret_cast<const double2*>(vg + k + 2);
+            wsum = __dadd_rn(wsum, v01.x);
+            wsum = __dadd_rn(wsum, v01.y);
+            wsum = __dadd_rn(wsum, v23.x);
+            wsum = __dadd_rn(wsum, v23.y);
+          }
+        } else {
+          while (gm != 0u) {
+            wsum = __dadd_rn(wsum, vg[__ffs(gm) - 1]);
+            gm &= gm - 1u;
+          }
+        }
       }
     }
     __syncthreads();
@@ -534,17 +546,34 @@ __device__ void replay_merged_mw(const OnlineParams& p, const unsigned long long
   const uint32_t st = tid - kThr;  // staging thread index (tid >= kThr)
   const uint32_t nwb = (p.W + MW - 1) / MW;
   const uint64_t items = static_cast<uint64_t>(p.C) * nwb;
-  const bool sep = p.wflag != nullptr && gridDim.x >= items + p.C;
+  // separate weight tasks when every item has a CTA, or when the items past
+  // the item CTAs are handed out dynamically
+  const bool sep = p.wflag != nullptr && (gridDim.x >= items + p.C || (p.item_ctr != nullptr && gridDim.x > p.C));
   const uint32_t epoch = static_cast<uint32_t>(b0 / p.bsz) + 1u;
-  // the weight tasks take the first C CTAs and the items the next ones: CTAs
-  // past the SM count share an SM with a low-numbered one, and there the rare
-  // class's (short) items cost the co-resident CTA least
   if (sep && blockIdx.x < p.C) {
     const uint32_t c = blockIdx.x;
     class_weight_task<false>(p, s, b0, n, c, p.weight + par * p.C + c, p.weight + (par ^ 1u) * p.C + c, epoch);
   }
   const uint32_t first = sep ? p.C : 0u, stride = gridDim.x - first;
-  for (uint64_t item = blockIdx.x - first; blockIdx.x >= first && item < items; item += stride) {
+  // one CTA per SM (a second CTA on an SM halves both replays' rate): item
+  // CTA k takes item k, and the items past the item CTAs go to whichever CTAs
+  // finish first — with unbalanced classes the rare class's short items. Every
+  // item CTA draws until it draws past the end, so the counter advances by
+  // max(items, stride) per batch and batch bi's draws start at bi * that.
+  const uint64_t dbase = static_cast<uint64_t>(b0 / p.bsz) * (items > stride ? items : stride);
+  auto next_item = [&](uint64_t item) -> uint64_t {
+    if (p.item_ctr == nullptr) return item + stride;
+    if (tid == 0) s.dyn_item = atomicAdd(p.item_ctr, 1u);
+    __syncthreads();
+    const uint64_t d = static_cast<uint64_t>(s.dyn_item) - dbase + stride;
+    __syncthreads();
+    return d;
+  };
+  for (uint64_t item = blockIdx.x - first; blockIdx.x >= first; item = next_item(item)) {
+    if (item >= items) {
+      if (p.item_ctr == nullptr || item >= stride) break;  // a dynamic CTA without a first item still draws once
+      continue;
+    }
     const uint32_t c = static_cast<uint32_t>(item / nwb);
     const uint32_t wb = static_cast<uint32_t>(item % nwb);
     const uint32_t w = wb * MW + warp, j = w * 32u + lane;
@@ -613,7 +642,7 @@ __device__ void replay_merged_mw(const OnlineParams& p, const unsigned long long
       prefetch_next_batch(p, b0, static_cast<uint64_t>(blockIdx.x - first) * kStg + (tid - kThr),
                           static_cast<uint64_t>(stride) * kStg);
     }
-    const bool pr = p.prof != nullptr && blockIdx.x == first && tid == 0;
+    const bool pr = p.prof != nullptr && blockIdx.x == ((p.ablate & 128u) ? gridDim.x - 1u : first) && tid == 0;
     const unsigned long long q0 = pr ? gtimer() : 0ull;
     if (tid >= kThr) {
       load_chunk(0);
@@ -1099,10 +1128,18 @@ __global__ void __launch_bounds__(kOThreads, 2) online_persistent_kernel(OnlineP
     if (prof) t1 = gtimer();
     t2 = t1;
     if constexpr (MERGED) {
+      // profile: every CTA's own replay work time (p.prof[7 + CTA])
+      const unsigned long long r0 = p.prof != nullptr && threadIdx.x == 0 ? gtimer() : 0ull;
       if (p.mw == 4) {
         replay_merged_mw<4>(p, bestv, s, b0, n, par);
       } else {
         replay_merged<COLS>(p, bestv, s, b0, n, par);
+      }
+      if (p.prof != nullptr && threadIdx.x == 0) {
+        p.prof[7 + blockIdx.x] += gtimer() - r0;
+        uint32_t sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        p.prof[7 + 2048 + blockIdx.x] = sm;
       }
     } else {
       const uint64_t litems = static_cast<uint64_t>(p.C) * ((p.W + RTile<COLS>::kWords - 1) / RTile<COLS>::kWords);
@@ -1384,7 +1421,7 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   if (const char* ab = getenv("HVB200_ONLINE_ABLATE")) p.ablate = static_cast<uint32_t>(atoi(ab));  // timing only
   // HVB200_ONLINE_PROFILE=1: print the time per phase (CTA 0's view, barrier waits included)
   const char* pe = getenv("HVB200_ONLINE_PROFILE");
-  DevBuf<unsigned long long> prof(pe && pe[0] == '1' ? 7 : 0, st);
+  DevBuf<unsigned long long> prof(pe && pe[0] == '1' ? 7 + 4096 : 0, st);
   if (prof.ptr) {
     prof.zero();
     p.prof = prof.ptr;
@@ -1394,11 +1431,22 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
   DevBuf<uint32_t> pscr, arrive;
   unsigned grid_est = 0;
   if (merged) {
-    // narrow items: at most one CTA per SM. A cooperative grid larger than the
-    // SM count doubles up its lowest-numbered CTAs (blocks 0-11 on six SMs
-    // for 160 CTAs, measured); the few CTAs with two work units get a second
-    // item (with unbalanced classes, usually a rare-class one)
-    grid_est = cooperative_grid<true, 1>(ctx, mw == 4 ? std::min<uint64_t>(want, ctx->sm_count) : want);
+    // narrow items, batches of >= 1,024 rows: at most one CTA per SM. A
+    // cooperative grid larger than the SM count doubles up its lowest-numbered
+    // CTAs (blocks 0-11 on six SMs for 160 CTAs, measured) and two replays on
+    // one SM each run at ~2/3 of the rate; the items past the item CTAs are
+    // handed out dynamically (CHB-MIT batch 1,024: 18.3 -> 17.7 us, batch
+    // 8,192: 100.7 -> 80.9 us). Shorter batches keep every item on its own CTA
+    // (batch 256: 9.9 vs 11.0 us: one chunk per item, a second item doubles it).
+    const char* dyn = getenv("HVB200_ONLINE_DYNAMIC");  // =0: every item its own CTA, SMs doubled up (A/B)
+    const bool dyn_ok = !(dyn && dyn[0] == '0') && n >= 4u * kLChunk;
+    grid_est = cooperative_grid<true, 1>(ctx, mw == 4 && dyn_ok ? std::min<uint64_t>(want, ctx->sm_count) : want);
+    const uint64_t draws = ((rows + n - 1) / n) * std::max<uint64_t>(items, grid_est);  // 32-bit counter
+    if (mw == 4 && items + C > grid_est && draws < (1ull << 32) && dyn_ok) {
+      item_ctr = DevBuf<uint32_t>(1, st);
+      item_ctr.zero();
+      p.item_ctr = item_ctr.ptr;
+    }
   } else if (cols8) {
     grid_est = cooperative_grid<false, 8>(ctx, want);
   } else if (cols4) {
@@ -1456,7 +1504,7 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
       launch(kern, grid_est);  // parity 0 only: best[0, n) was reset by the previous launch
     }
   } else if (merged) {
-    launch(online_persistent_kernel<true, 1>, cooperative_grid<true, 1>(ctx, want));
+    launch(online_persistent_kernel<true, 1>, grid_est);
   } else if (cols8) {
     launch(online_persistent_kernel<false, 8>, cooperative_grid<false, 8>(ctx, want));
   } else if (cols4) {
@@ -1474,6 +1522,25 @@ void train_online_persistent(hv_context* ctx, cudaStream_t st, const uint32_t* e
             " [CTA 0 item: stage %.2f chunks %.2f weight-wait %.2f store %.2f]\n",
             merged ? "merged" : "lists", cols8 ? 8 : cols4 ? 4 : 1, p.ksplit, h[0] / nb / 1e3, h[1] / nb / 1e3,
             h[2] / nb / 1e3, h[3] / nb / 1e3, h[4] / nb / 1e3, h[5] / nb / 1e3, h[6] / nb / 1e3);
+    if (merged) {  // the slowest CTAs' own replay work (weight tasks are CTAs 0 .. C-1 when separate)
+      const unsigned g = grid_est;
+      std::vector<unsigned long long> ct(g);
+      ck(cudaMemcpy(ct.data(), prof.ptr + 7, g * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "D2H");
+      std::vector<unsigned> ord(g);
+      for (unsigned i = 0; i < g; ++i) ord[i] = i;
+      std::sort(ord.begin(), ord.end(), [&](unsigned a, unsigned b) { return ct[a] > ct[b]; });
+      std::vector<unsigned long long> smv(g);
+      ck(cudaMemcpy(smv.data(), prof.ptr + 7 + 2048, g * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "D2H");
+      std::vector<int> per(1024, 0);
+      for (unsigned i = 0; i < g; ++i) per[smv[i] & 1023]++;
+      int shared = 0;
+      for (int v : per) shared += v > 1 ? v : 0;
+      fprintf(stderr, "online replay: %d of %u CTAs share an SM; work per CTA (us/batch), slowest:", shared, g);
+      for (unsigned i = 0; i < std::min(g, 10u); ++i)
+        fprintf(stderr, " %u(sm%llu,%d):%.2f", ord[i], smv[ord[i]], per[smv[ord[i]] & 1023], ct[ord[i]] / nb / 1e3);
+      fprintf(stderr, " | CTA 0: %.2f, CTA 1: %.2f, median %.2f\n", ct[0] / nb / 1e3, g > 1 ? ct[1] / nb / 1e3 : 0.0,
+              ct[ord[g / 2]] / nb / 1e3);
+    }
     if (!merged) {  // the last batch's per-class list lengths
       std::vector<uint32_t> len(C);
       ck(cudaMemcpy(len.data(), llen.ptr, C * sizeof(uint32_t), cudaMemcpyDeviceToHost), "D2H llen");

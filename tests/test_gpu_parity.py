@@ -364,6 +364,27 @@ def test_online_modes_vs_oracle_bitexact(C, D, n, bsz):
     np.testing.assert_array_equal(on.class_vectors.words, oo.class_vectors)
 
 
+@pytest.mark.parametrize("bsz,p1,dyn", [(1024, 0.01, "1"), (2048, 0.3, "1"), (1024, 0.01, "0"), (256, 0.01, "1")])
+def test_online_two_class_dynamic_items_vs_oracle_bitexact(bsz, p1, dyn, monkeypatch):
+    """Two classes at D = 10,000: 158 narrow replay items on at most one CTA
+    per SM, the items past the item CTAs drawn dynamically (batches >= 1,024
+    rows), and class-weight tasks that skip groups without true samples — an
+    unbalanced (CHB-MIT-like) and a balanced label mix, against the oracle."""
+    monkeypatch.setenv("HVB200_ONLINE_DYNAMIC", dyn)
+    rng = np.random.default_rng(int(p1 * 1000) + bsz)
+    C, D, n = 2, 10000, 5000
+    centers = rng.integers(0, 2, (C, D), dtype=np.uint8)
+    y = (rng.random(n) < p1).astype(np.int32)
+    enc = O.pack_rows(centers[y] ^ (rng.random((n, D)) < 0.4).astype(np.uint8))
+    cfg = hv.ModelConfig(class_count=C, dim=D, gamma=0.6, seed=77)
+    on = hv.train_online(P(enc, D), y, bsz, cfg)
+    oo = O.NaiveModel(C, D, on.tiebreak.words, O.HAMMING, 0.6).train_online(enc, y, bsz)
+    np.testing.assert_array_equal(on.accumulators.reshape(C, D), oo.acc)
+    np.testing.assert_array_equal(on.class_weight, oo.weight)
+    np.testing.assert_array_equal(on.sample_counts, oo.counts)
+    np.testing.assert_array_equal(on.class_vectors.words, oo.class_vectors)
+
+
 @pytest.mark.parametrize("C,D,n,bsz", [(1, 100, 50, 1), (2, 10000, 300, 1), (6, 10000, 400, 5), (6, 1000, 257, 16),
                                         (26, 2048, 200, 7), (32, 333, 130, 64), (3, 31, 90, 4), (13, 8192, 100, 33),
                                         (6, 20000, 120, 2)])
