@@ -644,9 +644,13 @@ __device__ void replay_merged_mw(const OnlineParams& p, const unsigned long long
     }
     const bool pr = p.prof != nullptr && blockIdx.x == ((p.ablate & 128u) ? gridDim.x - 1u : first) && tid == 0;
     const unsigned long long q0 = pr ? gtimer() : 0ull;
+    // staging runs a chunk ahead of the replay and its raw loads two ahead:
+    // chunk k + 2's loads are issued right after chunk k + 1 is stored, so an
+    // L2 round trip hides behind a whole chunk's replay
     if (tid >= kThr) {
       load_chunk(0);
       store_chunk(0);
+      if (kRows < n) load_chunk(kRows);
     }
     __syncthreads();
     const unsigned long long q1 = pr ? gtimer() : 0ull;
@@ -686,7 +690,6 @@ __device__ void replay_merged_mw(const OnlineParams& p, const unsigned long long
           }
         }
       } else {
-        if (more && !(p.ablate & 1u)) load_chunk(ch + kRows);
         if (tid == kOThreads - 32 && !sep) {  // lane 0 of the last warp: the class weight chain
 #pragma unroll 8
           for (uint32_t k = 0; k < m; ++k) {
@@ -696,6 +699,7 @@ __device__ void replay_merged_mw(const OnlineParams& p, const unsigned long long
           }
         }
         if (more && !(p.ablate & 4u)) store_chunk(buf ^ 1u);  // the other buffer was last read before the previous barrier
+        if (ch + 2u * kRows < n && !(p.ablate & 1u)) load_chunk(ch + 2u * kRows);
       }
       __syncthreads();
     }
