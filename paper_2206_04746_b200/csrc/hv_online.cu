@@ -1048,7 +1048,19 @@ __device__ void replay_lists(const OnlineParams& p, Smem& s, uint64_t b0, uint32
     const uint32_t* li = p.lidx + static_cast<uint64_t>(c) * p.bsz;
     const double* lv = p.lval + static_cast<uint64_t>(c) * p.bsz;
     uint32_t rw[kLoadsPer];
+    uint32_t ri[kLoadsPer];  // list entries (row indices) of the next chunk's gathers, loaded a chunk ahead
     double rv = 0.0;
+    auto load_idx = [&](uint32_t k0) {
+      const uint32_t m = min(static_cast<uint32_t>(RTile<COLS>::kChunk), len - k0);
+#pragma unroll
+      for (int i = 0; i < kLoadsPer; ++i) {
+        const uint32_t k = (tid + i * kOThreads) / RTile<COLS>::kWords;
+        ri[i] = k < m ? li[k0 + k] : 0u;
+      }
+    };
+    // the row gathers take their addresses from ri: the list-index round trip
+    // is not in front of every chunk's loads (Large: ~180 list entries per
+    // class, 6 chunks of 32 per item)
     auto load_chunk = [&](uint32_t k0) {
       const uint32_t m = min(static_cast<uint32_t>(RTile<COLS>::kChunk), len - k0);
       if (tid < m) rv = lv[k0 + tid];
@@ -1057,7 +1069,7 @@ __device__ void replay_lists(const OnlineParams& p, Smem& s, uint64_t b0, uint32
         const uint32_t e = tid + i * kOThreads;
         const uint32_t k = e / RTile<COLS>::kWords, ww = e % RTile<COLS>::kWords;
         const uint32_t w = wb * RTile<COLS>::kWords + ww;
-        rw[i] = (k < m && w < p.W) ? __ldg(p.enc + (b0 + li[k0 + k]) * p.W + w) : 0u;
+        rw[i] = (k < m && w < p.W) ? __ldg(p.enc + (b0 + ri[i]) * p.W + w) : 0u;
       }
     };
     auto store_chunk = [&](uint32_t buf) {
@@ -1069,14 +1081,19 @@ __device__ void replay_lists(const OnlineParams& p, Smem& s, uint64_t b0, uint32
         if (k < RTile<COLS>::kChunk) s.words[buf][staged_word<COLS>(k, ww)] = rw[i];
       }
     };
+    load_idx(0);
     load_chunk(0);
+    if (RTile<COLS>::kChunk < len) load_idx(RTile<COLS>::kChunk);
     store_chunk(0);
     __syncthreads();
     const unsigned long long q1 = pr ? gtimer() : 0ull;
     uint32_t buf = 0;
     for (uint32_t k0 = 0; k0 < len; k0 += RTile<COLS>::kChunk, buf ^= 1u) {
       const bool more = k0 + RTile<COLS>::kChunk < len;
-      if (more) load_chunk(k0 + RTile<COLS>::kChunk);
+      if (more) {
+        load_chunk(k0 + RTile<COLS>::kChunk);
+        if (k0 + 2u * RTile<COLS>::kChunk < len) load_idx(k0 + 2u * RTile<COLS>::kChunk);
+      }
       const uint32_t m = min(static_cast<uint32_t>(RTile<COLS>::kChunk), len - k0);
       if (tid < kOReplay) replay_chunk<COLS>(s.words[buf], s.val[buf], m, a);
       if (more) store_chunk(buf ^ 1u);
