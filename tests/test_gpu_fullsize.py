@@ -9,7 +9,7 @@ D = 32768, 100 classes) through properties the oracle can check in seconds:
   majority_binarize of those counts with the model tiebreak;
 * the predictions (labels and fp64 distances) of sampled test rows must equal
   the oracle's predict against the same class vectors;
-* online training of a 32-batch prefix is bit-exact against the oracle.
+* online training of a 256-batch prefix is bit-exact against the oracle.
 
 These are the bench workloads themselves, not scaled-down stand-ins."""
 import numpy as np
@@ -106,8 +106,8 @@ def test_chbmit_full_size_encode_train_predict_online():
     _check_sampled_encodes(eng, cbk, bins8, enc, _sample(N, 40, 1), C, 1, 9)
     ntr = N * 4 // 5
     _check_classical_and_predict(eng, cbk, enc, labels, ntr, C, _sample(N - ntr, 3000, 2))
-    # online: a 32-batch prefix bit-exact against the oracle
-    pre = 32 * 1024
+    # online: a 256-batch prefix (262,144 rows) bit-exact against the oracle
+    pre = 256 * 1024
     acc, weight, counts, cv = eng.train_online(enc[:pre], labels[:pre], 1024)
     om = O.NaiveModel(C, D, _u32(cbk.model_tiebreak)).train_online(_u32(enc[:pre]), labels[:pre].cpu().numpy(), 1024)
     assert torch.equal(acc.cpu(), torch.from_numpy(om.acc))
@@ -134,7 +134,7 @@ def test_chbmit_full_size_online_two_exact_paths_agree():
     trainer and the word-sliced multi-GPU mode with 2 ranks emulated on this
     GPU (different kernels: slice init, partial popcounts summed across ranks,
     slice update) — must give bit-identical fp64 accumulators, weights, counts
-    and class vectors (model.cpp:250-301). The 32-batch prefix is pinned
+    and class vectors (model.cpp:250-301). The 256-batch prefix is pinned
     against the oracle in the test above."""
     N, F, B, D, C = 7_060_000, 342, 16, 10000, 2
     ntr = N * 4 // 5
