@@ -189,8 +189,8 @@ __device__ void score_warp_per_row(const OnlineParams& p, unsigned long long* be
   // every class's word of a step in flight together (per batch of 1,024:
   // UCI-HAR C = 6 18.4 -> 16.2 us, MNIST C = 10 D = 10000 29.8 -> 26.7 us);
   // rows of a multiple of 32 words keep the per-class passes (MNIST D = 8192
-  // 23.4 vs 24.2, D = 16384 33.0 vs 34.9 us), and so do two classes (CHB-MIT:
-  // 18.2 vs 20.5 us with this path)
+  // 23.4 vs 24.2, D = 16384 33.0 vs 34.9 us); two classes have their own
+  // all-words-in-flight loop below (CHB-MIT: this path was 20.5 vs 18.2 us)
   const bool ragged = (p.W & 31u) != 0 && !(p.ablate & 64u);
   if (p.C >= 3 && p.C <= 8 && p.W > 64 && ragged) {
     score_rows_all_classes<8>(p, best_out, b0, n, gwarp, gwarps, lane);
@@ -229,6 +229,37 @@ __device__ void score_warp_per_row(const OnlineParams& p, unsigned long long* be
       if (lane == 0) {
         best_out[r] = (static_cast<unsigned long long>(bestp) << 32) | best;
         p.truep[r] = truep;
+      }
+    }
+    return;
+  }
+  if (p.C == 2 && p.W <= 32u * 10u && !(p.ablate & 4096u)) {
+    // two classes (CHB-MIT W = 313): the row's and both class vectors' words
+    // of every step loaded up front, one L2 round trip per row
+    for (uint64_t r = gwarp; r < n; r += gwarps) {
+      const uint32_t* q = p.enc + (b0 + r) * p.W;
+      const int32_t y = p.labels[b0 + r];
+      uint32_t x[10], v0[10], v1[10];
+#pragma unroll
+      for (int i = 0; i < 10; ++i) {
+        const uint32_t w = lane + 32u * i;
+        const bool ok = w < p.W;
+        x[i] = ok ? __ldg(q + w) : 0u;
+        v0[i] = ok ? p.cv[w] : 0u;
+        v1[i] = ok ? p.cv[p.W + w] : 0u;
+      }
+      uint32_t a0 = 0, a1 = 0;
+#pragma unroll
+      for (int i = 0; i < 10; ++i) {
+        a0 += __popc(x[i] ^ v0[i]);
+        a1 += __popc(x[i] ^ v1[i]);
+      }
+      a0 = __reduce_add_sync(kFull, a0);
+      a1 = __reduce_add_sync(kFull, a1);
+      if (lane == 0) {
+        const uint32_t best = a1 < a0 ? 1u : 0u;  // strict: class 0 wins ties (model.cpp:96-104)
+        best_out[r] = (static_cast<unsigned long long>(best ? a1 : a0) << 32) | best;
+        p.truep[r] = y == 1 ? a1 : (y == 0 ? a0 : 0u);
       }
     }
     return;
