@@ -346,7 +346,8 @@ def test_online_random_vs_oracle_bitexact(bsz):
                                        (26, 2048, 800, 100), (32, 777, 500, 128), (100, 4096, 600, 512),
                                        (40, 64, 300, 1), (3, 70, 257, 256), (6, 10000, 2100, 1024), (6, 2000, 300, 32),
                                        (100, 1500, 400, 7), (64, 10000, 700, 256), (130, 3000, 500, 128),
-                                       (100, 4096, 600, 100)])
+                                       (100, 4096, 600, 100), (2, 5000, 900, 300), (2, 10240, 700, 256),
+                                       (2, 10272, 600, 128)])
 def test_online_modes_vs_oracle_bitexact(C, D, n, bsz):
     """Every path of the persistent online trainer against the oracle:
     MERGED (C <= 2), LISTS with warp-per-row scoring (2 < C < 32) and with
